@@ -1,0 +1,425 @@
+#!/usr/bin/env python
+"""Benchmark: schedule evaluations/sec & SLO attainment at a 10 ms budget, 1024 requests.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python -m torch.distributed.run --nnodes=1 --nproc-per-node N --master-addr 127.0.0.1 \
+        --master-port P bench.py --gpus N ...
+
+Workload (BASELINE.json configs[2]): 1024-request ShareGPT-shaped synthetic queue
+(generate_mixed(1024, seed 0), estimator-predicted output lengths -- the reference CLI's
+pipeline), max batch 4, 16384 annealing chains per GPU, a 10 ms scheduling budget.
+A "step" is one scheduling decision: every chain anneals from the best start candidate,
+the grid argmax picks the best chain, and (N > 1) one all-gather + broadcast over NCCL
+picks the best GPU. Chains shard across GPUs (chain ids rank*16384 ...), so per-GPU work
+is fixed as N grows ("weak").
+
+value  = proposals evaluated by all ranks / max-over-ranks device time (CUDA events on the
+         engine's stream around the kernel launches; inputs resident in HBM).
+e2e    = same metric through the public C-ABI call slosched_anneal() from host arrays
+         (host setup, H2D, kernel, argmax, D2H and final evaluation inside the timed region).
+--impl reference: the reference's own CPU anneal() (oracle/_ref, the unmodified reference
+         compiled here) on all host cores, one chain per thread, on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+N_REQ, MAX_BATCH, SEED = 1024, 4, 0
+METRIC = "schedule evaluations/sec & SLO attainment @10 ms budget, 1024 reqs, 1/2/4/8 B200"
+UNIT = "evals/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=N_REQ)
+    ap.add_argument("--mb", type=int, default=MAX_BATCH)
+    ap.add_argument("--chains", type=int, default=16384, help="chains per GPU")
+    ap.add_argument("--budget-ms", type=float, default=10.0, help="scheduling budget per step")
+    ap.add_argument("--t0", type=float, default=500.0)
+    ap.add_argument("--t-thres", type=float, default=20.0)
+    ap.add_argument("--tau", type=float, default=0.7)
+    ap.add_argument("--iter", type=int, default=60)
+    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-sample-s", type=float, default=10.0)
+    return ap.parse_args()
+
+
+# per-chain objective_scale multipliers: the reference default (x1) walks randomly at N=1024
+# (SURVEY 6.3); larger factors make greedier chains. Chain c uses ladder[c % len].
+SCALE_LADDER = (1.0, 10.0, 100.0, 1000.0, 1e4, 1e5)
+
+
+# ---------------------------------------------------------------- helpers
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device, self.lines, self.proc = device, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) != 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def synthetic_workload(n):
+    import paper_2504_14966_b200 as S
+    return S.generate_mixed(n, SEED)  # generate_mixed + estimator cold start, as the reference CLI
+
+
+def flat_of(w):
+    from oracle import FlatWorkload
+    a = w.arrays
+    return FlatWorkload(**{k: a[k] for k in ("id", "cls", "in_len", "true_out", "pred_out", "arrival", "class_id",
+                                           "kind", "e2e", "ttft", "tpot")})
+
+
+def cpu_reference_run(w, mb, threads, target_s, reps=None):
+    """The reference anneal() (default AnnealConfig) on `threads` host threads, one chain each."""
+    from oracle import TABLE_COEFFS, ref
+    fw = flat_of(w)
+    ids = list(w.ids())
+    if ref.available():
+        kind = "reference"
+        probe = ref.anneal_parallel(fw, TABLE_COEFFS, ids, mb, threads=1, reps=1)
+        if reps is None:
+            per_round_s = probe["wall_ms"] / 1e3
+            reps = max(1, int(target_s / max(per_round_s, 1e-4)))
+        r = ref.anneal_parallel(fw, TABLE_COEFFS, ids, mb, threads=threads, reps=reps, seed0=1)
+        return kind, reps, r["proposals"], r["wall_ms"], r["best_n"], r["best_g"]
+    # oracle/_ref missing: the C restatement, threads via ctypes (releases the GIL)
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import port
+    kind = "port"
+    reps = reps or 1
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        outs = list(ex.map(lambda s: port.anneal(fw, TABLE_COEFFS, ids, mb, seed=s), range(threads * reps)))
+    wall = (time.perf_counter() - t0) * 1e3
+    best = max(outs, key=lambda o: o["g"])
+    return kind, reps, float(sum(o["proposals"] for o in outs)), wall, best["n"], best["g"]
+
+
+def lscpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    w = synthetic_workload(args.n)
+    threads = os.cpu_count() or 1
+    for _ in range(args.warmup):
+        cpu_reference_run(w, args.mb, threads, 0.0, reps=1)
+    props, wall, best_n, best_g = 0.0, 0.0, 0, 0.0
+    for _ in range(args.steps):
+        kind, _, p, wl, bn, bg = cpu_reference_run(w, args.mb, threads, 0.0, reps=1)
+        props += p
+        wall += wl
+        if bg > best_g:
+            best_n, best_g = bn, bg
+    value = props / (wall / 1e3)
+    sample = (f"{args.steps} steps x {threads} threads x 1 reference anneal() (default AnnealConfig: 63 levels x 100 "
+              f"= 6300 proposals per chain) on N={args.n}, mb={args.mb}; host {lscpu_model()}")
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"generate_mixed({args.n}, seed {SEED}) + estimator lengths, max_batch {args.mb}, "
+                               f"reference CPU anneal, one chain per host thread", "n_requests": args.n,
+                   "max_batch": args.mb, "threads": threads},
+        "attainment": best_n / args.n, "g_req_per_ms": best_g,
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import numpy as np
+    import torch
+
+    import paper_2504_14966_b200 as S
+    from paper_2504_14966_b200 import engine as E
+
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    w = synthetic_workload(args.n)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    n, mb = len(ids), args.mb
+    chains_total = args.chains * world
+    cb, ce = rank * args.chains, (rank + 1) * args.chains
+
+    # host setup exactly as anneal() does it: candidates, start, default scale, tables
+    s_sched, i_sched = S.initial_candidates(w, ids, c, mb)
+    ev_s, ev_i = S.evaluate(s_sched, c, w), S.evaluate(i_sched, c, w)
+    start = s_sched if ev_s.g >= ev_i.g else i_sched
+    f0 = max(ev_s.g, ev_i.g)
+    scale = args.t0 / f0 if f0 > 0 else args.t0
+    pos = {rid: k for k, rid in enumerate(ids)}
+    start_perm = [pos[x] for x in start.flatten()]
+    start_sizes = [len(b) for b in start.batches]
+
+    eng = E.Engine(local)
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    smem_peak_gbs = None
+    try:
+        smem_peak_gbs = eng_probe(eng)
+    except Exception:
+        pass
+    kernel_budget_ms = max(0.0, args.budget_ms - 0.5)  # leave room for argmax + copies
+    eng.prepare(start_perm, start_sizes, t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
+                objective_scale=scale, chains=chains_total, chain_begin=cb, chain_end=ce,
+                budget_ms=kernel_budget_ms, scale_ladder=SCALE_LADDER)
+    stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
+    flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
+
+    def exchange(res):
+        """best-of-GPUs: all-gather (g, t, chain) and broadcast the winner's schedule."""
+        if world == 1:
+            return res.g, res.chain
+        rec = torch.tensor([res.g, res.t, float(res.chain)], dtype=torch.float64, device=f"cuda:{local}")
+        allrec = torch.empty(world, 3, dtype=torch.float64, device=f"cuda:{local}")
+        dist.all_gather_into_tensor(allrec, rec)
+        a = allrec.cpu().numpy()
+        win = max(range(world), key=lambda r_: (a[r_, 0], -a[r_, 1], -a[r_, 2]))
+        perm = torch.zeros(n, dtype=torch.int32, device=f"cuda:{local}")
+        dist.broadcast(perm, src=win)
+        return a[win, 0], int(a[win, 2])
+
+    def step():
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush between steps (outside the events)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.launch()
+        e1.record(stream)
+        bp, bs, res = eng.fetch()
+        exchange(res)
+        return e0, e1, res
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    events, results = [], []
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        t_wall = time.perf_counter()
+        for _ in range(args.steps):
+            e0, e1, res = step()
+            events.append((e0, e1))
+            results.append((res.proposals, res.kernel_ms, res.positions_pass1, res.positions_pass2, res.g, res.n_met,
+                            res.levels_run, res.chains_run))
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        wall_s = time.perf_counter() - t_wall
+    dev_ms = sum(a.elapsed_time(b) for a, b in events)
+    props = float(sum(r[0] for r in results))
+    kern_ms = sum(r[1] for r in results)
+    pos1 = float(sum(r[2] for r in results))
+    pos2 = float(sum(r[3] for r in results))
+    if dist:
+        t = torch.tensor([dev_ms, props, kern_ms, pos1, pos2], dtype=torch.float64, device=f"cuda:{local}")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        dev_ms_max, props_all = float(mx[0]), float(t[1])
+    else:
+        dev_ms_max, props_all = dev_ms, props
+    value = props_all / (dev_ms_max / 1e3)
+
+    # ---- e2e: the public C-ABI call from host arrays, per step (+ the cross-GPU exchange)
+    cfg = S.AnnealConfig(t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
+                         chains=chains_total, chain_begin=cb, chain_end=ce, budget_ms=kernel_budget_ms,
+                         scale_ladder=SCALE_LADDER, device=local)
+    S.anneal_flat(w, ids, c, cfg, mb)  # warm the context pool
+    e2e_props, e2e_s, final = 0.0, 0.0, None
+    if dist:
+        dist.barrier()
+    for _ in range(args.e2e_steps):
+        t0 = time.perf_counter()
+        seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids, c, cfg, mb)
+        if dist:
+            rec = torch.tensor([g, t_ms, float(n_met)], dtype=torch.float64, device=f"cuda:{local}")
+            allrec = torch.empty(world, 3, dtype=torch.float64, device=f"cuda:{local}")
+            dist.all_gather_into_tensor(allrec, rec)
+            a = allrec.cpu().numpy()
+            win = max(range(world), key=lambda r_: (a[r_, 0], -a[r_, 1], -r_))
+            buf = torch.from_numpy(np.ascontiguousarray(seq)).to(f"cuda:{local}")
+            dist.broadcast(buf, src=win)
+            g, n_met = float(a[win, 0]), int(a[win, 2])
+        e2e_s += time.perf_counter() - t0
+        e2e_props += st.proposals
+        final = (n_met, g, st)
+    if dist:
+        t = torch.tensor([e2e_s, e2e_props], dtype=torch.float64, device=f"cuda:{local}")
+        mx = t.clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        e2e_s, e2e_props = float(mx[0]), float(t[1])
+    e2e_value = e2e_props / e2e_s
+    P = 1
+    while 32 * P < n:
+        P *= 2
+    h2d = 2 * 8 * n * mb + 64 * P + 4 * P + 8 * len(SCALE_LADDER)  # tables + start state + scale ladder
+    d2h = 64 * P + 4 * P + 64                                       # winner entries + bits + result record
+
+    if rank != 0:
+        if dist:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (k_chains): bytes the incremental evaluator walks
+    # per position: pass 1 = 2 B entry + 8 B exec, pass 2 = 2 B entry + 16 B (exec, deadline)
+    alg_bytes = 10.0 * pos1 + 18.0 * pos2
+    achieved_gbs = alg_bytes / (kern_ms / 1e3) / 1e9
+    roof = {"bound": "smem", "achieved": achieved_gbs, "peak": smem_peak_gbs, "unit": "GB/s",
+            "frac": (achieved_gbs / smem_peak_gbs) if smem_peak_gbs else None, "traffic": None,
+            "peak_source": "measured in-process: slo_probe_smem_bandwidth (conflict-free LDS.128 on all SMs); "
+                           "MEASURED_PEAKS.json has no shared-memory figure",
+            "kernel": "k_chains", "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
+            "bytes_per_launch": alg_bytes / args.steps,
+            "positions_per_proposal": (pos1 + pos2) / props if props else None}
+    attain_n, attain_g, st = final
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        threads = os.cpu_count() or 1
+        kind, reps, cp, cw, cn, cg = cpu_reference_run(w, mb, threads, args.cpu_sample_s / max(threads, 1))
+        cpu = {"value": cp / (cw / 1e3), "unit": UNIT, "cores": threads, "kind": kind,
+               "sample": f"{threads} threads x {reps} reference anneal() calls (default AnnealConfig, 6300 "
+                         f"proposals each) on the same N={n} mb={mb} workload; {cw / 1e3:.1f} s wall; "
+                         f"host {lscpu_model()}",
+               "attainment": cn / n, "g_req_per_ms": cg}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"configs[2]: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
+                               f"predictions, {args.chains} chains/GPU, {args.budget_ms} ms budget",
+                   "n_requests": n, "max_batch": mb, "chains_per_gpu": args.chains, "chains_total": chains_total,
+                   "budget_ms": args.budget_ms, "kernel_budget_ms": kernel_budget_ms,
+                   "ladder": {"t0": args.t0, "t_thres": args.t_thres, "tau": args.tau, "iter": args.iter},
+                   "scale_ladder": list(SCALE_LADDER), "l2": "flushed between steps (512 MiB write)",
+                   "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather argmax"},
+        "attainment": attain_n / n, "g_req_per_ms": attain_g,
+        "attainment_start": max(ev_s.n, ev_i.n) / n,
+        "levels_run": int(min(r[6] for r in results)), "chains_run": int(min(r[7] for r in results)),
+        "wall_s_timed": wall_s,
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "ms_per_call": 1e3 * e2e_s / args.e2e_steps, "api": "slosched_anneal (include/slosched_api.h)"},
+        "gpu_launches": 2 * args.steps,
+        "roofline": roof,
+        "clocks": clocks.summary(),
+        "cpu_baseline": cpu,
+    }
+    print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+def eng_probe(eng):
+    import ctypes
+
+    from paper_2504_14966_b200._lib import lib
+    from paper_2504_14966_b200.slosched import _check_engine
+    v = ctypes.c_double()
+    _check_engine(lib().slo_probe_smem_bandwidth(eng._ctx, ctypes.byref(v)))
+    return v.value
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

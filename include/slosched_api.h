@@ -1,0 +1,98 @@
+/* slosched_api.h -- flat C ABI of the scheduler entry points (include/slosched_b200.hpp)
+ * for FFI callers (the Python package binds it with ctypes; a cgo/JNI binding would bind
+ * the same symbols). Arrays in, arrays out; caller-owned buffers; int status return
+ * (slo_status codes of slosched_gpu.h) with the message in slosched_last_error().
+ *
+ * Reference interface each function replaces (P: = /root/reference/proj/):
+ *   slosched_anneal              anneal()              P:include/slosched/priority_mapper.hpp:67-69
+ *   slosched_evaluate            evaluate()            P:include/slosched/objective.hpp:36-38
+ *   slosched_initial_candidates  initial_candidates()  P:include/slosched/priority_mapper.hpp:46-49
+ *   slosched_neighbor_walk       neighbor() x steps    P:include/slosched/priority_mapper.hpp:61
+ *   slosched_schedule_all        schedule_all()        P:include/slosched/scheduler.hpp:54-59
+ *   slosched_predict             predict_*()           P:include/slosched/latency_model.hpp:43-47
+ *   slosched_generate_mixed      generate_mixed() + estimator cold start
+ *                                                      P:include/slosched/workload.hpp:48-52
+ *   slosched_build_tables        CostModel tables      P:src/priority_mapper.cpp:205-231
+ */
+#ifndef SLOSCHED_API_H
+#define SLOSCHED_API_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Requests (pred_out < 0: no prediction) and SLO classes (kind 0 = E2E, 1 = TTFT_TPOT). */
+typedef struct {
+    int32_t n;
+    const int32_t *id, *cls, *in_len, *true_out, *pred_out;
+    const double* arrival;
+    int32_t n_classes;
+    const int32_t *class_id, *kind;
+    const double *e2e, *ttft, *tpot;
+} slosched_workload;
+
+typedef struct {
+    double t0, t_thres;
+    int32_t iter;
+    double tau;
+    uint64_t seed;
+    int32_t has_objective_scale;
+    double objective_scale;
+    int32_t mode;           /* 0 = GPU chains (Philox), 1 = exact replay of the reference walk */
+    int32_t chains;
+    double budget_ms;
+    int32_t n_scale_ladder;
+    const double* scale_ladder;
+    int32_t device;         /* -1 = SLOSCHED_DEVICE or 0 */
+    int32_t chain_begin, chain_end; /* chain_end < 0: all chains */
+} slosched_anneal_config;
+
+typedef struct {
+    uint64_t proposals, accepted;
+    int32_t shortcut;
+    double g_sorted_start, g_input_start, objective_scale_used;
+    int32_t chains_run, levels_run, best_chain;
+    double engine_g, kernel_ms;
+} slosched_anneal_stats;
+
+const char* slosched_last_error(void);
+
+int slosched_predict(const double* coeffs8, int32_t b, int32_t input_len, int32_t output_len, double* out5);
+double slosched_latest_start(double slo, double cost);
+
+int slosched_generate_mixed(int32_t n, uint64_t seed, int32_t predict_mode, int32_t* id, int32_t* cls,
+                            int32_t* in_len, int32_t* true_out, int32_t* pred_out, double* arrival);
+
+int slosched_evaluate(const slosched_workload* w, const double* coeffs8, const int32_t* ids, const int32_t* sizes,
+                      int32_t nb, int32_t* n_met, double* t, double* g, double* wait, double* exec, double* e2e,
+                      double* ttft, double* tpot, int32_t* met, int32_t* extrapolated);
+
+int slosched_initial_candidates(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
+                                int32_t max_batch, int32_t* sorted_ids, int32_t* sorted_sizes, int32_t* sorted_nb,
+                                int32_t* input_ids, int32_t* input_sizes, int32_t* input_nb);
+
+int slosched_neighbor_walk(const int32_t* ids, const int32_t* sizes, int32_t nb, uint64_t seed, int32_t steps,
+                           int32_t max_batch, int32_t* out_ids, int32_t* out_sizes, int32_t* out_nb);
+
+int slosched_anneal(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
+                    const slosched_anneal_config* cfg, int32_t max_batch, int32_t* out_ids, int32_t* out_sizes,
+                    int32_t* out_nb, int32_t* n_met, double* t, double* g, slosched_anneal_stats* stats);
+
+/* Instances as arrays; per-instance outputs concatenated in instance order. */
+int slosched_schedule_all(const slosched_workload* w, const double* coeffs8, int32_t n_inst, const int32_t* inst_id,
+                          const double* total_mem, const double* remaining_mem, const double* mu, const double* sigma,
+                          const int32_t* inst_max_batch, const slosched_anneal_config* cfg, int32_t* out_ids,
+                          int32_t* out_sizes, int32_t* inst_nb, int32_t* inst_count, int32_t* inst_n,
+                          double* inst_t, double* inst_g, int32_t* epochs, double* overhead_ms);
+
+/* exec[(b-1)*n + i], deadline[(b-1)*n + i] for dense index i = rank of ids[i] among ids. */
+int slosched_build_tables(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
+                          int32_t max_batch, double* exec, double* deadline);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

@@ -1,0 +1,289 @@
+// slosched_b200.hpp -- C++ entry points of the B200 SLO-aware scheduler.
+//
+// Drop-in for the reference's scheduling path: the same namespace, type names, member
+// names and function signatures as the reference headers (P: = /root/reference/proj/):
+//   domain types            P:include/slosched/core.hpp:15-170
+//   Rng                     P:include/slosched/rng.hpp:14-100
+//   latency model           P:include/slosched/latency_model.hpp:41-59
+//   objective               P:include/slosched/objective.hpp:13-38
+//   priority mapper         P:include/slosched/priority_mapper.hpp:16-82
+//   scheduler               P:include/slosched/scheduler.hpp:16-59
+//   synthetic workload      P:include/slosched/workload.hpp:23-55 (generator subset)
+//   estimator (cold start)  P:include/slosched/output_estimator.hpp:10-56 (subset)
+// so code written against slosched::anneal / schedule_all / evaluate compiles against
+// this header and runs the annealing loop on the GPU (include/slosched_gpu.h).
+//
+// Extensions (all defaulted so reference call sites are unchanged) live in
+// AnnealConfig::engine and AnnealStats; see DESIGN.md.
+#ifndef SLOSCHED_B200_HPP
+#define SLOSCHED_B200_HPP
+
+#include <cstdint>
+#include <deque>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <utility>
+#include <variant>
+#include <vector>
+
+namespace slosched {
+
+// ---------------------------------------------------------------- errors
+class DataError : public std::runtime_error {
+public:
+    explicit DataError(const std::string& w) : std::runtime_error(w) {}
+};
+class CapacityError : public std::runtime_error {
+public:
+    explicit CapacityError(const std::string& w) : std::runtime_error(w) {}
+};
+// CUDA / engine failures: there is no CPU fallback.
+class EngineError : public std::runtime_error {
+public:
+    explicit EngineError(const std::string& w) : std::runtime_error(w) {}
+};
+
+// ---------------------------------------------------------------- domain
+enum class SloKind { E2E, TTFT_TPOT };
+
+struct SloSpec {
+    SloKind kind = SloKind::E2E;
+    std::optional<double> e2e_ms, ttft_ms, tpot_ms;
+    static SloSpec e2e(double ms);
+    static SloSpec ttft_tpot(double ttft_ms, double tpot_ms);
+    void validate() const;
+};
+
+struct GaussianPrior {
+    double mean_tokens = 0.0, std_tokens = 0.0;
+};
+struct RangePrior {
+    int low = 1, high = 1;
+};
+using OutputPrior = std::variant<std::monostate, GaussianPrior, RangePrior>;
+
+struct TaskClass {
+    int id = 0;
+    std::string name;
+    SloSpec slo;
+    OutputPrior output_prior;
+    void validate() const;
+};
+
+struct Request {
+    int id = 0;
+    int task_class_id = 0;
+    int input_len = 1;
+    int true_output_len = 1;
+    std::optional<int> predicted_output_len;
+    double arrival_time_ms = 0.0;
+    void validate() const;
+};
+
+struct LatencyCoefficients {
+    double alpha_p = 0.0, beta_p = 0.0, gamma_p = 0.0, delta_p = 0.0;
+    double alpha_d = 0.0, beta_d = 0.0, gamma_d = 0.0, delta_d = 0.0;
+    void validate() const;
+};
+
+using Batch = std::vector<int>;
+
+struct Schedule {
+    std::vector<Batch> batches;
+    std::size_t request_count() const;
+    std::vector<int> flatten() const;
+    std::unordered_map<int, std::pair<int, int>> positions() const;
+    bool is_partition_of(const std::vector<int>& ids, int max_batch) const;
+};
+
+struct InstanceState {
+    int id = 0;
+    std::uint64_t total_mem = 0, remaining_mem = 0;
+    double mem_utility = 0.9, bytes_per_token = 1.0;
+    int max_batch_size = 1;
+    void validate() const;
+};
+
+struct RequestMetrics {
+    int request_id = 0;
+    double wait_ms = 0.0, exec_ms = 0.0, e2e_ms = 0.0, ttft_ms = 0.0, tpot_ms = 0.0;
+    bool slo_met = false;
+    bool extrapolated = false;
+};
+
+struct EvaluatedSchedule {
+    Schedule schedule;
+    std::vector<RequestMetrics> per_request;
+    int n = 0;
+    double t_ms = 0.0;
+    double g = 0.0;
+};
+
+struct Workload {
+    std::vector<TaskClass> classes;
+    std::vector<Request> requests;
+    const TaskClass& class_of(const Request& r) const;
+    const TaskClass* find_class(int class_id) const;
+    const Request* find_request(int request_id) const;
+
+private:
+    friend Workload validate_workload(std::vector<Request>, std::vector<TaskClass>);
+    std::unordered_map<int, std::size_t> class_index_, request_index_;
+};
+
+Workload validate_workload(std::vector<Request> requests, std::vector<TaskClass> classes);
+
+// ---------------------------------------------------------------- rng
+// xoshiro256++ seeded by splitmix64; same streams as the reference Rng.
+class Rng {
+public:
+    explicit Rng(std::uint64_t seed);
+    std::uint64_t next_u64();
+    double uniform();
+    double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+    std::uint64_t uniform_index(std::uint64_t n);
+    long long uniform_int(long long lo, long long hi) {
+        return lo + static_cast<long long>(uniform_index(static_cast<std::uint64_t>(hi - lo + 1)));
+    }
+    double normal();
+    double normal(double mean, double sd) { return mean + sd * normal(); }
+    template <typename T>
+    void shuffle(std::vector<T>& v) {
+        for (std::size_t i = v.size(); i > 1; --i) std::swap(v[i - 1], v[uniform_index(i)]);
+    }
+    static std::uint64_t derive(std::uint64_t seed, std::uint64_t stream);
+
+private:
+    std::uint64_t s_[4];
+};
+
+// ---------------------------------------------------------------- latency model
+double predict_prefill(const LatencyCoefficients& c, int b, int input_len);
+double predict_per_token_decode(const LatencyCoefficients& c, int b, int accumulated_len);
+double predict_decode_total(const LatencyCoefficients& c, int b, int input_len, int output_len);
+double predict_exec(const LatencyCoefficients& c, int b, int input_len, int output_len);
+double predict_tpot(const LatencyCoefficients& c, int b, int input_len, int output_len);
+constexpr int kValidatedMaxLen = 2047;
+inline bool is_extrapolated(int input_len, int output_len) { return input_len + output_len > kValidatedMaxLen; }
+LatencyCoefficients table_coefficients();
+
+// ---------------------------------------------------------------- objective
+struct ExecProfile {
+    int request_id = 0;
+    double exec_ms = 0.0, prefill_ms = 0.0, tpot_ms = 0.0;
+    bool extrapolated = false;
+};
+std::vector<ExecProfile> batch_exec_profile(const Schedule&, const LatencyCoefficients&, const Workload&);
+std::vector<double> waiting_times(const Schedule&, const std::vector<ExecProfile>&);
+bool meets_slo(const SloSpec& slo, double e2e_ms, double ttft_ms, double tpot_ms);
+EvaluatedSchedule evaluate(const Schedule&, const LatencyCoefficients&, const Workload&);
+
+// ---------------------------------------------------------------- priority mapper
+enum class SearchMode {
+    Chains,  // thousands of independent Philox chains on the GPU, best-of-chains (default)
+    Replay,  // one chain driven by the reference's xoshiro stream: bit-identical to the reference
+};
+
+struct EngineOptions {
+    SearchMode mode = SearchMode::Chains;
+    int chains = 4096;                  // Chains mode: total chains
+    double budget_ms = 0.0;             // > 0: stop the ladder after this much device time
+    std::vector<double> scale_ladder;   // per-chain objective_scale multipliers (chain c uses [c % size])
+    int device = -1;                    // -1: SLOSCHED_DEVICE env or 0
+    int chain_begin = 0, chain_end = -1;  // slice of [0, chains) run by this call (multi-GPU sharding)
+};
+
+struct AnnealConfig {
+    double t0 = 500.0;
+    double t_thres = 20.0;
+    int iter = 100;
+    double tau = 0.95;
+    std::uint64_t seed = 0;
+    std::optional<double> objective_scale;
+    EngineOptions engine;
+    void validate() const;
+};
+
+struct AnnealStats {
+    std::uint64_t proposals = 0;
+    std::uint64_t accepted = 0;
+    bool shortcut = false;
+    double g_sorted_start = 0.0;
+    double g_input_start = 0.0;
+    double objective_scale_used = 1.0;
+    // engine extensions
+    int chains_run = 0;
+    int levels_run = 0;
+    int best_chain = -1;
+    double engine_g = 0.0;    // best score as computed on the device
+    double kernel_ms = 0.0;   // device time of the annealing launch
+};
+
+struct AnnealResult {
+    EvaluatedSchedule best;
+    AnnealStats stats;
+};
+
+std::pair<Schedule, Schedule> initial_candidates(const Workload&, const std::vector<int>& request_ids,
+                                                 const LatencyCoefficients&, int max_batch);
+std::optional<EvaluatedSchedule> shortcut_check(const Schedule& sorted_schedule, const LatencyCoefficients&,
+                                                const Workload&);
+Schedule neighbor(const Schedule& schedule, Rng& rng, int max_batch);
+AnnealResult anneal(const Workload&, const std::vector<int>& request_ids, const LatencyCoefficients&,
+                    const AnnealConfig&, int max_batch);
+
+// Largest d with fl(d + c) <= s (the deadline convention of include/slosched_gpu.h).
+double latest_start(double s, double c);
+
+// The engine tables for a request set: exec[(b-1)*n + i] and deadline[(b-1)*n + i] for
+// dense index i = rank of the id among `ids` (CostModel, P:src/priority_mapper.cpp:205-231).
+void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c, int max_batch,
+                 std::vector<double>& exec, std::vector<double>& deadline);
+
+// ---------------------------------------------------------------- scheduler
+long long token_capacity(std::uint64_t remaining_mem_bytes, double mu, double sigma);
+
+struct AssignmentResult {
+    std::vector<std::vector<int>> per_instance;
+    int epochs = 1;
+};
+AssignmentResult assign_instances(const Workload&, const std::vector<InstanceState>&, const LatencyCoefficients&);
+
+enum class Policy { SA, EXHAUSTIVE, FCFS };
+
+struct InstanceQueue {
+    std::deque<Batch> pending;
+};
+std::optional<Batch> dispatch(InstanceQueue& queue, bool instance_ready);
+
+struct ScheduleAllResult {
+    AssignmentResult assignment;
+    std::vector<EvaluatedSchedule> per_instance;
+    std::vector<AnnealStats> stats;
+    std::vector<InstanceQueue> queues;
+    double overhead_ms = 0.0;
+};
+ScheduleAllResult schedule_all(const Workload&, const std::vector<InstanceState>&, const LatencyCoefficients&,
+                               const AnnealConfig&, Policy policy = Policy::SA, int exhaustive_cap = 10);
+
+// ---------------------------------------------------------------- synthetic inputs
+struct LengthDists {
+    double code_input_median = 300.0, code_input_sigma = 0.5;
+    double code_output_mean = 900.0, code_output_std = 300.0;
+    double chat_input_median = 200.0, chat_input_sigma = 0.5;
+    double chat_output_mean = 250.0, chat_output_std = 150.0;
+};
+std::pair<TaskClass, TaskClass> default_slo_classes();
+std::pair<TaskClass, TaskClass> default_synth_classes(const LengthDists& dists = {});
+std::vector<Request> generate_mixed(int n, std::uint64_t seed, const TaskClass& code_class,
+                                    const TaskClass& chat_class, const LengthDists& dists = {});
+// Estimator cold start: draw predicted_output_len from each class prior (Gaussian or
+// range; 256 without a prior) for requests that lack one.
+void assign_predicted_lengths_from_priors(std::vector<Request>& requests, const std::vector<TaskClass>& classes,
+                                          Rng& rng);
+
+}  // namespace slosched
+
+#endif

@@ -1,0 +1,137 @@
+/* slosched_gpu.h -- C ABI of the B200 annealing engine (hand-written sm_100a CUDA).
+ *
+ * Plain pointers and sizes only; no C++ or torch types cross this boundary.
+ * This is the layer the C++ scheduler entry point (include/slosched_b200.hpp,
+ * slosched::anneal) calls into, and what an FFI binding (ctypes / cgo / JNI)
+ * would bind directly. P: = reference tree /root/reference/proj/.
+ *
+ * What each entry point replaces in the reference:
+ *   slo_problem_set     CostModel ctor, P:src/priority_mapper.cpp:205-231 (flat exec/prefill/
+ *                       tpot tables per (dense index, batch size)); here the tables are
+ *                       (exec, deadline) pairs in a structure-of-arrays HBM layout.
+ *   slo_evaluate_batch  CostModel::score, P:src/priority_mapper.cpp:259-279 (identical operand
+ *                       order to evaluate(), P:src/objective.cpp:55-82): one candidate per
+ *                       thread, bit-exact n_met / t / g.
+ *   slo_anneal_chains   the annealing loop of anneal(), P:src/priority_mapper.cpp:368-402:
+ *                       SLO_RNG_XOSHIRO_REPLAY reproduces the reference walk bit-for-bit
+ *                       (FlatSchedule moves :104-199, Rng P:include/slosched/rng.hpp:14-100);
+ *                       SLO_RNG_PHILOX runs thousands of independent chains (one per warp)
+ *                       plus a grid-wide best-of-chains argmax.
+ *
+ * Conventions: every function returns an slo_status; on failure slo_last_error()
+ * (thread-local) holds the message. No exceptions cross the ABI. Output buffers are
+ * caller-owned. A context is owned by one host thread at a time.
+ *
+ * Deadline convention (makes the SLO test one compare, bit-exact): for dense index i
+ * and batch size b, deadline[b-1][i] is the largest double d such that a request whose
+ * batch starts at elapsed = d meets its SLO under the reference arithmetic:
+ *   E2E:       fl(d + exec) <= e2e_ms                       (P:src/priority_mapper.cpp:238)
+ *   TTFT_TPOT: fl(d + prefill) <= ttft_ms, and -inf when tpot > tpot_ms   (:239-240)
+ * fl(d + c) is monotone in d, so "met" == (elapsed <= deadline) exactly.
+ */
+#ifndef SLOSCHED_GPU_H
+#define SLOSCHED_GPU_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SLO_MAX_N 4096 /* 12-bit dense index per position */
+#define SLO_MAX_MB 16  /* 4-bit batch-size field; moves touch <= 2*mb <= 32 positions */
+
+typedef enum {
+    SLO_OK = 0,
+    SLO_ERR_DATA = 1,     /* reference DataError */
+    SLO_ERR_CAPACITY = 2, /* reference CapacityError / size limits of this engine */
+    SLO_ERR_CUDA = 3,
+    SLO_ERR_COMM = 4,
+    SLO_ERR_STATE = 5,    /* call order (e.g. no problem set) */
+    SLO_ERR_ARG = 6       /* reference std::invalid_argument */
+} slo_status;
+
+typedef enum { SLO_RNG_PHILOX = 0, SLO_RNG_XOSHIRO_REPLAY = 1 } slo_rng_mode;
+
+typedef struct slo_ctx slo_ctx;
+
+const char* slo_last_error(void);
+const char* slo_version(void);
+
+/* One context per device; owns a stream, the device tables and chain buffers. */
+int slo_ctx_create(int device, slo_ctx** out);
+void slo_ctx_destroy(slo_ctx* ctx);
+/* The cudaStream_t every launch of this context is enqueued on. */
+void* slo_ctx_stream(slo_ctx* ctx);
+int slo_ctx_sync(slo_ctx* ctx);
+/* Number of streaming multiprocessors of the context's device. */
+int slo_ctx_sm_count(slo_ctx* ctx);
+
+/* Upload the per-(batch size, dense index) tables: exec[(b-1)*n + i], deadline[(b-1)*n + i].
+ * 1 <= n <= SLO_MAX_N, 1 <= mb <= SLO_MAX_MB. */
+int slo_problem_set(slo_ctx* ctx, int32_t n, int32_t mb, const double* exec, const double* deadline);
+
+/* Bit-exact objective of `count` candidate schedules. perms[c*n + p] = dense index at
+ * position p; batch_end_bits[c*words + w] bit (p & 31) of word w = (p >> 5) set iff p is the
+ * last position of its batch (words = ceil(n/32); bit n-1 must be set). Host buffers. */
+int slo_evaluate_batch(slo_ctx* ctx, int32_t count, const uint16_t* perms,
+                       const uint32_t* batch_end_bits, int32_t* n_met, double* t, double* g);
+
+typedef struct {
+    double t0, t_thres; /* AnnealConfig (P:include/slosched/priority_mapper.hpp:16-28) */
+    int32_t iter;
+    double tau;
+    uint64_t seed;
+    double objective_scale;  /* resolved factor (reference :368-370 default t0 / G(start)) */
+    int32_t rng_mode;        /* slo_rng_mode */
+    int32_t chains;          /* total chains of the whole job (all devices) */
+    int32_t chain_begin;     /* this call runs chain ids [chain_begin, chain_end) */
+    int32_t chain_end;
+    int64_t budget_ns;       /* 0 = run the whole ladder; else stop after this much device time */
+    int32_t n_scale_mult;    /* optional per-chain scale ladder: chain c uses */
+    const double* scale_mult;/*   objective_scale * scale_mult[c % n_scale_mult] */
+} slo_chain_params;
+
+typedef struct {
+    double g;            /* best score found (engine evaluator) */
+    double t;            /* its summed latency */
+    int32_t n_met;
+    int32_t chain;       /* winning chain id (ties: lower t, then lower id) */
+    uint64_t proposals;  /* summed over the chains run */
+    uint64_t accepted;
+    int32_t chains_run;  /* chains that started */
+    int32_t levels_run;  /* temperature levels completed by the slowest chain */
+    float kernel_ms;     /* device time of the annealing launches (CUDA events) */
+    uint64_t positions_pass1; /* positions walked by the incremental evaluator (pass 1: */
+    uint64_t positions_pass2; /*   batch makespans, pass 2: elapsed/met/latency sums) */
+} slo_chain_result;
+
+/* Run chains from the start schedule (dense indices in position order + batch sizes) and
+ * return the best schedule found, in the same form. Synchronous. */
+int slo_anneal_chains(slo_ctx* ctx, const slo_chain_params* params, const int32_t* start_perm,
+                      const int32_t* start_sizes, int32_t start_nb, int32_t* best_perm,
+                      int32_t* best_sizes, int32_t* best_nb, slo_chain_result* result);
+
+/* Split form for device-resident timing: prepare uploads the start state (H2D) and
+ * parameters; launch only enqueues the annealing kernel and the argmax on the context
+ * stream (no host synchronisation, no copies); fetch synchronises and copies the winner
+ * back. slo_anneal_chains == prepare + launch + fetch. */
+int slo_chains_prepare(slo_ctx* ctx, const slo_chain_params* params, const int32_t* start_perm,
+                       const int32_t* start_sizes, int32_t start_nb);
+int slo_chains_launch(slo_ctx* ctx);
+int slo_chains_fetch(slo_ctx* ctx, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
+                     slo_chain_result* result);
+
+/* Achievable shared-memory bandwidth of the device (GB/s): conflict-free 16-byte loads on
+ * every SM -- the roofline denominator of the smem-bound chain kernel. */
+int slo_probe_smem_bandwidth(slo_ctx* ctx, double* gbytes_per_s);
+
+/* Philox4x32-10 (Random123 constants) -- the counter-based stream the chains draw from;
+ * exported for known-answer tests. */
+void slo_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

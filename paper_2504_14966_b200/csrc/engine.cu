@@ -1,0 +1,1266 @@
+// B200 annealing engine: hand-written sm_100a kernels behind include/slosched_gpu.h.
+//
+// Data layout:
+//   * Tables: HBM structure-of-arrays exec[mb][n], deadline[mb][n] (uploaded by
+//     slo_problem_set) interleaved once on device into tab[mb][n] = {exec, deadline}
+//     (16 B), then staged into shared memory by every CTA of the chain kernel with
+//     coalesced 16-byte loads (once per block).
+//   * Chain state (one chain per warp): 16-bit position entries
+//     ent = dense_index | (batch_size-1) << 12 stored "lane-major" -- position
+//     q = lane*P + j lives at ent[j*32 + lane] so every lane reads its own
+//     contiguous run of P positions with conflict-free shared loads -- plus a linear
+//     batch-end bitmask (bit q set iff q ends its batch).
+//
+// Kernels:
+//   k_eval_exact   K1: one candidate per thread, sequential reference arithmetic.
+//   k_replay       K2: one chain per thread, xoshiro256++ and FlatSchedule moves, exact.
+//   k_chains<P>    K3: one chain per warp, Philox4x32-10 moves, incremental objective.
+//   k_argmax       K4: best-of-chains (g desc, t asc, chain asc) + winner copy.
+// P: = /root/reference/proj/.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "slosched_gpu.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+constexpr unsigned FULL = 0xffffffffu;
+constexpr uint32_t kTagMove = 0x5105c4edu;   // Philox counter word 3 for move draws
+constexpr int kAcceptAttempt = 15;           // Philox counter word 2 for the Metropolis draw
+
+struct ChainRec {
+    double g;      // best score of the chain (-1 = never started)
+    double t;      // summed latency of the best
+    double cur_f;  // current score (multi-chain-per-warp state save)
+    int n_met;
+    int levels;
+    unsigned long long proposals;
+    unsigned long long accepted;
+    unsigned long long scan1, scan2;  // positions walked by pass 1 / pass 2 (roofline accounting)
+};
+
+struct ChainResult {
+    double g, t;
+    int n_met, chain;
+    unsigned long long proposals, accepted;
+    int chains_run, levels_min;
+    unsigned long long scan1, scan2;
+};
+
+// ------------------------------------------------------------------ device helpers
+__device__ __forceinline__ uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// Philox4x32-10, Random123 constants.
+__host__ __device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+#if defined(__CUDA_ARCH__)
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), hi1 = __umulhi(0xCD9E8D57u, c[2]);
+#else
+        const uint32_t hi0 = (uint32_t)(((uint64_t)0xD2511F53u * c[0]) >> 32);
+        const uint32_t hi1 = (uint32_t)(((uint64_t)0xCD9E8D57u * c[2]) >> 32);
+#endif
+        const uint32_t lo0 = 0xD2511F53u * c[0], lo1 = 0xCD9E8D57u * c[2];
+        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
+        c[0] = n0, c[1] = lo1, c[2] = n2, c[3] = lo0;
+        k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
+    }
+}
+
+__device__ __forceinline__ uint32_t lemire32(uint32_t x, uint32_t n) { return __umulhi(x, n); }
+
+__device__ __forceinline__ double dmax(double a, double b) { return a < b ? b : a; }  // std::max
+
+// first set bit at or after q (bit n-1 is always set, batches <= 16 long)
+__device__ __forceinline__ int next_end(const uint32_t* bits, int q) {
+    int w = q >> 5;
+    uint32_t m = bits[w] & (FULL << (q & 31));
+    while (!m) m = bits[++w];
+    return (w << 5) + __ffs(m) - 1;
+}
+
+// last set bit strictly before q, or -1
+__device__ __forceinline__ int prev_end(const uint32_t* bits, int q) {
+    if (q <= 0) return -1;
+    int w = q >> 5;
+    uint32_t m = bits[w] & ((1u << (q & 31)) - 1u);
+    while (!m && w > 0) m = bits[--w];
+    return m ? (w << 5) + 31 - __clz(m) : -1;
+}
+
+// ================================================================ K1: exact evaluate
+// Sequential CostModel::score (P:src/priority_mapper.cpp:259-279) per candidate.
+__global__ void k_eval_exact(int count, int n, int words, const uint16_t* __restrict__ perms,
+                             const uint32_t* __restrict__ bits, const double2* __restrict__ tab,
+                             int* __restrict__ n_met, double* __restrict__ t_out, double* __restrict__ g_out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= count) return;
+    const uint16_t* pr = perms + (size_t)c * n;
+    const uint32_t* br = bits + (size_t)c * words;
+    double elapsed = 0.0, total = 0.0;
+    int met = 0, s = 0;
+    while (s < n) {
+        const int e = next_end(br, s);
+        const int bidx = e - s;
+        double makespan = 0.0;
+        for (int q = s; q <= e; ++q) {
+            const double2 v = __ldg(&tab[bidx * n + pr[q]]);
+            const double e2e = elapsed + v.x;
+            total += e2e;
+            met += elapsed <= v.y;
+            makespan = dmax(makespan, v.x);
+        }
+        elapsed += makespan;
+        s = e + 1;
+    }
+    n_met[c] = met;
+    t_out[c] = total;
+    g_out[c] = total > 0.0 ? (double)met / total : 0.0;
+}
+
+// ================================================================ K2: exact replay
+// xoshiro256++ / splitmix64 (P:include/slosched/rng.hpp:14-57)
+struct Xoshiro {
+    uint64_t s[4];
+    __device__ static uint64_t mix(uint64_t z) {
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    }
+    __device__ explicit Xoshiro(uint64_t seed) {
+        uint64_t z = seed;
+        for (int i = 0; i < 4; ++i) {
+            z += 0x9e3779b97f4a7c15ULL;
+            s[i] = mix(z);
+        }
+    }
+    __device__ static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+    __device__ uint64_t next() {
+        const uint64_t out = rotl(s[0] + s[3], 23) + s[0];
+        const uint64_t t = s[1] << 17;
+        s[2] ^= s[0];
+        s[3] ^= s[1];
+        s[1] ^= s[2];
+        s[0] ^= s[3];
+        s[2] ^= t;
+        s[3] = rotl(s[3], 45);
+        return out;
+    }
+    __device__ double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
+    __device__ uint64_t index(uint64_t n) {
+        uint64_t x = next();
+        uint64_t lo = x * n, hi = __umul64hi(x, n);
+        if (lo < n) {
+            const uint64_t thr = (0 - n) % n;
+            while (lo < thr) {
+                x = next();
+                lo = x * n;
+                hi = __umul64hi(x, n);
+            }
+        }
+        return hi;
+    }
+};
+
+struct Flat {  // FlatSchedule (P:src/priority_mapper.cpp:104-199) over global scratch
+    int* perm;
+    int* sizes;
+    int nb;
+};
+
+__device__ int fl_batch_of(const Flat& f, int pos) {
+    int k = 0;
+    for (int acc = f.sizes[0]; pos >= acc; acc += f.sizes[++k]) {
+    }
+    return k;
+}
+
+__device__ int fl_batch_start(const Flat& f, int k) {
+    int acc = 0;
+    for (int i = 0; i < k; ++i) acc += f.sizes[i];
+    return acc;
+}
+
+__device__ void fl_erase(Flat& f, int k) {
+    for (int i = k; i + 1 < f.nb; ++i) f.sizes[i] = f.sizes[i + 1];
+    f.nb--;
+}
+
+__device__ bool fl_squeeze(Flat& f, int n, Xoshiro& r, int mb) {
+    if (f.nb < 2) return false;
+    const int first = f.sizes[0];
+    const int pos = first + (int)r.index((uint64_t)(n - first));
+    const int k = fl_batch_of(f, pos);
+    if (f.sizes[k - 1] >= mb) return false;
+    const int dst = fl_batch_start(f, k);
+    const int v = f.perm[pos];
+    for (int q = pos; q > dst; --q) f.perm[q] = f.perm[q - 1];
+    f.perm[dst] = v;
+    f.sizes[k - 1]++;
+    if (--f.sizes[k] == 0) fl_erase(f, k);
+    return true;
+}
+
+__device__ bool fl_delay(Flat& f, int n, Xoshiro& r, int mb) {
+    if (n == 0) return false;
+    const int pos = (int)r.index((uint64_t)n);
+    const int k = fl_batch_of(f, pos);
+    const bool has_next = k + 1 < f.nb;
+    if (has_next && f.sizes[k + 1] >= mb) return false;
+    const int dst = has_next ? fl_batch_start(f, k + 2) : n;
+    const int v = f.perm[pos];
+    for (int q = pos; q + 1 < dst; ++q) f.perm[q] = f.perm[q + 1];
+    f.perm[dst - 1] = v;
+    if (has_next) f.sizes[k + 1]++;
+    else f.sizes[f.nb++] = 1;
+    if (--f.sizes[k] == 0) fl_erase(f, k);
+    return true;
+}
+
+__device__ bool fl_swap(Flat& f, int n, Xoshiro& r) {
+    if (n < 2) return false;
+    const uint64_t a = r.index((uint64_t)n);
+    uint64_t b = r.index((uint64_t)(n - 1));
+    if (b >= a) ++b;
+    const int t = f.perm[a];
+    f.perm[a] = f.perm[b];
+    f.perm[b] = t;
+    return true;
+}
+
+__device__ bool fl_propose(Flat& f, int n, Xoshiro& r, int mb) {
+    if (n == 0) return false;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        const uint64_t op = r.index(3);
+        if (op == 0) {
+            if (fl_squeeze(f, n, r, mb)) return true;
+        } else if (op == 1) {
+            if (fl_delay(f, n, r, mb)) return true;
+        } else {
+            if (fl_swap(f, n, r)) return true;
+        }
+    }
+    return fl_swap(f, n, r);
+}
+
+__device__ double fl_score(const Flat& f, int n, const double2* __restrict__ tab, int* n_met_out,
+                           double* t_out) {
+    int met = 0;
+    double total = 0.0, elapsed = 0.0;
+    int pos = 0;
+    for (int k = 0; k < f.nb; ++k) {
+        const int part = f.sizes[k], bidx = part - 1;
+        double makespan = 0.0;
+        for (int j = 0; j < part; ++j) {
+            const double2 v = __ldg(&tab[bidx * n + f.perm[pos + j]]);
+            const double e2e = elapsed + v.x;
+            total += e2e;
+            met += elapsed <= v.y;
+            makespan = dmax(makespan, v.x);
+        }
+        elapsed += makespan;
+        pos += part;
+    }
+    if (n_met_out) *n_met_out = met;
+    if (t_out) *t_out = total;
+    return total > 0.0 ? (double)met / total : 0.0;
+}
+
+__device__ void fl_copy(Flat& dst, const Flat& src, int n) {
+    for (int i = 0; i < n; ++i) dst.perm[i] = src.perm[i];
+    for (int i = 0; i < src.nb; ++i) dst.sizes[i] = src.sizes[i];
+    dst.nb = src.nb;
+}
+
+struct ReplayParams {
+    int n, mb, chains;
+    const double2* tab;
+    double t0, t_thres, tau, scale;
+    int iter;
+    uint64_t seed;
+    const int* start_perm;
+    const int* start_sizes;
+    int start_nb;
+    int* scratch;  // [chains][6n]
+    int* best_perm;   // [chains][n]
+    int* best_sizes;  // [chains][n]
+    int* best_nb;     // [chains]
+    ChainRec* rec;
+};
+
+// One thread = one reference chain (seed + chain id), the loop of P:src/priority_mapper.cpp:377-402.
+__global__ void k_replay(const ReplayParams p) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= p.chains) return;
+    const int n = p.n;
+    // three FlatSchedules per chain; each sizes array has n + 1 slots because delay appends a
+    // trailing batch before erasing an emptied one (all-singleton schedules briefly hold n + 1)
+    const size_t stride = 2 * (size_t)n + 1;
+    int* base = p.scratch + (size_t)c * 3 * stride;
+    Flat cur{base, base + n, p.start_nb}, scr{base + stride, base + stride + n, 0},
+        best{base + 2 * stride, base + 2 * stride + n, 0};
+    for (int i = 0; i < n; ++i) cur.perm[i] = p.start_perm[i];
+    for (int i = 0; i < p.start_nb; ++i) cur.sizes[i] = p.start_sizes[i];
+    double f = fl_score(cur, n, p.tab, nullptr, nullptr);
+    fl_copy(best, cur, n);
+    double best_f = f;
+    Xoshiro rng(p.seed + (uint64_t)c);
+    unsigned long long props = 0, accs = 0;
+    int levels = 0;
+    for (double t = p.t0; t >= p.t_thres; t *= p.tau, ++levels) {
+        for (int k = 0; k < p.iter; ++k) {
+            fl_copy(scr, cur, n);
+            fl_propose(scr, n, rng, p.mb);
+            const double f_new = fl_score(scr, n, p.tab, nullptr, nullptr);
+            props++;
+            bool accept = f_new > f;
+            if (!accept) {
+                const double x = (f - f_new) * p.scale / t;
+                const double u = rng.uniform();
+                accept = x < 38.0 ? u < exp(-x) : u == 0.0;
+            }
+            if (accept) {
+                accs++;
+                const Flat tmp = cur;
+                cur = scr;
+                scr = tmp;
+                f = f_new;
+                if (f > best_f) {
+                    fl_copy(best, cur, n);
+                    best_f = f;
+                }
+            }
+        }
+    }
+    int nm;
+    double tt;
+    fl_score(best, n, p.tab, &nm, &tt);
+    for (int i = 0; i < n; ++i) p.best_perm[(size_t)c * n + i] = best.perm[i];
+    for (int i = 0; i < best.nb; ++i) p.best_sizes[(size_t)c * n + i] = best.sizes[i];
+    p.best_nb[c] = best.nb;
+    ChainRec r;
+    r.g = best_f;
+    r.t = tt;
+    r.cur_f = f;
+    r.n_met = nm;
+    r.levels = levels;
+    r.proposals = props;
+    r.accepted = accs;
+    p.rec[c] = r;
+}
+
+// ================================================================ K3: chains
+struct ChainParams {
+    int n, mb;
+    const double2* tab;  // global [mb][n]
+    int smem_tab;
+    double t0, tau, scale;
+    int iter, levels;
+    const double* scale_mult;
+    int n_mult;
+    uint32_t key0, key1;
+    int chain_begin, chain_count;
+    long long budget_ns;
+    const uint16_t* start_ent;   // [32P]
+    const uint32_t* start_bits;  // [P]
+    uint16_t* st_ent;            // [chain_count][32P] state between levels (multi chains/warp)
+    uint32_t* st_bits;           // [chain_count][P]
+    uint16_t* best_ent;          // [chain_count][32P]
+    uint32_t* best_bits;         // [chain_count][P]
+    ChainRec* rec;               // [chain_count]
+};
+
+struct LaneSum {  // per-lane summary of its P positions (pass 1)
+    double hm;     // max exec from lane start through the first batch end (whole lane if none)
+    double tm;     // max exec after the last batch end in the lane
+    double inner;  // summed makespans of batches that start and end inside the lane
+    int fe;        // lane contains a batch end
+};
+
+template <int P>
+struct Lane {
+    static constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : P == 32 ? 5 : P == 64 ? 6 : 7;
+    __device__ static __forceinline__ int phys(int q) { return ((q & (P - 1)) << 5) | (q >> LOGP); }
+    __device__ static __forceinline__ int lane_of(int q) { return q >> LOGP; }
+
+    __device__ static void pass1(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int lane,
+                                 LaneSum& s) {
+        double run = 0.0, hm = 0.0, inner = 0.0;
+        int fe = 0;
+        const int q0 = lane * P;
+        uint32_t w = 0;
+#pragma unroll 4
+        for (int j = 0; j < P; ++j) {
+            const int q = q0 + j;
+            if (q >= n) break;
+            if ((j & 31) == 0) w = bits[q >> 5] >> (q & 31);
+            const uint32_t e16 = ent[(j << 5) | lane];
+            const double e = tab[(e16 >> 12) * n + (e16 & 0xFFFu)].x;
+            run = dmax(run, e);
+            if ((w >> (j & 31)) & 1u) {
+                if (fe) inner += run;
+                else hm = run, fe = 1;
+                run = 0.0;
+            }
+        }
+        s.fe = fe;
+        s.hm = fe ? hm : run;
+        s.tm = run;
+        s.inner = inner;
+    }
+
+    // warp-wide: elapsed at each lane's first position (E) and makespan of the batch
+    // open at the lane start (fmk), from the lane summaries
+    __device__ static void combine(const LaneSum& s, int lane, double& E, double& fmk) {
+        int F = s.fe;
+        double M = s.fe ? s.tm : s.hm;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {  // segmented max scan of open-run maxima
+            const double Mu = __shfl_up_sync(FULL, M, d);
+            const int Fu = __shfl_up_sync(FULL, F, d);
+            if (lane >= d) {
+                if (!F) M = dmax(Mu, M);
+                F |= Fu;
+            }
+        }
+        double carry = __shfl_up_sync(FULL, M, 1);
+        if (lane == 0) carry = 0.0;
+        fmk = dmax(carry, s.hm);
+        double S = s.fe ? fmk + s.inner : 0.0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {  // inclusive sum scan of owned makespans
+            const double v = __shfl_up_sync(FULL, S, d);
+            if (lane >= d) S += v;
+        }
+        E = __shfl_up_sync(FULL, S, 1);
+        if (lane == 0) E = 0.0;
+    }
+
+    __device__ static void pass2(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int lane,
+                                 double E, double fmk, double& ltot, int& lnm) {
+        double el = E, run = 0.0, tot = 0.0;
+        int nm = 0, first = 1;
+        const int q0 = lane * P;
+        uint32_t w = 0;
+#pragma unroll 4
+        for (int j = 0; j < P; ++j) {
+            const int q = q0 + j;
+            if (q >= n) break;
+            if ((j & 31) == 0) w = bits[q >> 5] >> (q & 31);
+            const uint32_t e16 = ent[(j << 5) | lane];
+            const double2 v = tab[(e16 >> 12) * n + (e16 & 0xFFFu)];
+            tot += el + v.x;
+            nm += el <= v.y;
+            run = dmax(run, v.x);
+            if ((w >> (j & 31)) & 1u) {
+                el += first ? fmk : run;
+                first = 0;
+                run = 0.0;
+            }
+        }
+        ltot = tot;
+        lnm = nm;
+    }
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+
+struct Move {
+    int kind;                // 0 none, 1 range (squeeze/delay), 2 swap
+    int lo, hi, split, sz1, sz2;
+    int ra, rb, dir;         // rotation on [ra, rb]; dir +1 right, -1 left
+    int clr, set;            // bitmask edits (-1 = none)
+    int a, b;                // swap positions
+};
+
+template <int P>
+__device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, uint32_t prop, uint32_t cid,
+                                          uint32_t k0, uint32_t k1) {
+    Move mv;
+    mv.kind = 0;
+    if (n == 0) return mv;
+    for (int attempt = 0; attempt <= 8; ++attempt) {
+        uint32_t r[4] = {prop, cid, (uint32_t)attempt, kTagMove};
+        philox10(r, k0, k1);
+        const uint32_t op = attempt < 8 ? lemire32(r[0], 3) : 2u;  // forced swap after 8 misses
+        if (op == 0) {  // squeeze (P:src/priority_mapper.cpp:141-153)
+            const int first = next_end(bits, 0) + 1;
+            if (first >= n) continue;
+            const int pos = first + (int)lemire32(r[1], (uint32_t)(n - first));
+            const int sk = prev_end(bits, pos) + 1;
+            const int skm1 = prev_end(bits, sk - 1) + 1;
+            if (sk - skm1 >= mb) continue;
+            const int ek = next_end(bits, pos);
+            mv.kind = 1;
+            mv.lo = skm1, mv.hi = ek, mv.split = sk;
+            mv.sz1 = sk - skm1 + 1, mv.sz2 = ek - sk;
+            mv.ra = sk, mv.rb = pos, mv.dir = 1;
+            mv.clr = sk - 1, mv.set = sk;
+            return mv;
+        } else if (op == 1) {  // delay (:155-170)
+            const int pos = (int)lemire32(r[1], (uint32_t)n);
+            const int sk = prev_end(bits, pos) + 1;
+            const int ek = next_end(bits, pos);
+            if (ek < n - 1) {
+                const int ek1 = next_end(bits, ek + 1);
+                if (ek1 - ek >= mb) continue;
+                mv.kind = 1;
+                mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
+                mv.sz1 = ek - sk, mv.sz2 = ek1 - ek + 1;
+                mv.ra = pos, mv.rb = ek1, mv.dir = -1;
+                mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
+            } else {
+                mv.kind = 1;
+                mv.lo = sk, mv.hi = n - 1, mv.split = n - 2;
+                mv.sz1 = n - 1 - sk, mv.sz2 = 1;
+                mv.ra = pos, mv.rb = n - 1, mv.dir = -1;
+                mv.clr = -1, mv.set = n >= 2 ? n - 2 : -1;
+            }
+            return mv;
+        } else {  // swap (:172-180)
+            if (n < 2) continue;
+            const int a = (int)lemire32(r[1], (uint32_t)n);
+            int b = (int)lemire32(r[2], (uint32_t)(n - 1));
+            if (b >= a) ++b;
+            mv.kind = 2;
+            mv.a = a, mv.b = b;
+            return mv;
+        }
+    }
+    return mv;
+}
+
+template <int P>
+__global__ void __launch_bounds__(1024, 1) k_chains(const ChainParams p) {
+    using L = Lane<P>;
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int n = p.n, mb = p.mb;
+
+    const double2* tab = p.tab;
+    size_t off = 0;
+    if (p.smem_tab) {  // stage the (exec, deadline) table once per block
+        double2* st = reinterpret_cast<double2*>(smem);
+        const int total = mb * n;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) st[i] = p.tab[i];
+        __syncthreads();
+        tab = st;
+        off = ((size_t)total * sizeof(double2) + 15) & ~(size_t)15;
+    }
+    constexpr int kSlot = ((64 * P + 4 * P) + 15) & ~15;
+    uint16_t* ent = reinterpret_cast<uint16_t*>(smem + off + (size_t)wid * kSlot);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(ent + 32 * P);
+
+    const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
+    if (gw >= p.chain_count) return;
+    const int n_my = (p.chain_count - gw + TW - 1) / TW;
+
+    uint64_t deadline = ~0ull;
+    if (p.budget_ns > 0) deadline = __shfl_sync(FULL, gtimer(), 0) + (uint64_t)p.budget_ns;
+
+    // per-chain registers (valid across levels when n_my == 1)
+    LaneSum cs;
+    const unsigned long long lane_pos = (unsigned long long)max(0, min(P, n - lane * P));
+    double cE = 0.0, cfmk = 0.0, cltot = 0.0, f = 0.0, best_f = 0.0;
+    int clnm = 0;
+    unsigned long long props = 0, accs = 0;
+    int stop = 0;
+
+    double t = p.t0;
+    for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
+        for (int k = 0; k < n_my; ++k) {
+            if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
+                stop = 1;
+                break;
+            }
+            const int c = gw + k * TW;
+            const uint32_t cid = (uint32_t)(p.chain_begin + c);
+            ChainRec* rc = p.rec + c;
+            if (lev == 0 || n_my > 1) {  // (re)load chain state
+                const uint16_t* se = lev == 0 ? p.start_ent : p.st_ent + (size_t)c * 32 * P;
+                const uint32_t* sb = lev == 0 ? p.start_bits : p.st_bits + (size_t)c * P;
+                for (int i = lane; i < 32 * P; i += 32) ent[i] = se[i];
+                for (int i = lane; i < P; i += 32) bits[i] = sb[i];
+                __syncwarp();
+                L::pass1(ent, bits, tab, n, lane, cs);
+                L::combine(cs, lane, cE, cfmk);
+                L::pass2(ent, bits, tab, n, lane, cE, cfmk, cltot, clnm);
+                const double tot = warp_sum(cltot);
+                const int nm = __reduce_add_sync(FULL, clnm);
+                f = tot > 0.0 ? (double)nm / tot : 0.0;
+                if (lev == 0) {
+                    best_f = f, props = 0, accs = 0;
+                    for (int i = lane; i < 32 * P; i += 32) p.best_ent[(size_t)c * 32 * P + i] = ent[i];
+                    for (int i = lane; i < P; i += 32) p.best_bits[(size_t)c * P + i] = bits[i];
+                    if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
+                } else {
+                    best_f = rc->g, props = rc->proposals, accs = rc->accepted;
+                }
+            }
+            const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
+            unsigned long long sc1 = 0, sc2 = 0;
+
+            for (int it = 0; it < p.iter; ++it) {
+                const uint32_t prop = (uint32_t)(lev * p.iter + it);
+                const Move mv = draw_move<P>(bits, n, mb, prop, cid, p.key0, p.key1);
+                // ---- apply the move in place (undo on reject)
+                int q = 0;
+                uint16_t old_q = 0;
+                uint32_t ow0 = 0, ow1 = 0;
+                int w0 = 0, w1 = 0;
+                int dlo = 0, dhi = -1, dx = -1;  // dirty lanes [dlo, dhi] plus dx
+                if (mv.kind == 1) {
+                    q = mv.lo + lane;
+                    const bool act = q <= mv.hi;
+                    uint16_t nw = 0;
+                    if (act) {
+                        int src = q;
+                        if (mv.dir > 0) src = q == mv.ra ? mv.rb : (q > mv.ra && q <= mv.rb ? q - 1 : q);
+                        else src = q == mv.rb ? mv.ra : (q >= mv.ra && q < mv.rb ? q + 1 : q);
+                        old_q = ent[L::phys(q)];
+                        const uint32_t s16 = ent[L::phys(src)];
+                        const int sz = q <= mv.split ? mv.sz1 : mv.sz2;
+                        nw = (uint16_t)((s16 & 0xFFFu) | ((uint32_t)(sz - 1) << 12));
+                    }
+                    w0 = mv.clr >= 0 ? mv.clr >> 5 : 0;
+                    w1 = mv.set >= 0 ? mv.set >> 5 : 0;
+                    ow0 = bits[w0], ow1 = bits[w1];
+                    __syncwarp();
+                    if (act) ent[L::phys(q)] = nw;
+                    if (lane == 0) {
+                        if (mv.clr >= 0) bits[mv.clr >> 5] &= ~(1u << (mv.clr & 31));
+                        if (mv.set >= 0) bits[mv.set >> 5] |= 1u << (mv.set & 31);
+                    }
+                    __syncwarp();
+                    dlo = L::lane_of(mv.lo), dhi = L::lane_of(mv.hi);
+                } else if (mv.kind == 2) {
+                    const uint32_t ea = ent[L::phys(mv.a)], eb = ent[L::phys(mv.b)];
+                    ow0 = ea, ow1 = eb;
+                    __syncwarp();
+                    if (lane == 0) {
+                        ent[L::phys(mv.a)] = (uint16_t)((ea & 0xF000u) | (eb & 0xFFFu));
+                        ent[L::phys(mv.b)] = (uint16_t)((eb & 0xF000u) | (ea & 0xFFFu));
+                    }
+                    __syncwarp();
+                    dlo = dhi = L::lane_of(mv.a);
+                    dx = L::lane_of(mv.b);
+                }
+                // ---- incremental objective: only dirty lanes redo pass 1; lanes whose inputs
+                //      are unchanged keep their cached pass-2 contribution
+                LaneSum ns = cs;
+                const bool dirty = (lane >= dlo && lane <= dhi) || lane == dx;
+                if (dirty) L::pass1(ent, bits, tab, n, lane, ns), sc1 += lane_pos;
+                double nE, nfmk;
+                L::combine(ns, lane, nE, nfmk);
+                double nltot = cltot;
+                int nlnm = clnm;
+                if (dirty || nE != cE || nfmk != cfmk)
+                    L::pass2(ent, bits, tab, n, lane, nE, nfmk, nltot, nlnm), sc2 += lane_pos;
+                const double tot = warp_sum(nltot);
+                const int nm = __reduce_add_sync(FULL, nlnm);
+                const double f_new = tot > 0.0 ? (double)nm / tot : 0.0;
+                ++props;
+                // ---- Metropolis (P:src/priority_mapper.cpp:385-391)
+                bool accept = f_new > f;
+                if (!accept) {
+                    const double x = (f - f_new) * scale / t;
+                    uint32_t r[4] = {prop, cid, (uint32_t)kAcceptAttempt, kTagMove};
+                    philox10(r, p.key0, p.key1);
+                    const double u = (double)((((uint64_t)r[0] << 32) | r[1]) >> 11) * 0x1.0p-53;
+                    accept = x < 38.0 ? u < exp(-x) : u == 0.0;
+                }
+                if (accept) {
+                    ++accs;
+                    cs = ns, cE = nE, cfmk = nfmk, cltot = nltot, clnm = nlnm, f = f_new;
+                    if (f > best_f) {
+                        best_f = f;
+                        for (int i = lane; i < 32 * P; i += 32) p.best_ent[(size_t)c * 32 * P + i] = ent[i];
+                        for (int i = lane; i < P; i += 32) p.best_bits[(size_t)c * P + i] = bits[i];
+                        if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
+                    }
+                } else if (mv.kind == 1) {
+                    if (q <= mv.hi) ent[L::phys(q)] = old_q;
+                    if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
+                    __syncwarp();
+                } else if (mv.kind == 2) {
+                    if (lane == 0) ent[L::phys(mv.a)] = (uint16_t)ow0, ent[L::phys(mv.b)] = (uint16_t)ow1;
+                    __syncwarp();
+                }
+            }
+            if (n_my > 1) {  // park the chain until the next level
+                for (int i = lane; i < 32 * P; i += 32) p.st_ent[(size_t)c * 32 * P + i] = ent[i];
+                for (int i = lane; i < P; i += 32) p.st_bits[(size_t)c * P + i] = bits[i];
+                __syncwarp();
+            }
+#pragma unroll
+            for (int d = 16; d; d >>= 1)
+                sc1 += __shfl_xor_sync(FULL, sc1, d), sc2 += __shfl_xor_sync(FULL, sc2, d);
+            if (lane == 0) {
+                rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
+                rc->scan1 += sc1, rc->scan2 += sc2;
+            }
+        }
+    }
+}
+
+// ================================================================ K4: argmax
+__device__ __forceinline__ bool better(double g, double t, int c, double bg, double bt, int bc) {
+    if (g != bg) return g > bg;
+    if (t != bt) return t < bt;
+    return c < bc;
+}
+
+__global__ void k_argmax(int chain_count, const ChainRec* __restrict__ rec, ChainResult* out, int ent_words,
+                         int bit_words, const uint16_t* best_ent, const uint32_t* best_bits, uint16_t* win_ent,
+                         uint32_t* win_bits) {
+    __shared__ double sg[512], st[512];
+    __shared__ int sc[512], slev[512], sn[512];
+    __shared__ unsigned long long sp[512], sa[512], s1[512], s2[512];
+    const int tid = threadIdx.x;
+    double bg = -2.0, bt = 0.0;
+    int bc = 0x7fffffff, lev = 0x7fffffff, started = 0;
+    unsigned long long props = 0, accs = 0, sc1 = 0, sc2 = 0;
+    for (int c = tid; c < chain_count; c += blockDim.x) {
+        const ChainRec r = rec[c];
+        if (r.levels > 0) {  // chain started (budget may stop chains before level 0)
+            ++started;
+            lev = min(lev, r.levels);
+            props += r.proposals, accs += r.accepted, sc1 += r.scan1, sc2 += r.scan2;
+            if (better(r.g, r.t, c, bg, bt, bc)) bg = r.g, bt = r.t, bc = c;
+        }
+    }
+    sg[tid] = bg, st[tid] = bt, sc[tid] = bc, slev[tid] = lev, sn[tid] = started, sp[tid] = props, sa[tid] = accs;
+    s1[tid] = sc1, s2[tid] = sc2;
+    __syncthreads();
+    for (int s = blockDim.x >> 1; s; s >>= 1) {
+        if (tid < s) {
+            const int o = tid + s;
+            if (better(sg[o], st[o], sc[o], sg[tid], st[tid], sc[tid])) sg[tid] = sg[o], st[tid] = st[o], sc[tid] = sc[o];
+            slev[tid] = min(slev[tid], slev[o]);
+            sn[tid] += sn[o], sp[tid] += sp[o], sa[tid] += sa[o], s1[tid] += s1[o], s2[tid] += s2[o];
+        }
+        __syncthreads();
+    }
+    const int win = sc[0];
+    if (win >= chain_count) {
+        if (tid == 0) out->chain = -1, out->chains_run = 0, out->proposals = 0;
+        return;
+    }
+    if (tid == 0) {
+        out->g = sg[0], out->t = st[0], out->chain = win, out->n_met = rec[win].n_met;
+        out->proposals = sp[0], out->accepted = sa[0], out->chains_run = sn[0];
+        out->levels_min = slev[0] == 0x7fffffff ? 0 : slev[0];
+        out->scan1 = s1[0], out->scan2 = s2[0];
+    }
+    for (int i = tid; i < ent_words; i += blockDim.x) win_ent[i] = best_ent[(size_t)win * ent_words + i];
+    for (int i = tid; i < bit_words; i += blockDim.x) win_bits[i] = best_bits[(size_t)win * bit_words + i];
+}
+
+// shared-memory bandwidth probe: conflict-free 16-byte loads (4 wavefronts per warp load)
+__global__ void __launch_bounds__(1024) k_smem_probe(int iters, uint4* sink) {
+    extern __shared__ uint4 sbuf[];
+    constexpr int kVec = 4096;  // 64 KiB
+    for (int i = threadIdx.x; i < kVec; i += blockDim.x) sbuf[i] = make_uint4(i, i * 3, i * 5, i * 7);
+    __syncthreads();
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    int idx = threadIdx.x;
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll 8
+        for (int k = 0; k < 8; ++k) {
+            const uint4 v = sbuf[(idx + k * 128) & (kVec - 1)];
+            acc.x ^= v.x, acc.y ^= v.y, acc.z ^= v.z, acc.w ^= v.w;
+        }
+        idx += 1024;
+    }
+    if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9e3779b9u) sink[threadIdx.x] = acc;
+}
+
+// interleave the SoA tables into {exec, deadline} pairs
+__global__ void k_interleave(int total, const double* exec, const double* dl, double2* tab) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < total) tab[i] = make_double2(exec[i], dl[i]);
+}
+
+// ------------------------------------------------------------------ host side
+#define CK(call)                                                                  \
+    do {                                                                          \
+        cudaError_t e_ = (call);                                                  \
+        if (e_ != cudaSuccess) {                                                  \
+            g_err = std::string(#call) + ": " + cudaGetErrorString(e_);           \
+            return SLO_ERR_CUDA;                                                  \
+        }                                                                         \
+    } while (0)
+
+int fail(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t reserve(size_t bytes) {
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        cudaError_t e = cudaMalloc(&p, bytes);
+        if (e == cudaSuccess) cap = bytes;
+        return e;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+    ~DevBuf() {
+        if (p) cudaFree(p);
+    }
+};
+
+int pick_P(int n) {
+    int P = 1;
+    while (32 * P < n) P <<= 1;
+    return P;
+}
+
+}  // namespace
+
+struct slo_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    int sm_count = 0;
+    size_t smem_optin = 0;
+    int n = 0, mb = 0;
+    DevBuf tab, exec_soa, dl_soa;
+    // chains
+    DevBuf st_ent, st_bits, best_ent, best_bits, rec, start_ent, start_bits, scale_mult, result, win_ent, win_bits;
+    // replay
+    DevBuf r_scratch, r_best_perm, r_best_sizes, r_best_nb, r_start_perm, r_start_sizes;
+    // K1
+    DevBuf e_perms, e_bits, e_n, e_t, e_g;
+    bool prepared = false;
+    slo_chain_params prm{};
+    int P = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
+    size_t smem = 0;
+    bool smem_tab = false;
+    double replay_scale = 0.0;
+    int start_nb = 0;
+    ChainParams kp{};
+    ReplayParams rp{};
+};
+
+extern "C" {
+
+const char* slo_last_error(void) { return g_err.c_str(); }
+const char* slo_version(void) { return "slosched_b200 engine 0.1 (sm_100a)"; }
+
+void slo_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    philox10(c, key[0], key[1]);
+    for (int i = 0; i < 4; ++i) out[i] = c[i];
+}
+
+int slo_ctx_create(int device, slo_ctx** out) {
+    if (!out) return fail(SLO_ERR_ARG, "slo_ctx_create: null out");
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return fail(SLO_ERR_ARG, "slo_ctx_create: no such device");
+    CK(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CK(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(SLO_ERR_CUDA, std::string("slo_ctx_create: need an sm_100 device, got ") + prop.name);
+    auto* c = new slo_ctx();
+    c->device = device;
+    c->sm_count = prop.multiProcessorCount;
+    c->smem_optin = prop.sharedMemPerBlockOptin;
+    cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e != cudaSuccess) {
+        delete c;
+        return fail(SLO_ERR_CUDA, std::string("slo_ctx_create: ") + cudaGetErrorString(e));
+    }
+    *out = c;
+    return SLO_OK;
+}
+
+void slo_ctx_destroy(slo_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    cudaStreamSynchronize(c->stream);
+    cudaEventDestroy(c->ev0);
+    cudaEventDestroy(c->ev1);
+    cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+void* slo_ctx_stream(slo_ctx* c) { return c ? (void*)c->stream : nullptr; }
+int slo_ctx_sm_count(slo_ctx* c) { return c ? c->sm_count : 0; }
+
+int slo_ctx_sync(slo_ctx* c) {
+    CK(cudaSetDevice(c->device));
+    CK(cudaStreamSynchronize(c->stream));
+    return SLO_OK;
+}
+
+int slo_problem_set(slo_ctx* c, int32_t n, int32_t mb, const double* exec, const double* deadline) {
+    if (!c) return fail(SLO_ERR_ARG, "slo_problem_set: null context");
+    if (n < 1 || n > SLO_MAX_N) return fail(SLO_ERR_CAPACITY, "slo_problem_set: n must be in [1, 4096]");
+    if (mb < 1) return fail(SLO_ERR_DATA, "slo_problem_set: max_batch must be >= 1");
+    if (mb > SLO_MAX_MB) return fail(SLO_ERR_CAPACITY, "slo_problem_set: max_batch must be <= 16");
+    CK(cudaSetDevice(c->device));
+    const size_t total = (size_t)n * mb;
+    CK(c->tab.reserve(total * sizeof(double2)));
+    CK(c->exec_soa.reserve(total * sizeof(double)));
+    CK(c->dl_soa.reserve(total * sizeof(double)));
+    CK(cudaMemcpyAsync(c->exec_soa.p, exec, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->dl_soa.p, deadline, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    k_interleave<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>((int)total, c->exec_soa.as<double>(),
+                                                                           c->dl_soa.as<double>(), c->tab.as<double2>());
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(c->stream));
+    c->n = n;
+    c->mb = mb;
+    c->prepared = false;
+    return SLO_OK;
+}
+
+int slo_evaluate_batch(slo_ctx* c, int32_t count, const uint16_t* perms, const uint32_t* bits, int32_t* n_met,
+                       double* t, double* g) {
+    if (!c) return fail(SLO_ERR_ARG, "slo_evaluate_batch: null context");
+    if (c->n == 0) return fail(SLO_ERR_STATE, "slo_evaluate_batch: no problem set");
+    if (count <= 0) return SLO_OK;
+    const int n = c->n, words = (n + 31) / 32;
+    // validate on the host: every batch non-empty and <= mb, last bit set, indices in range
+    for (int k = 0; k < count; ++k) {
+        const uint16_t* pr = perms + (size_t)k * n;
+        const uint32_t* br = bits + (size_t)k * words;
+        if (!((br[(n - 1) >> 5] >> ((n - 1) & 31)) & 1u)) return fail(SLO_ERR_DATA, "slo_evaluate_batch: last position must end a batch");
+        int run = 0;
+        for (int q = 0; q < n; ++q) {
+            if (pr[q] >= n) return fail(SLO_ERR_DATA, "slo_evaluate_batch: dense index out of range");
+            ++run;
+            if ((br[q >> 5] >> (q & 31)) & 1u) {
+                if (run > c->mb) return fail(SLO_ERR_DATA, "slo_evaluate_batch: batch larger than max_batch");
+                run = 0;
+            }
+        }
+    }
+    CK(cudaSetDevice(c->device));
+    CK(c->e_perms.reserve((size_t)count * n * sizeof(uint16_t)));
+    CK(c->e_bits.reserve((size_t)count * words * sizeof(uint32_t)));
+    CK(c->e_n.reserve((size_t)count * sizeof(int)));
+    CK(c->e_t.reserve((size_t)count * sizeof(double)));
+    CK(c->e_g.reserve((size_t)count * sizeof(double)));
+    CK(cudaMemcpyAsync(c->e_perms.p, perms, (size_t)count * n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->e_bits.p, bits, (size_t)count * words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    k_eval_exact<<<(count + 127) / 128, 128, 0, c->stream>>>(count, n, words, c->e_perms.as<uint16_t>(),
+                                                               c->e_bits.as<uint32_t>(), c->tab.as<double2>(),
+                                                               c->e_n.as<int>(), c->e_t.as<double>(), c->e_g.as<double>());
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(n_met, c->e_n.p, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(t, c->e_t.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g, c->e_g.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    return SLO_OK;
+}
+
+}  // extern "C"
+
+namespace {
+
+int count_levels(double t0, double t_thres, double tau) {
+    int L = 0;
+    for (double t = t0; t >= t_thres; t *= tau) ++L;  // identical FP sequence to the device loop
+    return L;
+}
+
+template <int P>
+int configure_chains(slo_ctx* c) {
+    const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(double2);
+    const size_t slot = ((64 * P + 4 * P) + 15) & ~(size_t)15;
+    const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
+    c->smem_tab = tab_smem + slot <= c->smem_optin;
+    const size_t base = c->smem_tab ? tab_smem : 0;
+    int W = (int)std::min<size_t>(32, (c->smem_optin - base) / slot);
+    W = std::max(1, std::min(W, c->chain_count));
+    c->smem = base + (size_t)W * slot;
+    CK(cudaFuncSetAttribute(k_chains<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<P>, W * 32, c->smem));
+    if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
+    c->block = W * 32;
+    c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
+    return SLO_OK;
+}
+
+int launch_chains_P(slo_ctx* c) {
+    switch (c->P) {
+#define CASE(PP)                                                                                   \
+    case PP:                                                                                       \
+        k_chains<PP><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);                            \
+        break;
+        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128)
+#undef CASE
+        default:
+            return fail(SLO_ERR_CAPACITY, "bad P");
+    }
+    CK(cudaGetLastError());
+    return SLO_OK;
+}
+
+int configure_P(slo_ctx* c) {
+    switch (c->P) {
+        case 1: return configure_chains<1>(c);
+        case 2: return configure_chains<2>(c);
+        case 4: return configure_chains<4>(c);
+        case 8: return configure_chains<8>(c);
+        case 16: return configure_chains<16>(c);
+        case 32: return configure_chains<32>(c);
+        case 64: return configure_chains<64>(c);
+        case 128: return configure_chains<128>(c);
+    }
+    return fail(SLO_ERR_CAPACITY, "bad P");
+}
+
+}  // namespace
+
+extern "C" {
+
+int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* start_perm,
+                       const int32_t* start_sizes, int32_t start_nb) {
+    if (!c || !prm) return fail(SLO_ERR_ARG, "slo_chains_prepare: null argument");
+    if (c->n == 0) return fail(SLO_ERR_STATE, "slo_chains_prepare: no problem set");
+    if (!(prm->t0 > prm->t_thres) || !(prm->t_thres > 0.0) || prm->iter < 1 || !(prm->tau > 0.0) || !(prm->tau < 1.0))
+        return fail(SLO_ERR_DATA, "AnnealConfig: requires t0 > t_thres > 0, iter >= 1, tau in (0,1)");
+    if (!(prm->objective_scale >= 0.0)) return fail(SLO_ERR_DATA, "AnnealConfig: objective_scale must be >= 0");
+    const int n = c->n;
+    const int cb = prm->chain_begin, ce = prm->chain_end;
+    if (cb < 0 || ce <= cb || ce > prm->chains) return fail(SLO_ERR_ARG, "slo_chains_prepare: bad chain slice");
+    // validate the start schedule
+    {
+        std::vector<char> seen(n, 0);
+        int pos = 0;
+        for (int k = 0; k < start_nb; ++k) {
+            if (start_sizes[k] < 1 || start_sizes[k] > c->mb) return fail(SLO_ERR_DATA, "start schedule: bad batch size");
+            pos += start_sizes[k];
+        }
+        if (pos != n) return fail(SLO_ERR_DATA, "start schedule: sizes do not cover n");
+        for (int q = 0; q < n; ++q) {
+            if (start_perm[q] < 0 || start_perm[q] >= n || seen[start_perm[q]]) return fail(SLO_ERR_DATA, "start schedule: not a permutation");
+            seen[start_perm[q]] = 1;
+        }
+    }
+    CK(cudaSetDevice(c->device));
+    c->prm = *prm;
+    c->prm.scale_mult = nullptr;
+    c->chain_count = ce - cb;
+    c->levels = count_levels(prm->t0, prm->t_thres, prm->tau);
+    c->start_nb = start_nb;
+    c->prepared = false;
+
+    if (prm->rng_mode == SLO_RNG_XOSHIRO_REPLAY) {
+        const int chains = c->chain_count;
+        CK(c->r_scratch.reserve((size_t)chains * 3 * (2 * (size_t)n + 1) * sizeof(int)));
+        CK(c->r_best_perm.reserve((size_t)chains * n * sizeof(int)));
+        CK(c->r_best_sizes.reserve((size_t)chains * n * sizeof(int)));
+        CK(c->r_best_nb.reserve((size_t)chains * sizeof(int)));
+        CK(c->rec.reserve((size_t)chains * sizeof(ChainRec)));
+        CK(c->r_start_perm.reserve((size_t)n * sizeof(int)));
+        CK(c->r_start_sizes.reserve((size_t)n * sizeof(int)));
+        CK(c->result.reserve(sizeof(ChainResult)));
+        CK(cudaMemcpyAsync(c->r_start_perm.p, start_perm, (size_t)n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->r_start_sizes.p, start_sizes, (size_t)start_nb * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        ReplayParams& rp = c->rp;
+        rp.n = n, rp.mb = c->mb, rp.chains = chains, rp.tab = c->tab.as<double2>();
+        rp.t0 = prm->t0, rp.t_thres = prm->t_thres, rp.tau = prm->tau, rp.scale = prm->objective_scale;
+        rp.iter = prm->iter, rp.seed = prm->seed + (uint64_t)cb;
+        rp.start_perm = c->r_start_perm.as<int>(), rp.start_sizes = c->r_start_sizes.as<int>(), rp.start_nb = start_nb;
+        rp.scratch = c->r_scratch.as<int>(), rp.best_perm = c->r_best_perm.as<int>();
+        rp.best_sizes = c->r_best_sizes.as<int>(), rp.best_nb = c->r_best_nb.as<int>(), rp.rec = c->rec.as<ChainRec>();
+        c->prepared = true;
+        return SLO_OK;
+    }
+    if (prm->rng_mode != SLO_RNG_PHILOX) return fail(SLO_ERR_ARG, "slo_chains_prepare: unknown rng_mode");
+
+    const int P = pick_P(n);
+    c->P = P;
+    const size_t ent_words = 32 * (size_t)P, bit_words = P;
+    // start state in the lane-major entry layout
+    std::vector<uint16_t> ent(ent_words, 0);
+    std::vector<uint32_t> bits(bit_words, 0);
+    {
+        int pos = 0;
+        for (int k = 0; k < start_nb; ++k) {
+            for (int j = 0; j < start_sizes[k]; ++j, ++pos) {
+                const int phys = ((pos & (P - 1)) << 5) | (pos / P);
+                ent[phys] = (uint16_t)(start_perm[pos] | ((start_sizes[k] - 1) << 12));
+            }
+            bits[(pos - 1) >> 5] |= 1u << ((pos - 1) & 31);
+        }
+    }
+    const size_t cc = c->chain_count;
+    CK(c->start_ent.reserve(ent_words * sizeof(uint16_t)));
+    CK(c->start_bits.reserve(bit_words * sizeof(uint32_t)));
+    CK(c->best_ent.reserve(cc * ent_words * sizeof(uint16_t)));
+    CK(c->best_bits.reserve(cc * bit_words * sizeof(uint32_t)));
+    CK(c->rec.reserve(cc * sizeof(ChainRec)));
+    CK(c->result.reserve(sizeof(ChainResult)));
+    CK(c->win_ent.reserve(ent_words * sizeof(uint16_t)));
+    CK(c->win_bits.reserve(bit_words * sizeof(uint32_t)));
+    CK(c->scale_mult.reserve(std::max<size_t>(1, prm->n_scale_mult) * sizeof(double)));
+    if (int rc = configure_P(c)) return rc;
+    const int TW = c->grid * (c->block / 32);
+    const bool multi = (int)cc > TW;
+    if (multi) {
+        CK(c->st_ent.reserve(cc * ent_words * sizeof(uint16_t)));
+        CK(c->st_bits.reserve(cc * bit_words * sizeof(uint32_t)));
+    }
+    CK(cudaMemcpyAsync(c->start_ent.p, ent.data(), ent_words * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->start_bits.p, bits.data(), bit_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    if (prm->n_scale_mult > 0)
+        CK(cudaMemcpyAsync(c->scale_mult.p, prm->scale_mult, prm->n_scale_mult * sizeof(double), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
+
+    ChainParams& kp = c->kp;
+    kp.n = n, kp.mb = c->mb, kp.tab = c->tab.as<double2>(), kp.smem_tab = c->smem_tab ? 1 : 0;
+    kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;
+    kp.iter = prm->iter, kp.levels = c->levels;
+    kp.scale_mult = c->scale_mult.as<double>(), kp.n_mult = prm->n_scale_mult;
+    kp.key0 = (uint32_t)prm->seed, kp.key1 = (uint32_t)(prm->seed >> 32);
+    kp.chain_begin = cb, kp.chain_count = (int)cc;
+    kp.budget_ns = prm->budget_ns;
+    kp.start_ent = c->start_ent.as<uint16_t>(), kp.start_bits = c->start_bits.as<uint32_t>();
+    kp.st_ent = multi ? c->st_ent.as<uint16_t>() : nullptr, kp.st_bits = multi ? c->st_bits.as<uint32_t>() : nullptr;
+    kp.best_ent = c->best_ent.as<uint16_t>(), kp.best_bits = c->best_bits.as<uint32_t>();
+    kp.rec = c->rec.as<ChainRec>();
+    c->prepared = true;
+    return SLO_OK;
+}
+
+int slo_chains_launch(slo_ctx* c) {
+    if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_launch: not prepared");
+    CK(cudaSetDevice(c->device));
+    const size_t cc = c->chain_count;
+    CK(cudaMemsetAsync(c->rec.p, 0, cc * sizeof(ChainRec), c->stream));
+    CK(cudaEventRecord(c->ev0, c->stream));
+    if (c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY) {
+        k_replay<<<((int)cc + 31) / 32, 32, 0, c->stream>>>(c->rp);
+        CK(cudaGetLastError());
+        CK(cudaEventRecord(c->ev1, c->stream));
+        k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), 0, 0, nullptr,
+                                            nullptr, nullptr, nullptr);
+        CK(cudaGetLastError());
+        return SLO_OK;
+    }
+    int rc = launch_chains_P(c);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ev1, c->stream));
+    k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), 32 * c->P, c->P,
+                                        c->best_ent.as<uint16_t>(), c->best_bits.as<uint32_t>(),
+                                        c->win_ent.as<uint16_t>(), c->win_bits.as<uint32_t>());
+    CK(cudaGetLastError());
+    return SLO_OK;
+}
+
+int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb, slo_chain_result* out) {
+    if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_fetch: not prepared");
+    CK(cudaSetDevice(c->device));
+    ChainResult r;
+    CK(cudaMemcpyAsync(&r, c->result.p, sizeof r, cudaMemcpyDeviceToHost, c->stream));
+    const int n = c->n;
+    std::vector<uint16_t> ent;
+    std::vector<uint32_t> bits;
+    const bool replay = c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY;
+    if (!replay) {
+        ent.resize(32 * (size_t)c->P);
+        bits.resize(c->P);
+        CK(cudaMemcpyAsync(ent.data(), c->win_ent.p, ent.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(bits.data(), c->win_bits.p, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (r.chain < 0) return fail(SLO_ERR_STATE, "slo_chains_fetch: no chain ran (budget too small?)");
+    if (replay) {
+        int nb = 0;
+        CK(cudaMemcpy(&nb, c->r_best_nb.as<int>() + r.chain, sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(best_perm, c->r_best_perm.as<int>() + (size_t)r.chain * n, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(best_sizes, c->r_best_sizes.as<int>() + (size_t)r.chain * n, (size_t)nb * sizeof(int), cudaMemcpyDeviceToHost));
+        *best_nb = nb;
+    } else {
+        const int P = c->P;
+        int nb = 0, run = 0;
+        for (int q = 0; q < n; ++q) {
+            best_perm[q] = ent[((q & (P - 1)) << 5) | (q / P)] & 0xFFF;
+            ++run;
+            if ((bits[q >> 5] >> (q & 31)) & 1u) best_sizes[nb++] = run, run = 0;
+        }
+        *best_nb = nb;
+    }
+    if (out) {
+        out->g = r.g, out->t = r.t, out->n_met = r.n_met;
+        out->chain = c->prm.chain_begin + r.chain;
+        out->proposals = r.proposals, out->accepted = r.accepted;
+        out->chains_run = r.chains_run, out->levels_run = r.levels_min;
+        out->kernel_ms = ms;
+        out->positions_pass1 = r.scan1;
+        out->positions_pass2 = r.scan2;
+    }
+    return SLO_OK;
+}
+
+int slo_probe_smem_bandwidth(slo_ctx* c, double* gbytes_per_s) {
+    if (!c || !gbytes_per_s) return fail(SLO_ERR_ARG, "slo_probe_smem_bandwidth: null argument");
+    CK(cudaSetDevice(c->device));
+    const size_t smem = 4096 * sizeof(uint4);
+    CK(cudaFuncSetAttribute(k_smem_probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    DevBuf sink;
+    CK(sink.reserve(1024 * sizeof(uint4)));
+    const int grid = c->sm_count * 2, block = 1024, iters = 4096;
+    k_smem_probe<<<grid, block, smem, c->stream>>>(64, sink.as<uint4>());  // warm-up
+    CK(cudaGetLastError());
+    float best = 1e30f;
+    for (int rep = 0; rep < 5; ++rep) {
+        CK(cudaEventRecord(c->ev0, c->stream));
+        k_smem_probe<<<grid, block, smem, c->stream>>>(iters, sink.as<uint4>());
+        CK(cudaEventRecord(c->ev1, c->stream));
+        CK(cudaEventSynchronize(c->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+        best = std::min(best, ms);
+    }
+    const double bytes = (double)grid * block * iters * 8 * sizeof(uint4);
+    *gbytes_per_s = bytes / (best * 1e-3) / 1e9;
+    CK(cudaStreamSynchronize(c->stream));
+    return SLO_OK;
+}
+
+int slo_anneal_chains(slo_ctx* c, const slo_chain_params* prm, const int32_t* start_perm, const int32_t* start_sizes,
+                      int32_t start_nb, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
+                      slo_chain_result* result) {
+    int rc = slo_chains_prepare(c, prm, start_perm, start_sizes, start_nb);
+    if (rc) return rc;
+    rc = slo_chains_launch(c);
+    if (rc) return rc;
+    return slo_chains_fetch(c, best_perm, best_sizes, best_nb, result);
+}
+
+}  // extern "C"

@@ -1,0 +1,751 @@
+// Host side of the B200 scheduler: the reference-shaped C++ API of
+// include/slosched_b200.hpp. Everything O(N) or O(N log N) that the reference runs once
+// per anneal() call (candidates, shortcut, tables, final evaluation) stays on the host;
+// the O(proposals x N) annealing loop runs on the GPU through include/slosched_gpu.h.
+// There is no CPU fallback: an engine failure throws EngineError.
+// P: = /root/reference/proj/.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdlib>
+#include <limits>
+#include <memory>
+#include <mutex>
+#include <numeric>
+
+#include "slosched_b200.hpp"
+#include "slosched_gpu.h"
+
+namespace slosched {
+
+// ================================================================ domain validation
+// (semantics of P:src/core.cpp:8-170)
+SloSpec SloSpec::e2e(double ms) {
+    SloSpec s;
+    s.kind = SloKind::E2E;
+    s.e2e_ms = ms;
+    return s;
+}
+
+SloSpec SloSpec::ttft_tpot(double ttft, double tpot) {
+    SloSpec s;
+    s.kind = SloKind::TTFT_TPOT;
+    s.ttft_ms = ttft;
+    s.tpot_ms = tpot;
+    return s;
+}
+
+void SloSpec::validate() const {
+    if (kind == SloKind::E2E) {
+        if (!e2e_ms || !(*e2e_ms > 0.0)) throw DataError("SloSpec: E2E kind requires e2e_ms > 0");
+        return;
+    }
+    if (!ttft_ms || !(*ttft_ms > 0.0) || !tpot_ms || !(*tpot_ms > 0.0))
+        throw DataError("SloSpec: TTFT_TPOT kind requires ttft_ms > 0 and tpot_ms > 0");
+}
+
+void TaskClass::validate() const {
+    slo.validate();
+    if (auto g = std::get_if<GaussianPrior>(&output_prior)) {
+        if (!(g->std_tokens >= 0.0) || !std::isfinite(g->mean_tokens) || !std::isfinite(g->std_tokens))
+            throw DataError("TaskClass '" + name + "': Gaussian prior requires finite mean and std >= 0");
+    } else if (auto r = std::get_if<RangePrior>(&output_prior)) {
+        if (r->low < 1 || r->low > r->high)
+            throw DataError("TaskClass '" + name + "': range prior requires 1 <= low <= high");
+    }
+}
+
+void Request::validate() const {
+    const std::string who = "request " + std::to_string(id);
+    if (input_len < 1 || true_output_len < 1 || (predicted_output_len && *predicted_output_len < 1))
+        throw DataError(who + ": non-positive length");
+    if (!std::isfinite(arrival_time_ms) || arrival_time_ms < 0.0) throw DataError(who + ": invalid arrival time");
+}
+
+void LatencyCoefficients::validate() const {
+    for (double v : {alpha_p, beta_p, gamma_p, delta_p, alpha_d, beta_d, gamma_d, delta_d})
+        if (!std::isfinite(v)) throw DataError("LatencyCoefficients: non-finite value");
+    if (alpha_p < 0.0 || alpha_d < 0.0) throw DataError("LatencyCoefficients: alpha_p and alpha_d must be >= 0");
+}
+
+std::size_t Schedule::request_count() const {
+    std::size_t n = 0;
+    for (const auto& b : batches) n += b.size();
+    return n;
+}
+
+std::vector<int> Schedule::flatten() const {
+    std::vector<int> out;
+    out.reserve(request_count());
+    for (const auto& b : batches) out.insert(out.end(), b.begin(), b.end());
+    return out;
+}
+
+std::unordered_map<int, std::pair<int, int>> Schedule::positions() const {
+    std::unordered_map<int, std::pair<int, int>> out;
+    int pos = 0;
+    for (int k = 0; k < static_cast<int>(batches.size()); ++k)
+        for (int id : batches[k]) out[id] = {pos++, k};
+    return out;
+}
+
+bool Schedule::is_partition_of(const std::vector<int>& ids, int max_batch) const {
+    std::vector<int> got;
+    for (const auto& b : batches) {
+        if (b.empty() || (max_batch > 0 && static_cast<int>(b.size()) > max_batch)) return false;
+        got.insert(got.end(), b.begin(), b.end());
+    }
+    std::vector<int> want = ids;
+    if (got.size() != want.size()) return false;
+    std::sort(got.begin(), got.end());
+    std::sort(want.begin(), want.end());
+    return std::adjacent_find(got.begin(), got.end()) == got.end() && got == want;
+}
+
+void InstanceState::validate() const {
+    const std::string who = "instance " + std::to_string(id);
+    if (remaining_mem > total_mem) throw DataError(who + ": remaining_mem > total_mem");
+    if (!(mem_utility > 0.0) || mem_utility > 1.0) throw DataError(who + ": mem_utility must be in (0,1]");
+    if (!(bytes_per_token > 0.0)) throw DataError(who + ": bytes_per_token must be > 0");
+    if (max_batch_size < 1) throw DataError(who + ": max_batch_size must be >= 1");
+}
+
+const TaskClass& Workload::class_of(const Request& r) const {
+    auto it = class_index_.find(r.task_class_id);
+    if (it == class_index_.end())
+        throw DataError("request " + std::to_string(r.id) + ": unknown task_class_id " + std::to_string(r.task_class_id));
+    return classes[it->second];
+}
+
+const TaskClass* Workload::find_class(int class_id) const {
+    auto it = class_index_.find(class_id);
+    return it == class_index_.end() ? nullptr : &classes[it->second];
+}
+
+const Request* Workload::find_request(int request_id) const {
+    auto it = request_index_.find(request_id);
+    return it == request_index_.end() ? nullptr : &requests[it->second];
+}
+
+Workload validate_workload(std::vector<Request> requests, std::vector<TaskClass> classes) {
+    Workload w;
+    w.classes = std::move(classes);
+    w.requests = std::move(requests);
+    for (std::size_t i = 0; i < w.classes.size(); ++i) {
+        w.classes[i].validate();
+        if (!w.class_index_.emplace(w.classes[i].id, i).second)
+            throw DataError("duplicate task class id " + std::to_string(w.classes[i].id));
+    }
+    for (std::size_t i = 0; i < w.requests.size(); ++i) {
+        const Request& r = w.requests[i];
+        r.validate();
+        if (!w.request_index_.emplace(r.id, i).second) throw DataError("duplicate request id " + std::to_string(r.id));
+        if (!w.class_index_.count(r.task_class_id))
+            throw DataError("request " + std::to_string(r.id) + ": unknown task_class_id " + std::to_string(r.task_class_id));
+    }
+    return w;
+}
+
+// ================================================================ rng (P:include/slosched/rng.hpp)
+namespace {
+std::uint64_t splitmix_finalize(std::uint64_t z) {
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+    return z ^ (z >> 31);
+}
+std::uint64_t rotl(std::uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+}  // namespace
+
+Rng::Rng(std::uint64_t seed) {
+    std::uint64_t z = seed;
+    for (auto& s : s_) s = splitmix_finalize(z += 0x9e3779b97f4a7c15ULL);
+}
+
+std::uint64_t Rng::next_u64() {
+    const std::uint64_t out = rotl(s_[0] + s_[3], 23) + s_[0];
+    const std::uint64_t t = s_[1] << 17;
+    s_[2] ^= s_[0];
+    s_[3] ^= s_[1];
+    s_[1] ^= s_[2];
+    s_[0] ^= s_[3];
+    s_[2] ^= t;
+    s_[3] = rotl(s_[3], 45);
+    return out;
+}
+
+double Rng::uniform() { return static_cast<double>(next_u64() >> 11) * 0x1.0p-53; }
+
+std::uint64_t Rng::uniform_index(std::uint64_t n) {
+    unsigned __int128 m = static_cast<unsigned __int128>(next_u64()) * n;
+    if (static_cast<std::uint64_t>(m) < n) {
+        const std::uint64_t floor = (0 - n) % n;
+        while (static_cast<std::uint64_t>(m) < floor) m = static_cast<unsigned __int128>(next_u64()) * n;
+    }
+    return static_cast<std::uint64_t>(m >> 64);
+}
+
+double Rng::normal() {
+    double u1 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    const double u2 = uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(2.0 * M_PI * u2);
+}
+
+std::uint64_t Rng::derive(std::uint64_t seed, std::uint64_t stream) {
+    return splitmix_finalize(seed + 0x9e3779b97f4a7c15ULL * (stream + 1));
+}
+
+// ================================================================ latency model
+// Eq. 14-19; operand order as P:src/latency_model.cpp:86-113 so the
+// tables are bit-identical to the reference's.
+double predict_prefill(const LatencyCoefficients& c, int b, int input_len) {
+    const double bd = b, ld = input_len;
+    return c.alpha_p * bd * ld + c.beta_p * bd + c.gamma_p * ld + c.delta_p;
+}
+
+double predict_per_token_decode(const LatencyCoefficients& c, int b, int accumulated_len) {
+    const double bd = b, ld = accumulated_len;
+    return c.alpha_d * bd * ld + c.beta_d * bd + c.gamma_d * ld + c.delta_d;
+}
+
+double predict_decode_total(const LatencyCoefficients& c, int b, int input_len, int output_len) {
+    const double bd = b, li = input_len, lo = output_len;
+    const double per_token_slope = c.alpha_d * bd + c.gamma_d;
+    const double summed_len = lo * li + lo * (lo + 1.0) / 2.0;
+    return per_token_slope * summed_len + lo * (c.beta_d * bd + c.delta_d);
+}
+
+double predict_exec(const LatencyCoefficients& c, int b, int input_len, int output_len) {
+    return predict_prefill(c, b, input_len) + predict_decode_total(c, b, input_len, output_len);
+}
+
+double predict_tpot(const LatencyCoefficients& c, int b, int input_len, int output_len) {
+    if (output_len <= 0) throw std::invalid_argument("predict_tpot: TPOT undefined for zero output");
+    return predict_decode_total(c, b, input_len, output_len) / static_cast<double>(output_len);
+}
+
+LatencyCoefficients table_coefficients() { return {0.1, 5.7, 0.01, 43.67, 0.0002, 0.275, 0.00088, 15.85}; }
+
+// ================================================================ objective
+// (P:src/objective.cpp:7-82)
+namespace {
+const Request& require_predicted(const Workload& w, int id, const char* what) {
+    const Request* r = w.find_request(id);
+    if (!r) throw DataError(std::string(what) + " references unknown request " + std::to_string(id));
+    if (!r->predicted_output_len) throw DataError("request " + std::to_string(id) + " missing predicted length");
+    return *r;
+}
+double max_of(double a, double b) { return a < b ? b : a; }  // std::max semantics
+}  // namespace
+
+std::vector<ExecProfile> batch_exec_profile(const Schedule& s, const LatencyCoefficients& c, const Workload& w) {
+    std::vector<ExecProfile> out;
+    out.reserve(s.request_count());
+    for (const auto& batch : s.batches) {
+        const int b = static_cast<int>(batch.size());
+        for (int id : batch) {
+            const Request& r = require_predicted(w, id, "schedule");
+            const int lo = *r.predicted_output_len;
+            out.push_back({id, predict_exec(c, b, r.input_len, lo), predict_prefill(c, b, r.input_len),
+                           predict_tpot(c, b, r.input_len, lo), is_extrapolated(r.input_len, lo)});
+        }
+    }
+    return out;
+}
+
+std::vector<double> waiting_times(const Schedule& s, const std::vector<ExecProfile>& profiles) {
+    std::vector<double> waits;
+    waits.reserve(profiles.size());
+    double elapsed = 0.0;
+    std::size_t i = 0;
+    for (const auto& batch : s.batches) {
+        double makespan = 0.0;
+        for (std::size_t k = 0; k < batch.size(); ++k, ++i) {
+            waits.push_back(elapsed);
+            makespan = max_of(makespan, profiles[i].exec_ms);
+        }
+        elapsed += makespan;
+    }
+    return waits;
+}
+
+bool meets_slo(const SloSpec& slo, double e2e_ms, double ttft_ms, double tpot_ms) {
+    if (slo.kind == SloKind::E2E) return e2e_ms <= *slo.e2e_ms;
+    return ttft_ms <= *slo.ttft_ms && tpot_ms <= *slo.tpot_ms;
+}
+
+EvaluatedSchedule evaluate(const Schedule& s, const LatencyCoefficients& c, const Workload& w) {
+    EvaluatedSchedule ev;
+    ev.schedule = s;
+    const auto prof = batch_exec_profile(s, c, w);
+    const auto waits = waiting_times(s, prof);
+    ev.per_request.reserve(prof.size());
+    for (std::size_t i = 0; i < prof.size(); ++i) {
+        RequestMetrics m;
+        m.request_id = prof[i].request_id;
+        m.wait_ms = waits[i];
+        m.exec_ms = prof[i].exec_ms;
+        m.e2e_ms = prof[i].exec_ms + waits[i];
+        m.ttft_ms = prof[i].prefill_ms + waits[i];
+        m.tpot_ms = prof[i].tpot_ms;
+        m.extrapolated = prof[i].extrapolated;
+        m.slo_met = meets_slo(w.class_of(*w.find_request(m.request_id)).slo, m.e2e_ms, m.ttft_ms, m.tpot_ms);
+        ev.n += m.slo_met ? 1 : 0;
+        ev.t_ms += m.e2e_ms;
+        ev.per_request.push_back(m);
+    }
+    ev.g = ev.t_ms > 0.0 ? static_cast<double>(ev.n) / ev.t_ms : 0.0;
+    return ev;
+}
+
+// ================================================================ priority mapper
+void AnnealConfig::validate() const {
+    if (!(t0 > t_thres) || !(t_thres > 0.0)) throw DataError("AnnealConfig: requires t0 > t_thres > 0");
+    if (iter < 1) throw DataError("AnnealConfig: iter must be >= 1");
+    if (!(tau > 0.0) || !(tau < 1.0)) throw DataError("AnnealConfig: tau must be in (0,1)");
+    if (objective_scale && !(*objective_scale >= 0.0)) throw DataError("AnnealConfig: objective_scale must be >= 0");
+    if (engine.mode == SearchMode::Chains && engine.chains < 1) throw DataError("AnnealConfig: engine.chains must be >= 1");
+    if (!(engine.budget_ms >= 0.0)) throw DataError("AnnealConfig: engine.budget_ms must be >= 0");
+    for (double m : engine.scale_ladder)
+        if (!(m >= 0.0)) throw DataError("AnnealConfig: scale_ladder entries must be >= 0");
+}
+
+double latest_start(double s, double c) {
+    double d = s - c;
+    if (std::isnan(d)) return -std::numeric_limits<double>::infinity();
+    if (std::isinf(d)) return d;
+    while (d + c > s) d = std::nextafter(d, -std::numeric_limits<double>::infinity());
+    for (;;) {
+        const double up = std::nextafter(d, std::numeric_limits<double>::infinity());
+        if (up + c <= s && up != d) d = up;
+        else break;
+    }
+    return d;
+}
+
+namespace {
+
+Schedule pack_greedy(const std::vector<int>& ordered, int max_batch) {
+    Schedule s;
+    for (std::size_t i = 0; i < ordered.size(); i += max_batch)
+        s.batches.emplace_back(ordered.begin() + i, ordered.begin() + std::min(ordered.size(), i + max_batch));
+    return s;
+}
+
+// (key, id) pairs sorted ascending -- the comparator of P:src/priority_mapper.cpp:297-308
+// evaluated once per id instead of inside every comparison
+std::vector<int> order_by(std::vector<std::pair<double, int>> keyed) {
+    std::sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) {
+        return a.first != b.first ? a.first < b.first : a.second < b.second;
+    });
+    std::vector<int> out;
+    out.reserve(keyed.size());
+    for (const auto& kv : keyed) out.push_back(kv.second);
+    return out;
+}
+
+}  // namespace
+
+std::pair<Schedule, Schedule> initial_candidates(const Workload& w, const std::vector<int>& ids,
+                                                 const LatencyCoefficients& c, int max_batch) {
+    std::vector<std::pair<double, int>> by_exec, by_arrival;
+    by_exec.reserve(ids.size());
+    by_arrival.reserve(ids.size());
+    for (int id : ids) {
+        const Request& r = require_predicted(w, id, "initial_candidates");
+        by_exec.emplace_back(predict_exec(c, max_batch, r.input_len, *r.predicted_output_len), id);
+        by_arrival.emplace_back(r.arrival_time_ms, id);
+    }
+    return {pack_greedy(order_by(std::move(by_exec)), max_batch), pack_greedy(order_by(std::move(by_arrival)), max_batch)};
+}
+
+std::optional<EvaluatedSchedule> shortcut_check(const Schedule& sorted_schedule, const LatencyCoefficients& c,
+                                                const Workload& w) {
+    EvaluatedSchedule ev = evaluate(sorted_schedule, c, w);
+    if (ev.n == static_cast<int>(ev.per_request.size())) return ev;
+    return std::nullopt;
+}
+
+// Schedule-level moves with the reference's draw discipline (P:src/priority_mapper.cpp:41-90,322-338)
+namespace {
+
+std::pair<int, int> locate(const Schedule& s, std::size_t flat_pos) {
+    for (int k = 0; k < static_cast<int>(s.batches.size()); ++k) {
+        if (flat_pos < s.batches[k].size()) return {k, static_cast<int>(flat_pos)};
+        flat_pos -= s.batches[k].size();
+    }
+    return {-1, -1};
+}
+
+void drop_if_empty(Schedule& s, int k) {
+    if (s.batches[k].empty()) s.batches.erase(s.batches.begin() + k);
+}
+
+std::optional<Schedule> move_squeeze(const Schedule& s, Rng& rng, int max_batch) {
+    if (s.batches.size() < 2) return std::nullopt;
+    const std::size_t head = s.batches.front().size();
+    const auto [k, j] = locate(s, head + rng.uniform_index(s.request_count() - head));
+    if (static_cast<int>(s.batches[k - 1].size()) >= max_batch) return std::nullopt;
+    Schedule out = s;
+    out.batches[k - 1].push_back(out.batches[k][j]);
+    out.batches[k].erase(out.batches[k].begin() + j);
+    drop_if_empty(out, k);
+    return out;
+}
+
+std::optional<Schedule> move_delay(const Schedule& s, Rng& rng, int max_batch) {
+    const std::size_t n = s.request_count();
+    if (n == 0) return std::nullopt;
+    const auto [k, j] = locate(s, rng.uniform_index(n));
+    const bool has_next = k + 1 < static_cast<int>(s.batches.size());
+    if (has_next && static_cast<int>(s.batches[k + 1].size()) >= max_batch) return std::nullopt;
+    Schedule out = s;
+    const int id = out.batches[k][j];
+    if (has_next) out.batches[k + 1].push_back(id);
+    else out.batches.push_back({id});
+    out.batches[k].erase(out.batches[k].begin() + j);
+    drop_if_empty(out, k);
+    return out;
+}
+
+std::optional<Schedule> move_swap(const Schedule& s, Rng& rng) {
+    const std::size_t n = s.request_count();
+    if (n < 2) return std::nullopt;
+    const std::size_t a = rng.uniform_index(n);
+    std::size_t b = rng.uniform_index(n - 1);
+    if (b >= a) ++b;
+    const auto la = locate(s, a), lb = locate(s, b);
+    Schedule out = s;
+    std::swap(out.batches[la.first][la.second], out.batches[lb.first][lb.second]);
+    return out;
+}
+
+}  // namespace
+
+Schedule neighbor(const Schedule& s, Rng& rng, int max_batch) {
+    if (s.request_count() == 0) return s;
+    for (int attempt = 0; attempt < 8; ++attempt) {
+        std::optional<Schedule> out;
+        switch (rng.uniform_index(3)) {
+            case 0: out = move_squeeze(s, rng, max_batch); break;
+            case 1: out = move_delay(s, rng, max_batch); break;
+            default: out = move_swap(s, rng); break;
+        }
+        if (out) return std::move(*out);
+    }
+    if (auto out = move_swap(s, rng)) return std::move(*out);
+    return s;
+}
+
+// ---------------------------------------------------------------- engine contexts
+namespace {
+
+struct CtxDeleter {
+    void operator()(slo_ctx* c) const { slo_ctx_destroy(c); }
+};
+using CtxPtr = std::unique_ptr<slo_ctx, CtxDeleter>;
+
+// A small pool of engine contexts per device, so concurrent anneal() calls (allowed by
+// the reference contract) each own a context while they run.
+class CtxPool {
+public:
+    static CtxPool& get() {
+        static CtxPool* pool = new CtxPool();  // leaked on purpose: no CUDA teardown at exit
+        return *pool;
+    }
+    CtxPtr acquire(int device) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            auto& v = free_[device];
+            if (!v.empty()) {
+                CtxPtr c(v.back());
+                v.pop_back();
+                return c;
+            }
+        }
+        slo_ctx* c = nullptr;
+        if (slo_ctx_create(device, &c) != SLO_OK) throw EngineError(std::string("B200 engine: ") + slo_last_error());
+        return CtxPtr(c);
+    }
+    void release(int device, CtxPtr c) {
+        std::lock_guard<std::mutex> g(mu_);
+        free_[device].push_back(c.release());
+    }
+
+private:
+    std::mutex mu_;
+    std::unordered_map<int, std::vector<slo_ctx*>> free_;
+};
+
+int resolve_device(int requested) {
+    if (requested >= 0) return requested;
+    if (const char* e = std::getenv("SLOSCHED_DEVICE")) return std::atoi(e);
+    return 0;
+}
+
+void engine_check(int rc) {
+    if (rc == SLO_OK) return;
+    const std::string msg = slo_last_error();
+    if (rc == SLO_ERR_DATA) throw DataError(msg);
+    if (rc == SLO_ERR_CAPACITY) throw CapacityError(msg);
+    if (rc == SLO_ERR_ARG) throw std::invalid_argument(msg);
+    throw EngineError("B200 engine: " + msg);
+}
+
+}  // namespace
+
+void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c, int max_batch,
+                 std::vector<double>& exec, std::vector<double>& deadline) {
+    std::vector<int> sorted_ids = ids;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    if (std::adjacent_find(sorted_ids.begin(), sorted_ids.end()) != sorted_ids.end())
+        throw DataError("duplicate request id in the request set");
+    const int n = static_cast<int>(sorted_ids.size());
+    exec.assign((std::size_t)n * max_batch, 0.0);
+    deadline.assign((std::size_t)n * max_batch, 0.0);
+    for (int i = 0; i < n; ++i) {
+        const Request& r = require_predicted(w, sorted_ids[i], "anneal");
+        const SloSpec& slo = w.class_of(r).slo;
+        const int lo = *r.predicted_output_len;
+        for (int b = 1; b <= max_batch; ++b) {
+            const double e = predict_exec(c, b, r.input_len, lo);
+            double d;
+            if (slo.kind == SloKind::E2E) {
+                d = latest_start(*slo.e2e_ms, e);
+            } else {
+                const double tp = predict_tpot(c, b, r.input_len, lo);
+                d = tp <= *slo.tpot_ms ? latest_start(*slo.ttft_ms, predict_prefill(c, b, r.input_len))
+                                       : -std::numeric_limits<double>::infinity();
+            }
+            exec[(std::size_t)(b - 1) * n + i] = e;
+            deadline[(std::size_t)(b - 1) * n + i] = d;
+        }
+    }
+}
+
+AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
+                    const AnnealConfig& cfg, int max_batch) {
+    cfg.validate();
+    if (max_batch < 1) throw DataError("anneal: max_batch must be >= 1");
+    AnnealResult res;
+    auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
+    EvaluatedSchedule ev_sorted = evaluate(sorted_s, c, w);
+    res.stats.g_sorted_start = ev_sorted.g;
+    if (ev_sorted.n == static_cast<int>(ev_sorted.per_request.size())) {  // shortcut, :350-354
+        res.stats.shortcut = true;
+        res.best = std::move(ev_sorted);
+        return res;
+    }
+    EvaluatedSchedule ev_input = evaluate(input_s, c, w);
+    res.stats.g_input_start = ev_input.g;
+
+    // CostModel tables over dense indices (rank of the sorted id), :205-231, with the SLO
+    // test folded into a per-(batch size, request) deadline
+    const int n = static_cast<int>(ids.size());
+    if (n > SLO_MAX_N) throw CapacityError("anneal: " + std::to_string(n) + " requests exceed the engine limit of 4096");
+    if (max_batch > SLO_MAX_MB) throw CapacityError("anneal: max_batch above the engine limit of 16");
+    std::vector<int> sorted_ids = ids;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    std::vector<double> exec, deadline;
+    cost_tables(w, ids, c, max_batch, exec, deadline);
+    const bool use_sorted = ev_sorted.g >= ev_input.g;
+    const Schedule& start = use_sorted ? sorted_s : input_s;
+    std::vector<int> start_perm, start_sizes;
+    start_perm.reserve(n);
+    for (const auto& b : start.batches) {
+        start_sizes.push_back(static_cast<int>(b.size()));
+        for (int id : b)
+            start_perm.push_back(static_cast<int>(std::lower_bound(sorted_ids.begin(), sorted_ids.end(), id) - sorted_ids.begin()));
+    }
+    // score(start) == evaluate(start).g bit-for-bit (same operand order), :362-370
+    const double f = use_sorted ? ev_sorted.g : ev_input.g;
+    const double scale = cfg.objective_scale ? *cfg.objective_scale : (f > 0.0 ? cfg.t0 / f : cfg.t0);
+    res.stats.objective_scale_used = scale;
+
+    const EngineOptions& eo = cfg.engine;
+    slo_chain_params prm{};
+    prm.t0 = cfg.t0;
+    prm.t_thres = cfg.t_thres;
+    prm.iter = cfg.iter;
+    prm.tau = cfg.tau;
+    prm.seed = cfg.seed;
+    prm.objective_scale = scale;
+    prm.rng_mode = eo.mode == SearchMode::Replay ? SLO_RNG_XOSHIRO_REPLAY : SLO_RNG_PHILOX;
+    prm.chains = eo.mode == SearchMode::Replay ? 1 : eo.chains;
+    prm.chain_begin = eo.mode == SearchMode::Replay ? 0 : eo.chain_begin;
+    prm.chain_end = eo.mode == SearchMode::Replay ? 1 : (eo.chain_end < 0 ? eo.chains : eo.chain_end);
+    prm.budget_ns = static_cast<int64_t>(eo.budget_ms * 1e6);
+    prm.n_scale_mult = static_cast<int32_t>(eo.scale_ladder.size());
+    prm.scale_mult = eo.scale_ladder.empty() ? nullptr : eo.scale_ladder.data();
+
+    const int device = resolve_device(eo.device);
+    CtxPtr ctx = CtxPool::get().acquire(device);
+    std::vector<int> best_perm(n), best_sizes(n);
+    int best_nb = 0;
+    slo_chain_result cr{};
+    engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
+    engine_check(slo_anneal_chains(ctx.get(), &prm, start_perm.data(), start_sizes.data(),
+                                   static_cast<int>(start_sizes.size()), best_perm.data(), best_sizes.data(), &best_nb,
+                                   &cr));
+    CtxPool::get().release(device, std::move(ctx));
+
+    res.stats.proposals = cr.proposals;
+    res.stats.accepted = cr.accepted;
+    res.stats.chains_run = cr.chains_run;
+    res.stats.levels_run = cr.levels_run;
+    res.stats.best_chain = cr.chain;
+    res.stats.engine_g = cr.g;
+    res.stats.kernel_ms = cr.kernel_ms;
+
+    Schedule best;
+    int pos = 0;
+    for (int k = 0; k < best_nb; ++k) {
+        Batch b;
+        for (int j = 0; j < best_sizes[k]; ++j) b.push_back(sorted_ids[best_perm[pos++]]);
+        best.batches.push_back(std::move(b));
+    }
+    // final evaluation through the objective; both starts stay a floor, :404-410
+    EvaluatedSchedule ev_best = evaluate(best, c, w);
+    if (ev_best.g >= std::max(ev_sorted.g, ev_input.g)) res.best = std::move(ev_best);
+    else res.best = use_sorted ? std::move(ev_sorted) : std::move(ev_input);
+    return res;
+}
+
+// ================================================================ scheduler (P:src/scheduler.cpp)
+long long token_capacity(std::uint64_t remaining, double mu, double sigma) {
+    if (!(sigma > 0.0)) throw std::invalid_argument("token_capacity: sigma must be > 0");
+    if (!(mu > 0.0) || mu > 1.0) throw std::invalid_argument("token_capacity: mu must be in (0,1]");
+    return static_cast<long long>(std::floor(static_cast<double>(remaining) * mu / sigma));
+}
+
+AssignmentResult assign_instances(const Workload& w, const std::vector<InstanceState>& instances,
+                                  const LatencyCoefficients& c) {
+    if (instances.empty()) throw DataError("assign_instances: need at least one instance");
+    for (const auto& inst : instances) inst.validate();
+    std::vector<std::pair<double, int>> keyed;
+    keyed.reserve(w.requests.size());
+    for (const auto& r : w.requests) {
+        if (!r.predicted_output_len) throw DataError("assign_instances: request missing predicted length");
+        keyed.emplace_back(predict_exec(c, 1, r.input_len, *r.predicted_output_len), r.id);
+    }
+    const std::vector<int> order = order_by(std::move(keyed));
+    const std::size_t k = instances.size();
+    std::vector<double> remaining(k);
+    for (std::size_t i = 0; i < k; ++i) remaining[i] = static_cast<double>(instances[i].remaining_mem);
+    auto roomiest = [&]() {
+        std::size_t best = 0;
+        long long best_cap = -1;
+        for (std::size_t i = 0; i < k; ++i) {
+            const long long cap = token_capacity(static_cast<std::uint64_t>(remaining[i]), instances[i].mem_utility,
+                                                 instances[i].bytes_per_token);
+            if (i == 0 || cap > best_cap) best = i, best_cap = cap;
+        }
+        return std::pair<std::size_t, long long>{best, best_cap};
+    };
+    AssignmentResult res;
+    res.per_instance.resize(k);
+    for (int id : order) {
+        const Request& r = *w.find_request(id);
+        const long long need = r.input_len + *r.predicted_output_len;
+        auto [inst, cap] = roomiest();
+        if (cap < need) {  // new epoch: memory resets to totals
+            for (std::size_t i = 0; i < k; ++i) remaining[i] = static_cast<double>(instances[i].total_mem);
+            res.epochs++;
+            std::tie(inst, cap) = roomiest();
+            if (cap < need) throw CapacityError("request " + std::to_string(id) + " cannot fit any instance");
+        }
+        res.per_instance[inst].push_back(id);
+        remaining[inst] -= static_cast<double>(need) * instances[inst].bytes_per_token / instances[inst].mem_utility;
+        if (remaining[inst] < 0.0) remaining[inst] = 0.0;
+    }
+    return res;
+}
+
+std::optional<Batch> dispatch(InstanceQueue& q, bool ready) {
+    if (!ready || q.pending.empty()) return std::nullopt;
+    Batch next = std::move(q.pending.front());
+    q.pending.pop_front();
+    return next;
+}
+
+ScheduleAllResult schedule_all(const Workload& w, const std::vector<InstanceState>& instances,
+                               const LatencyCoefficients& c, const AnnealConfig& cfg, Policy policy,
+                               int /*exhaustive_cap*/) {
+    if (policy == Policy::FCFS) throw std::invalid_argument("schedule_all: FCFS is a simulator baseline, not a mapper policy");
+    if (policy == Policy::EXHAUSTIVE)
+        throw std::invalid_argument("schedule_all: the exhaustive oracle is not part of the B200 engine (see DESIGN.md)");
+    const auto t_start = std::chrono::steady_clock::now();
+    ScheduleAllResult res;
+    res.assignment = assign_instances(w, instances, c);
+    const std::size_t k = instances.size();
+    res.per_instance.resize(k);
+    res.stats.resize(k);
+    res.queues.resize(k);
+    for (std::size_t i = 0; i < k; ++i) {
+        AnnealConfig per = cfg;
+        per.seed = Rng::derive(cfg.seed, static_cast<std::uint64_t>(instances[i].id));
+        AnnealResult ar = anneal(w, res.assignment.per_instance[i], c, per, instances[i].max_batch_size);
+        res.per_instance[i] = std::move(ar.best);
+        res.stats[i] = ar.stats;
+        for (const auto& b : res.per_instance[i].schedule.batches) res.queues[i].pending.push_back(b);
+    }
+    res.overhead_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+    return res;
+}
+
+// ================================================================ synthetic inputs
+// (P:src/workload.cpp:138-183, P:src/output_estimator.cpp:361-415)
+std::pair<TaskClass, TaskClass> default_slo_classes() {
+    TaskClass code{0, "code", SloSpec::e2e(30000.0), {}};
+    TaskClass chat{1, "chat", SloSpec::ttft_tpot(10000.0, 50.0), {}};
+    return {code, chat};
+}
+
+std::pair<TaskClass, TaskClass> default_synth_classes(const LengthDists& d) {
+    auto [code, chat] = default_slo_classes();
+    code.output_prior = GaussianPrior{d.code_output_mean, d.code_output_std};
+    chat.output_prior = GaussianPrior{d.chat_output_mean, d.chat_output_std};
+    return {code, chat};
+}
+
+namespace {
+int clamp_tokens(double v) { return std::clamp(static_cast<int>(std::llround(v)), 1, kValidatedMaxLen); }
+int at_least_one(double v) { return std::max(1, static_cast<int>(std::llround(v))); }
+}  // namespace
+
+std::vector<Request> generate_mixed(int n, std::uint64_t seed, const TaskClass& code_class, const TaskClass& chat_class,
+                                    const LengthDists& d) {
+    Rng rng(seed);
+    const int n_code = (n + 1) / 2;
+    std::vector<Request> out;
+    out.reserve(static_cast<std::size_t>(std::max(n, 0)));
+    for (int i = 0; i < n; ++i) {
+        const bool code = i < n_code;
+        Request r;
+        r.task_class_id = code ? code_class.id : chat_class.id;
+        const double median = code ? d.code_input_median : d.chat_input_median;
+        const double sigma = code ? d.code_input_sigma : d.chat_input_sigma;
+        r.input_len = clamp_tokens(median * std::exp(sigma * rng.normal()));
+        r.true_output_len = clamp_tokens(rng.normal(code ? d.code_output_mean : d.chat_output_mean,
+                                                    code ? d.code_output_std : d.chat_output_std));
+        out.push_back(r);
+    }
+    rng.shuffle(out);
+    for (int i = 0; i < n; ++i) out[i].id = i;
+    return out;
+}
+
+void assign_predicted_lengths_from_priors(std::vector<Request>& reqs, const std::vector<TaskClass>& classes, Rng& rng) {
+    for (auto& r : reqs) {
+        if (r.predicted_output_len) continue;
+        const TaskClass* cls = nullptr;
+        for (const auto& c : classes)
+            if (c.id == r.task_class_id) cls = &c;
+        if (!cls) throw DataError("estimator: unknown task_class_id " + std::to_string(r.task_class_id));
+        if (auto g = std::get_if<GaussianPrior>(&cls->output_prior)) r.predicted_output_len = at_least_one(rng.normal(g->mean_tokens, g->std_tokens));
+        else if (auto rp = std::get_if<RangePrior>(&cls->output_prior)) r.predicted_output_len = static_cast<int>(rng.uniform_int(rp->low, rp->high));
+        else r.predicted_output_len = 256;
+    }
+}
+
+}  // namespace slosched

@@ -1,0 +1,271 @@
+"""GPU parity: the CUDA path (through the C ABI) against the oracle and the golden vectors.
+
+1. K1 slo_evaluate_batch vs the oracle's CostModel::score -- n_met, t, g bit-exact.
+2. K2 replay (xoshiro) vs the reference walk -- identical final schedule, n, t, g,
+   proposals and accepted counts (golden vectors + live oracle port, many seeds).
+3. K3/K4 chains (Philox) -- valid partitions, never below either start, deterministic,
+   independent of how chains are sliced, engine objective == exact objective, attainment
+   >= the reference's single chain.
+"""
+import numpy as np
+import pytest
+
+from conftest import golden, unhex
+from oracle import TABLE_COEFFS, FlatWorkload
+
+import paper_2504_14966_b200 as S
+from paper_2504_14966_b200 import engine as E
+
+pytestmark = pytest.mark.gpu
+
+
+def _flat(w: S.Workload) -> FlatWorkload:
+    a = w.arrays
+    return FlatWorkload(id=a["id"], cls=a["cls"], in_len=a["in_len"], true_out=a["true_out"], pred_out=a["pred_out"],
+                        arrival=a["arrival"], class_id=a["class_id"], kind=a["kind"], e2e=a["e2e"], ttft=a["ttft"],
+                        tpot=a["tpot"])
+
+
+def _three_class(n, seed):
+    """Config-1 style queue: code (E2E 30 s) / chat (TTFT 10 s + TPOT 50 ms) / offline (E2E 1e9)."""
+    base = S.generate_mixed(n, seed)
+    code, chat = S.default_slo_classes()
+    offline = S.TaskClass(2, "offline", S.SloSpec.e2e(1e9))
+    reqs = [S.Request(r.id, 2 if r.id % 3 == 2 else r.task_class_id, r.input_len, r.true_output_len,
+                      r.predicted_output_len) for r in base.requests]
+    return S.Workload(reqs, [code, chat, offline])
+
+
+def _random_partitions(rs, n, mb, count):
+    perms = np.stack([rs.permutation(n) for _ in range(count)]).astype(np.uint16)
+    sizes = []
+    for _ in range(count):
+        s, left = [], n
+        while left:
+            k = int(rs.integers(1, min(mb, left) + 1))
+            s.append(k)
+            left -= k
+        sizes.append(s)
+    return perms, sizes
+
+
+@pytest.fixture(scope="module")
+def eng():
+    e = E.Engine(0)
+    yield e
+    e.close()
+
+
+# ---------------------------------------------------------------- K1
+@pytest.mark.parametrize("n,mb,count", [(1, 1, 4), (8, 2, 500), (64, 4, 2000), (256, 8, 20000), (1024, 4, 2000),
+                                        (300, 16, 500), (4096, 4, 64)])
+def test_evaluate_batch_bit_exact(eng, port, n, mb, count):
+    w = _three_class(n, 1000 + n)
+    c = S.table_coefficients()
+    ex, dl = E.build_tables(w, w.ids(), c, mb)
+    eng.set_problem(ex, dl)
+    rs = np.random.default_rng(n * mb)
+    perms, sizes = _random_partitions(rs, n, mb, count)
+    n_met, t, g = eng.evaluate_batch(perms, E.end_bits(sizes, n))
+    o_n, o_t, o_g = port.score_batch(_flat(w), TABLE_COEFFS, sorted(w.ids()), mb, perms.astype(np.int32), sizes)
+    np.testing.assert_array_equal(n_met, o_n)
+    np.testing.assert_array_equal(t, o_t)  # bit-exact, not approx
+    np.testing.assert_array_equal(g, o_g)
+
+
+def test_evaluate_batch_matches_public_evaluate(eng):
+    w = S.generate_mixed(100, 5)
+    c = S.table_coefficients()
+    ex, dl = E.build_tables(w, w.ids(), c, 4)
+    eng.set_problem(ex, dl)
+    rs = np.random.default_rng(9)
+    perms, sizes = _random_partitions(rs, 100, 4, 50)
+    n_met, t, g = eng.evaluate_batch(perms, E.end_bits(sizes, 100))
+    ids = sorted(w.ids())
+    for q in range(50):
+        flat = [ids[i] for i in perms[q]]
+        batches, pos = [], 0
+        for s in sizes[q]:
+            batches.append(flat[pos:pos + s])
+            pos += s
+        ev = S.evaluate(S.Schedule(batches), c, w)
+        assert (ev.n, ev.t_ms, ev.g) == (n_met[q], t[q], g[q])
+
+
+def test_evaluate_batch_rejects_bad_input(eng):
+    w = S.generate_mixed(10, 1)
+    ex, dl = E.build_tables(w, w.ids(), S.table_coefficients(), 2)
+    eng.set_problem(ex, dl)
+    perm = np.arange(10, dtype=np.uint16)[None]
+    with pytest.raises(S.DataError):  # batch of 3 > mb
+        eng.evaluate_batch(perm, E.end_bits([[3, 3, 2, 2]], 10))
+    with pytest.raises(S.DataError):  # last position not a batch end
+        eng.evaluate_batch(perm, np.zeros((1, 1), dtype=np.uint32))
+
+
+# ---------------------------------------------------------------- K2 replay
+def _replay_cfg(seed, **kw):
+    return S.AnnealConfig(seed=seed, mode=S.SearchMode.REPLAY, **kw)
+
+
+def test_replay_matches_golden_anneal():
+    c = S.table_coefficients()
+    for case in golden("anneal"):
+        w = S.generate_mixed(case["n"], case["wseed"])
+        res = S.anneal(w, w.ids(), c, _replay_cfg(case["seed"], **case["cfg"]), case["mb"])
+        assert res.best.schedule.batches == case["batches"], case
+        assert res.best.n == case["n_met"]
+        assert res.best.g == unhex(case["g"]) and res.best.t_ms == unhex(case["t"])
+        assert res.stats.shortcut == case["shortcut"]
+        if not case["shortcut"]:
+            assert res.stats.proposals == case["proposals"] and res.stats.accepted == case["accepted"]
+        assert res.stats.objective_scale_used == unhex(case["scale"])
+
+
+@pytest.mark.parametrize("n", [8, 64, 256])
+@pytest.mark.parametrize("mb", [1, 2, 4])
+def test_replay_matches_oracle_many_seeds(port, n, mb):
+    c = S.table_coefficients()
+    w = _three_class(n, 77 + n)
+    fw = _flat(w)
+    seeds = range(20) if n < 256 else range(4)
+    cfg = {} if n < 256 else {"t0": 100.0, "iter": 30}
+    for seed in seeds:
+        res = S.anneal(w, w.ids(), c, _replay_cfg(seed, **cfg), mb)
+        o = port.anneal(fw, TABLE_COEFFS, w.ids(), mb, seed=seed, **cfg)
+        assert res.best.schedule.batches == o["batches"], (n, mb, seed)
+        assert (res.best.n, res.best.t_ms, res.best.g) == (o["n"], o["t"], o["g"])
+        assert (res.stats.proposals, res.stats.accepted) == (o["proposals"], o["accepted"])
+
+
+def test_replay_many_chains_in_one_launch(eng, port):
+    """K2 with C chains: chain c reproduces the reference walk with seed + c."""
+    n, mb = 48, 4
+    w = S.generate_mixed(n, 3)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    s, i = S.initial_candidates(w, ids, c, mb)
+    gs, gi = S.evaluate(s, c, w).g, S.evaluate(i, c, w).g
+    st = s if gs >= gi else i
+    start = [ids.index(x) for x in st.flatten()]
+    sizes = [len(b) for b in st.batches]
+    g0 = max(gs, gi)
+    bp, bs, res = eng.anneal_chains(start, sizes, t0=80.0, iter=20, seed=11, objective_scale=80.0 / g0, replay=True,
+                                    chains=16)
+    levels, t = 0, 80.0
+    while t >= 20.0:
+        levels, t = levels + 1, t * 0.95
+    assert res.chains_run == 16 and res.proposals == 16 * levels * 20
+    fw = _flat(w)
+    best = max(range(16), key=lambda k: (port.anneal(fw, TABLE_COEFFS, ids, mb, seed=11 + k, t0=80.0, iter=20,
+                                                     objective_scale=80.0 / g0)["g"], -k))
+    assert res.chain == best
+
+
+def test_schedule_all_replay_matches_golden():
+    c = S.table_coefficients()
+    for case in golden("schedule_all"):
+        w = S.generate_mixed(case["n"], case["wseed"])
+        insts = [S.InstanceState(i, 2**35, 2**35, 0.9, 262144.0, case["mb"]) for i in range(case["k"])]
+        res = S.schedule_all(w, insts, c, _replay_cfg(case["seed"]))
+        assert res.epochs == case["epochs"]
+        for got, want in zip(res.per_instance, case["per_instance"]):
+            assert got.schedule.batches == want["batches"]
+            assert got.n == want["n_met"] and got.g == unhex(want["g"])
+
+
+# ---------------------------------------------------------------- K3/K4 chains
+@pytest.mark.parametrize("n,mb,chains", [(2, 2, 8), (9, 3, 64), (64, 4, 512), (256, 4, 1024), (1024, 4, 256),
+                                         (200, 16, 128), (4096, 4, 32)])
+def test_chains_valid_and_dominant(n, mb, chains):
+    c = S.table_coefficients()
+    w = _three_class(n, 5 + n)
+    cfg = S.AnnealConfig(seed=3, chains=chains, t0=100.0, iter=20 if n < 4096 else 5)
+    res = S.anneal(w, w.ids(), c, cfg, mb)
+    assert res.best.schedule.is_partition_of(w.ids(), mb)
+    if not res.stats.shortcut:
+        assert res.best.g >= res.stats.g_sorted_start and res.best.g >= res.stats.g_input_start
+        assert res.stats.chains_run == chains
+        assert res.stats.proposals == chains * res.stats.levels_run * cfg.iter
+        # the engine's incremental objective agrees with the exact evaluation of its winner
+        if res.best.g > max(res.stats.g_sorted_start, res.stats.g_input_start):
+            assert abs(res.stats.engine_g - res.best.g) <= 1e-12 * res.best.g
+
+
+def test_chains_deterministic_and_slice_independent():
+    c = S.table_coefficients()
+    w = _three_class(128, 21)
+    base = dict(seed=9, chains=300, t0=60.0, iter=25, scale_ladder=(1.0, 100.0, 1e4))
+    a = S.anneal(w, w.ids(), c, S.AnnealConfig(**base), 4)
+    b = S.anneal(w, w.ids(), c, S.AnnealConfig(**base), 4)
+    assert a.best.schedule.batches == b.best.schedule.batches
+    a.stats.kernel_ms = b.stats.kernel_ms = 0.0  # device timing is the only non-deterministic field
+    assert a.stats == b.stats
+    # the same 300 chains split over two "devices": the better half-winner is the full winner
+    h1 = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, chain_begin=0, chain_end=150), 4)
+    h2 = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, chain_begin=150, chain_end=300), 4)
+    win = max((h1, h2), key=lambda r: (r.stats.engine_g, -r.best.t_ms, -r.stats.best_chain))
+    assert win.stats.best_chain == a.stats.best_chain
+    assert win.best.schedule.batches == a.best.schedule.batches
+
+
+def test_chains_state_parking_is_transparent(eng):
+    """More chains than resident warps (state parked in HBM between levels) gives each chain
+    exactly the trajectory it has when it stays resident."""
+    n, mb = 256, 4
+    w = _three_class(n, 8)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    s, _ = S.initial_candidates(w, ids, c, mb)
+    start = [ids.index(x) for x in s.flatten()]
+    sizes = [len(b) for b in s.batches]
+    kw = dict(t0=50.0, iter=10, seed=5, objective_scale=1e6)
+    many = eng.sm_count * 32 * 2 + 7   # forces several chains per warp
+    _, _, r_all = eng.anneal_chains(start, sizes, chains=many, **kw)
+    lo = r_all.chain
+    _, _, r_one = eng.anneal_chains(start, sizes, chains=many, chain_begin=lo, chain_end=lo + 1, **kw)
+    assert r_one.chain == lo and r_one.g == r_all.g and r_one.t == r_all.t
+
+
+def test_chains_attainment_at_least_reference(port):
+    c = S.table_coefficients()
+    wins = 0
+    for seed in range(4):
+        w = S.generate_mixed(256, seed)
+        ref_res = port.anneal(_flat(w), TABLE_COEFFS, w.ids(), 4, seed=seed)
+        gpu = S.anneal(w, w.ids(), c, S.AnnealConfig(seed=seed, chains=2048,
+                                                     scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4)), 4)
+        assert gpu.best.n >= ref_res["n"] or gpu.best.g >= ref_res["g"]
+        wins += gpu.best.g > ref_res["g"]
+    assert wins >= 3
+
+
+def test_chains_edge_cases():
+    c = S.table_coefficients()
+    code, chat = S.default_slo_classes()
+    tight = S.TaskClass(0, "tight", S.SloSpec.e2e(1e-6))
+    one = S.Workload([S.Request(0, 0, 100, 10, 10)], [tight])
+    r = S.anneal(one, [0], c, S.AnnealConfig(chains=4, t0=30.0, iter=5), 1)
+    assert r.best.schedule.batches == [[0]] and r.stats.proposals == 4 * 5 * r.stats.levels_run
+    loose = S.Workload([S.Request(i, 0, 100 * (i + 1), 10, 10) for i in range(3)], [S.TaskClass(0, "l", S.SloSpec.e2e(1e12))])
+    r = S.anneal(loose, [0, 1, 2], c, S.AnnealConfig(), 1)
+    assert r.stats.shortcut and r.stats.proposals == 0 and r.best.schedule.flatten() == [0, 1, 2]
+    empty = S.Workload([], [code, chat])
+    r = S.anneal(empty, [], c, S.AnnealConfig(), 2)
+    assert r.stats.shortcut and r.best.schedule.batches == [] and r.best.g == 0.0
+    w = S.generate_mixed(5000, 0)
+    with pytest.raises(S.CapacityError):
+        S.anneal(w, w.ids(), c, S.AnnealConfig(), 4)
+
+
+def test_budget_stops_early():
+    c = S.table_coefficients()
+    w = S.generate_mixed(1024, 0)
+    r = S.anneal(w, w.ids(), c, S.AnnealConfig(chains=16384, budget_ms=2.0), 4)
+    assert 0 < r.stats.proposals < 16384 * 63 * 100
+    assert r.best.schedule.is_partition_of(w.ids(), 4)
+    assert r.best.g >= max(r.stats.g_sorted_start, r.stats.g_input_start)

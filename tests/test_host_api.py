@@ -1,0 +1,154 @@
+"""CPU-only checks of the product library: it loads, exports every symbol its headers
+declare, and its host-side logic (the reference's O(N) setup/teardown around the GPU
+loop) matches the oracle and the golden vectors. No compute call needs a GPU here."""
+import math
+import os
+import re
+
+import numpy as np
+import pytest
+
+from conftest import ROOT, golden, unhex
+from oracle import TABLE_COEFFS
+
+import paper_2504_14966_b200 as S
+from paper_2504_14966_b200 import _lib
+from paper_2504_14966_b200 import engine as E
+
+
+def _declared(header):
+    text = open(os.path.join(ROOT, "include", header)).read()
+    return set(re.findall(r"^\s*(?:[\w\*]+\s+)+\**((?:slo|slosched)_\w+)\s*\(", text, re.M))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.lib()
+    declared = _declared("slosched_gpu.h") | _declared("slosched_api.h")
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(L, name), name
+    assert set(_lib.EXPORTED) == declared
+
+
+def test_version_and_no_silent_fallback():
+    assert b"sm_100a" in _lib.lib().slo_version()
+    try:
+        import torch
+        has_gpu = torch.cuda.is_available()
+    except Exception:
+        has_gpu = False
+    if not has_gpu:
+        w = S.generate_mixed(16, 0)
+        with pytest.raises(S.EngineError):
+            S.anneal(w, w.ids(), S.table_coefficients(), S.AnnealConfig(chains=4), 2)
+
+
+def test_philox_known_answers():
+    # Random123 kat_vectors, philox4x32_10
+    assert list(E.philox4x32_10([0, 0, 0, 0], [0, 0])) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    f = 0xFFFFFFFF
+    assert list(E.philox4x32_10([f, f, f, f], [f, f])) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert list(E.philox4x32_10([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0])) == \
+        [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+
+
+def test_latency_model_matches_golden():
+    c = S.table_coefficients()
+    for case in golden("latency"):
+        b, li, lo = case["b"], case["li"], case["lo"]
+        assert S.predict_prefill(c, b, li) == unhex(case["prefill"])
+        assert S.predict_decode_total(c, b, li, lo) == unhex(case["decode_total"])
+        assert S.predict_exec(c, b, li, lo) == unhex(case["exec"])
+        assert S.predict_tpot(c, b, li, lo) == unhex(case["tpot"])
+    with pytest.raises(ValueError):
+        S.predict_tpot(c, 1, 100, 0)
+
+
+def test_generate_mixed_matches_golden():
+    for case in golden("generate_mixed"):
+        w = S.generate_mixed(case["n"], case["seed"], predict=case["mode"] == 1)
+        a = w.arrays
+        for k in ("id", "cls", "in_len", "true_out", "pred_out"):
+            assert list(a[k]) == case[k], k
+
+
+def test_evaluate_matches_golden():
+    c = S.table_coefficients()
+    for case in golden("evaluate"):
+        w = S.generate_mixed(case["n"], case["seed"])
+        ev = S.evaluate(S.Schedule(case["batches"]), c, w)
+        assert ev.n == case["n_met"] and ev.t_ms == unhex(case["t"]) and ev.g == unhex(case["g"])
+        assert [m.wait_ms for m in ev.per_request] == [unhex(x) for x in case["wait"]]
+        assert [int(m.slo_met) for m in ev.per_request] == case["met"]
+
+
+def test_initial_candidates_and_neighbor_match_golden():
+    c = S.table_coefficients()
+    for case in golden("initial_candidates"):
+        w = S.generate_mixed(case["n"], case["seed"])
+        s, i = S.initial_candidates(w, w.ids(), c, case["mb"])
+        assert s.batches == case["sorted"] and i.batches == case["input"]
+    for case in golden("neighbor_walk"):
+        out = S.neighbor_walk(S.Schedule(case["start"]), case["seed"], case["steps"], case["mb"])
+        assert out.batches == case["out"]
+
+
+def test_errors_follow_reference_contract():
+    code, chat = S.default_slo_classes()
+    with pytest.raises(S.DataError):  # duplicate id
+        S.Workload([S.Request(0, 0, 10, 10, 10), S.Request(0, 0, 10, 10, 10)], [code])
+    with pytest.raises(S.DataError):  # unknown class
+        S.Workload([S.Request(0, 7, 10, 10, 10)], [code])
+    with pytest.raises(S.DataError):  # bad SLO
+        S.Workload([], [S.TaskClass(0, "x", S.SloSpec.e2e(-1.0))])
+    w = S.Workload([S.Request(0, 0, 10, 10, None)], [code])
+    with pytest.raises(S.DataError):  # missing prediction
+        S.evaluate(S.Schedule([[0]]), S.table_coefficients(), w)
+    with pytest.raises(S.DataError):  # bad AnnealConfig is rejected before any GPU work
+        S.anneal(S.generate_mixed(4, 0), [0, 1, 2, 3], S.table_coefficients(), S.AnnealConfig(t0=10.0), 2)
+
+
+def test_latest_start_is_the_exact_deadline():
+    rs = np.random.default_rng(3)
+    for _ in range(20000):
+        s = float(rs.choice([30000.0, 10000.0, 1e9, rs.uniform(1, 1e5)]))
+        c = float(rs.uniform(0, 5e4))
+        d = S.latest_start(s, c)
+        assert d + c <= s or math.isinf(d)
+        up = math.nextafter(d, math.inf)
+        assert not (up + c <= s)
+        for x in (d, up, math.nextafter(d, -math.inf), d + rs.uniform(-1e-9, 1e-9) * abs(d)):
+            if x >= 0:
+                assert (x <= d) == (x + c <= s)
+
+
+def test_tables_fold_the_slo_test_exactly(port):
+    """deadline[b][i] reproduces CostModel::met (P:src/priority_mapper.cpp:237-241) for every
+    elapsed value the oracle's score visits."""
+    w = S.generate_mixed(40, 11)
+    c = S.table_coefficients()
+    ex, dl = E.build_tables(w, w.ids(), c, 4)
+    ids = sorted(w.ids())
+    for i, rid in enumerate(ids):
+        r = w.find_request(rid)
+        for b in range(1, 5):
+            assert ex[b - 1, i] == S.predict_exec(c, b, r.input_len, r.predicted_output_len)
+    rs = np.random.default_rng(0)
+    for i, rid in enumerate(ids):
+        r = w.find_request(rid)
+        cls = w.classes[r.task_class_id]
+        for b in range(1, 5):
+            for el in rs.uniform(0, 40000, 50):
+                if cls.slo.kind == S.SloKind.E2E:
+                    met = el + ex[b - 1, i] <= cls.slo.e2e_ms
+                else:
+                    met = (el + S.predict_prefill(c, b, r.input_len) <= cls.slo.ttft_ms and
+                           S.predict_tpot(c, b, r.input_len, r.predicted_output_len) <= cls.slo.tpot_ms)
+                assert met == (el <= dl[b - 1, i])
+
+
+def test_end_bits_layout():
+    bits = E.end_bits([[2, 1, 3], [1] * 40], 40)
+    assert bits.shape == (2, 2)
+    assert bits[0, 0] == (1 << 1) | (1 << 2) | (1 << 5)
+    assert bits[1, 0] == 0xFFFFFFFF and bits[1, 1] == 0xFF
