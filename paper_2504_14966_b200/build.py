@@ -49,6 +49,7 @@ def _stale(out, srcs):
 def build(verbose=False, force=False, ptxas_info=False) -> str:
     os.makedirs(BUILD, exist_ok=True)
     headers = [os.path.join(INC, h) for h in os.listdir(INC)]
+    headers += [os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith((".cuh", ".h", ".hpp"))]
     objs, log = [], ""
     for src in CUDA_SRCS:
         s = os.path.join(CSRC, src)

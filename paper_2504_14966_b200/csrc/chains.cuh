@@ -1,0 +1,509 @@
+// K3: one annealing chain per warp (Philox4x32-10 moves, incremental objective).
+// Included by engine.cu inside its anonymous namespace.
+//
+// Chain state (shared memory, per warp):
+//   ent[q]   u16, q = position: combined table index (batch_size-1) * n + dense_index
+//   bits[w]  u32 linear batch-end bitmask (bit q set iff q is the last position of a batch)
+//   rnd      the Philox words of the next 32 proposals, drawn lane-parallel
+// Objective: the schedule is cut into units of 32 consecutive positions. Each unit has a
+// content-only summary (its batches' makespans, latency moments, deadline bound) computed
+// cooperatively by the 32 lanes. A warp-wide scan over the unit summaries gives every
+// unit's start time E and the makespan fmk of the batch open at its start; a unit's summed
+// latency is then closed-form (cnt*E + fmk*A + bs), and the SLO test walks only "live" units
+// (E <= an upper bound of the unit's deadlines) -- at N=1024 the first one or two. After a
+// move only the (<= 2) dirty units are re-summarised.
+
+#define kNegInf (-static_cast<double>(INFINITY))
+
+struct ChainParams {
+    int n, mb;
+    uint64_t magic;      // floor(2^32 / n) + 1: (e * magic) >> 32 == e / n exactly for e < 65536
+    const double2* tab;  // global [mb][n] (exec, deadline)
+    int smem_tab;
+    double t0, tau, scale;
+    int iter, levels;
+    const double* scale_mult;
+    int n_mult;
+    uint32_t key0, key1;
+    int chain_begin, chain_count;
+    long long budget_ns;
+    const uint16_t* start_ent;   // [1024*UPL]
+    const uint32_t* start_bits;  // [32*UPL]
+    uint16_t* st_ent;            // [chain_count][1024*UPL]  parked state (several chains per warp)
+    uint32_t* st_bits;           // [chain_count][32*UPL]
+    uint16_t* best_ent;          // [chain_count][1024*UPL]
+    uint32_t* best_bits;         // [chain_count][32*UPL]
+    ChainRec* rec;
+};
+
+struct UnitSum {
+    double hm;    // max exec from the unit start through its first batch end (whole unit if none)
+    double tm;    // max exec after the unit's last batch end
+    double inner; // summed makespans of batches that start and end inside the unit
+    double bs;    // sum of exec over the unit + sum over inner batches of makespan * positions after it
+    float dmax;   // upper bound of the unit's deadlines (rounded up; -inf if none)
+    int fe;       // unit contains a batch end
+    int cnt;      // positions in the unit
+    int A;        // positions after the first batch end
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
+    return v;
+}
+
+// segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
+// and are at most mb long, so log2(mb) shuffle steps suffice
+__device__ __forceinline__ double seg_max(double e, uint32_t w, int lane, int mb) {
+    double m = fmax(e, 0.0);  // makespans start at 0 (reference P:src/priority_mapper.cpp:266)
+    int head = lane == 0 ? 1 : (int)((w >> (lane - 1)) & 1u);
+    for (int d = 1; d < mb; d <<= 1) {
+        const double mu = __shfl_up_sync(FULL, m, d);
+        const int hu = __shfl_up_sync(FULL, head, d);
+        if (lane >= d && !head) m = fmax(m, mu), head = hu;
+    }
+    return m;
+}
+
+// cooperative summary of unit u (all 32 lanes; every lane receives the result)
+__device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n,
+                                                int mb, int u, int lane) {
+    UnitSum s;
+    const int q0 = u << 5;
+    const int cnt = min(32, n - q0);
+    const uint32_t w = bits[u];
+    double e = 0.0, D = kNegInf;
+    if (lane < cnt) {
+        const double2 v = tab[ent[q0 + lane]];
+        e = v.x, D = v.y;
+    }
+    const double m = seg_max(e, w, lane, mb);
+    const int f = w ? __ffs(w) - 1 : -1;
+    const int la = w ? 31 - __clz(w) : -1;
+    const double m_last = __shfl_sync(FULL, m, cnt - 1);
+    const double m_first = __shfl_sync(FULL, m, f < 0 ? cnt - 1 : f);
+    const bool inner_end = ((w >> lane) & 1u) && lane != f;
+    const double mk = inner_end ? m : 0.0;
+    double inner = mk, bs = e + mk * (double)(cnt - 1 - lane);
+    float dm = __double2float_ru(D);
+#pragma unroll
+    for (int d = 16; d; d >>= 1) {  // three interleaved butterfly reductions
+        inner += __shfl_xor_sync(FULL, inner, d);
+        bs += __shfl_xor_sync(FULL, bs, d);
+        dm = fmaxf(dm, __shfl_xor_sync(FULL, dm, d));
+    }
+    s.fe = w != 0;
+    s.cnt = cnt;
+    s.A = w ? cnt - 1 - f : 0;
+    s.hm = m_first;
+    s.tm = (w == 0 || la < cnt - 1) ? m_last : 0.0;
+    s.inner = inner;
+    s.bs = bs;
+    s.dmax = dm;
+    return s;
+}
+
+// cooperative SLO count of unit u whose first position starts at elapsed E, the batch open at
+// the unit start having makespan fmk. Rare (live units whose inputs changed): kept out of line.
+__device__ __noinline__ int unit_met(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int mb,
+                                     int u, int lane, double E, double fmk) {
+    const int q0 = u << 5;
+    const int cnt = min(32, n - q0);
+    const uint32_t w = bits[u];
+    double e = 0.0, D = kNegInf;
+    if (lane < cnt) {
+        const double2 v = tab[ent[q0 + lane]];
+        e = v.x, D = v.y;
+    }
+    const double m = seg_max(e, w, lane, mb);
+    const int f = w ? __ffs(w) - 1 : -1;
+    double v = ((w >> lane) & 1u) ? (lane == f ? fmk : m) : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // inclusive prefix of closed makespans
+        const double up = __shfl_up_sync(FULL, v, d);
+        if (lane >= d) v += up;
+    }
+    double off = __shfl_up_sync(FULL, v, 1);
+    if (lane == 0) off = 0.0;
+    const bool met = lane < cnt && E + off <= D;
+    return __popc(__ballot_sync(FULL, met));
+}
+
+// Philox words of (proposal, chain, attempt) -- out of line: only retries >= 2 need it
+__device__ __noinline__ uint4 philox_draw(uint32_t prop, uint32_t cid, uint32_t attempt, uint32_t k0, uint32_t k1) {
+    uint32_t r[4] = {prop, cid, attempt, kTagMove};
+    philox10(r, k0, k1);
+    return make_uint4(r[0], r[1], r[2], r[3]);
+}
+
+struct Move {
+    int kind;        // 0 none, 1 range (squeeze/delay), 2 swap
+    int lo, hi, split, sz1, sz2;
+    int ra, rb, dir; // rotation on [ra, rb]; dir +1 right, -1 left
+    int clr, set;    // bitmask edits (-1 = none)
+    int a, b;        // swap positions
+};
+
+// The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the bitmask
+// representation. Attempts 0 and 1 read the lane-parallel Philox block (rw[0..5]); further
+// retries draw directly. Counter = (proposal, chain, attempt, tag): geometry-independent.
+__device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, uint32_t prop, uint32_t cid,
+                                          uint32_t k0, uint32_t k1, const uint32_t* rw) {
+    Move mv;
+    mv.kind = 0;
+    if (n == 0) return mv;
+    for (int attempt = 0; attempt <= 8; ++attempt) {
+        uint32_t r0, r1, r2;
+        if (attempt < 2) {
+            r0 = rw[3 * attempt], r1 = rw[3 * attempt + 1], r2 = rw[3 * attempt + 2];
+        } else {
+            const uint4 r = philox_draw(prop, cid, (uint32_t)attempt, k0, k1);
+            r0 = r.x, r1 = r.y, r2 = r.z;
+        }
+        const uint32_t op = attempt < 8 ? lemire32(r0, 3) : 2u;  // forced swap after 8 misses
+        if (op == 0) {  // squeeze (:141-153)
+            const int first = next_end(bits, 0) + 1;
+            if (first >= n) continue;
+            const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
+            const int sk = prev_end(bits, pos) + 1;
+            const int skm1 = prev_end(bits, sk - 1) + 1;
+            if (sk - skm1 >= mb) continue;
+            const int ek = next_end(bits, pos);
+            mv.kind = 1;
+            mv.lo = skm1, mv.hi = ek, mv.split = sk;
+            mv.sz1 = sk - skm1 + 1, mv.sz2 = ek - sk;
+            mv.ra = sk, mv.rb = pos, mv.dir = 1;
+            mv.clr = sk - 1, mv.set = sk;
+            return mv;
+        } else if (op == 1) {  // delay (:155-170)
+            const int pos = (int)lemire32(r1, (uint32_t)n);
+            const int sk = prev_end(bits, pos) + 1;
+            const int ek = next_end(bits, pos);
+            if (ek < n - 1) {
+                const int ek1 = next_end(bits, ek + 1);
+                if (ek1 - ek >= mb) continue;
+                mv.kind = 1;
+                mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
+                mv.sz1 = ek - sk, mv.sz2 = ek1 - ek + 1;
+                mv.ra = pos, mv.rb = ek1, mv.dir = -1;
+                mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
+            } else {
+                mv.kind = 1;
+                mv.lo = sk, mv.hi = n - 1, mv.split = n - 2;
+                mv.sz1 = n - 1 - sk, mv.sz2 = 1;
+                mv.ra = pos, mv.rb = n - 1, mv.dir = -1;
+                mv.clr = -1, mv.set = n >= 2 ? n - 2 : -1;
+            }
+            return mv;
+        } else {  // swap (:172-180)
+            if (n < 2) continue;
+            const int a = (int)lemire32(r1, (uint32_t)n);
+            int b = (int)lemire32(r2, (uint32_t)(n - 1));
+            if (b >= a) ++b;
+            mv.kind = 2;
+            mv.a = a, mv.b = b;
+            return mv;
+        }
+    }
+    return mv;
+}
+
+template <int UPL>
+struct ChainState {  // per-lane registers: summaries of this lane's units + SLO-walk cache
+    UnitSum s[UPL];
+    double wE[UPL], wF[UPL];
+    int wN[UPL];
+};
+
+// Warp-wide scan over unit summaries: E[k] (start elapsed) and fmk[k] for this lane's units.
+template <int UPL>
+__device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lane, double (&E)[UPL],
+                                              double (&fmk)[UPL]) {
+    int F = 0;
+    double M = 0.0, head = 0.0, rest = 0.0;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) {
+        const UnitSum& s = cs.s[k];
+        if (!F) {
+            if (s.fe) head = fmax(M, s.hm), rest = s.inner, M = s.tm, F = 1;
+            else M = fmax(M, s.hm);
+        } else {
+            if (s.fe) rest = rest + fmax(M, s.hm), rest = rest + s.inner, M = s.tm;
+            else M = fmax(M, s.hm);
+        }
+    }
+    int Fs = F;
+    double Ms = M;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // segmented max scan of open-batch maxima
+        const double Mu = __shfl_up_sync(FULL, Ms, d);
+        const int Fu = __shfl_up_sync(FULL, Fs, d);
+        if (lane >= d) {
+            if (!Fs) Ms = fmax(Mu, Ms);
+            Fs |= Fu;
+        }
+    }
+    double carry = __shfl_up_sync(FULL, Ms, 1);
+    if (lane == 0) carry = 0.0;
+    double S = F ? fmax(carry, head) + rest : 0.0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {  // sum scan of the makespans closed in each lane
+        const double v = __shfl_up_sync(FULL, S, d);
+        if (lane >= d) S += v;
+    }
+    double el = __shfl_up_sync(FULL, S, 1);
+    if (lane == 0) el = 0.0;
+    double cm = carry;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) {
+        const UnitSum& s = cs.s[k];
+        E[k] = el;
+        fmk[k] = fmax(cm, s.hm);
+        if (s.fe) el = el + fmk[k], el = el + s.inner, cm = s.tm;
+        else cm = fmax(cm, s.hm);
+    }
+}
+
+// Objective of the current state. full: re-summarise every unit and re-walk every live unit;
+// otherwise only units du0/du1 (-1 = none). Outputs the total latency, the SLO count and the
+// per-unit (E, fmk, walk result) to commit when the state is accepted.
+template <int UPL>
+__device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16_t* ent, const uint32_t* bits,
+                                               const double2* tab, int n, int mb, int lane, bool full, int du0,
+                                               int du1, double& tot_out, int& nm_out, double (&E)[UPL],
+                                               double (&fmk)[UPL], int (&nN)[UPL], unsigned long long& sc1,
+                                               unsigned long long& sc2) {
+    const int U = (n + 31) >> 5;
+    const int todo = full ? 32 * UPL : (du0 < 0 ? 0 : (du1 >= 0 && du1 != du0 ? 2 : 1));
+    for (int i = 0; i < todo; ++i) {  // one inlined copy of the unit summary
+        const int u = full ? i : (i == 0 ? du0 : du1);
+        UnitSum v{0.0, 0.0, 0.0, 0.0, -INFINITY, 0, 0, 0};
+        if (u < U) v = unit_summary(ent, bits, tab, n, mb, u, lane), sc1 += lane == 0 ? 32 : 0;
+        if (lane == u / UPL) {
+#pragma unroll
+            for (int k = 0; k < UPL; ++k)
+                if (k == u % UPL) cs.s[k] = v;
+        }
+    }
+    combine_units<UPL>(cs, lane, E, fmk);
+    double tot = 0.0;
+    int nm = 0;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) {
+        const UnitSum& s = cs.s[k];
+        const int u = lane * UPL + k;
+        // summed latency of the unit's positions, closed form
+        tot += (double)s.cnt * E[k] + (s.fe ? fmk[k] * (double)s.A : 0.0) + s.bs;
+        const bool live = E[k] <= (double)s.dmax;
+        const bool dirty = full || u == du0 || u == du1;
+        const bool need = live && (dirty || E[k] != cs.wE[k] || fmk[k] != cs.wF[k]);
+        nN[k] = live ? cs.wN[k] : 0;
+        unsigned mask = __ballot_sync(FULL, need);
+        while (mask) {  // cooperative SLO walks of the units that need one
+            const int ln = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const double Eu = __shfl_sync(FULL, E[k], ln);
+            const double Fu = __shfl_sync(FULL, fmk[k], ln);
+            const int cntm = unit_met(ent, bits, tab, n, mb, ln * UPL + k, lane, Eu, Fu);
+            if (lane == ln) nN[k] = cntm;
+            sc2 += lane == 0 ? 32 : 0;
+        }
+        nm += nN[k];
+    }
+    tot_out = warp_sum(tot);
+    nm_out = __reduce_add_sync(FULL, nm);
+}
+
+template <int UPL>
+__host__ __device__ constexpr int slot_bytes() {
+    // entries + bitmask + two parked unit summaries + Philox block (32 proposals x 8 words)
+    return 1024 * UPL * 2 + 32 * UPL * 4 + 2 * (int)sizeof(UnitSum) + 32 * 8 * 4;
+}
+
+template <int UPL>
+__device__ __forceinline__ void copy_state(uint16_t* de, uint32_t* db, const uint16_t* se, const uint32_t* sb,
+                                           int lane) {
+    constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
+    for (int i = lane; i < kEnt / 8; i += 32) reinterpret_cast<uint4*>(de)[i] = reinterpret_cast<const uint4*>(se)[i];
+    for (int i = lane; i < kBits; i += 32) db[i] = sb[i];
+}
+
+template <int UPL>
+__global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const ChainParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
+    const int n = p.n, mb = p.mb;
+
+    const double2* tab = p.tab;
+    size_t off = 0;
+    if (p.smem_tab) {  // stage the (exec, deadline) table once per block: coalesced 16 B loads
+        double2* st = reinterpret_cast<double2*>(smem);
+        const int total = mb * n;
+        for (int i = threadIdx.x; i < total; i += blockDim.x) st[i] = p.tab[i];
+        __syncthreads();
+        tab = st;
+        off = ((size_t)total * sizeof(double2) + 15) & ~(size_t)15;
+    }
+    constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
+    unsigned char* slot = smem + off + (size_t)wid * slot_bytes<UPL>();
+    uint16_t* ent = reinterpret_cast<uint16_t*>(slot);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2);
+    UnitSum* saved = reinterpret_cast<UnitSum*>(slot + kEnt * 2 + kBits * 4);
+    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + kBits * 4 + 2 * sizeof(UnitSum));
+
+    const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
+    if (gw >= p.chain_count) return;
+    const int n_my = (p.chain_count - gw + TW - 1) / TW;
+
+    uint64_t deadline = ~0ull;
+    if (p.budget_ns > 0) deadline = __shfl_sync(FULL, gtimer(), 0) + (uint64_t)p.budget_ns;
+
+    ChainState<UPL> cs;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) cs.wE[k] = 0.0, cs.wF[k] = 0.0, cs.wN[k] = 0;
+    double f = 0.0, best_f = 0.0;
+    unsigned long long props = 0, accs = 0;
+    int stop = 0;
+    const uint32_t nn = (uint32_t)n;
+    const uint64_t magic = p.magic;
+
+    double t = p.t0;
+    for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
+        for (int k = 0; k < n_my; ++k) {
+            if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
+                stop = 1;
+                break;
+            }
+            const int c = gw + k * TW;
+            const uint32_t cid = (uint32_t)(p.chain_begin + c);
+            ChainRec* rc = p.rec + c;
+            unsigned long long sc1 = 0, sc2 = 0;
+            const bool load = lev == 0 || n_my > 1;
+            if (load) {  // (re)load the chain state; it is evaluated in full below (it = -1)
+                copy_state<UPL>(ent, bits, lev == 0 ? p.start_ent : p.st_ent + (size_t)c * kEnt,
+                                lev == 0 ? p.start_bits : p.st_bits + (size_t)c * kBits, lane);
+                __syncwarp();
+                if (lev > 0) best_f = rc->g, props = rc->proposals, accs = rc->accepted;
+            }
+            const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
+
+            for (int it = load ? -1 : 0; it < p.iter; ++it) {
+                const bool full = it < 0;
+                const uint32_t prop = (uint32_t)(lev * p.iter + max(it, 0));
+                if (!full && (it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0, 1 and accept
+                    uint32_t r[4] = {prop + (uint32_t)lane, cid, 0u, kTagMove};
+                    philox10(r, p.key0, p.key1);
+                    uint32_t r1[4] = {prop + (uint32_t)lane, cid, 1u, kTagMove};
+                    philox10(r1, p.key0, p.key1);
+                    uint32_t a[4] = {prop + (uint32_t)lane, cid, (uint32_t)kAcceptAttempt, kTagMove};
+                    philox10(a, p.key0, p.key1);
+                    reinterpret_cast<uint4*>(rnd)[2 * lane] = make_uint4(r[0], r[1], r[2], r1[0]);
+                    reinterpret_cast<uint4*>(rnd)[2 * lane + 1] = make_uint4(r1[1], r1[2], a[0], a[1]);
+                    __syncwarp();
+                }
+                const uint32_t* rw = rnd + 8 * (max(it, 0) & 31);
+                Move mv;
+                mv.kind = 0;
+                if (!full) mv = draw_move(bits, n, mb, prop, cid, p.key0, p.key1, rw);
+
+                // ---- apply in place (undo on reject)
+                int q = 0;
+                uint16_t old_q = 0;
+                uint32_t ow0 = 0, ow1 = 0;
+                int w0 = 0, w1 = 0, du0 = -1, du1 = -1;
+                if (mv.kind == 1) {
+                    q = mv.lo + lane;
+                    const bool act = q <= mv.hi;
+                    uint16_t nw = 0;
+                    if (act) {
+                        int s = q;
+                        if (mv.dir > 0) s = q == mv.ra ? mv.rb : (q > mv.ra && q <= mv.rb ? q - 1 : q);
+                        else s = q == mv.rb ? mv.ra : (q >= mv.ra && q < mv.rb ? q + 1 : q);
+                        old_q = ent[q];
+                        const uint32_t se = ent[s];
+                        const uint32_t idx = se - (uint32_t)(((uint64_t)se * magic) >> 32) * nn;
+                        const int sz = q <= mv.split ? mv.sz1 : mv.sz2;
+                        nw = (uint16_t)(idx + (uint32_t)(sz - 1) * nn);
+                    }
+                    w0 = mv.clr >= 0 ? mv.clr >> 5 : 0;
+                    w1 = mv.set >= 0 ? mv.set >> 5 : 0;
+                    ow0 = bits[w0], ow1 = bits[w1];
+                    __syncwarp();
+                    if (act) ent[q] = nw;
+                    if (lane == 0) {
+                        if (mv.clr >= 0) bits[mv.clr >> 5] &= ~(1u << (mv.clr & 31));
+                        if (mv.set >= 0) bits[mv.set >> 5] |= 1u << (mv.set & 31);
+                    }
+                    __syncwarp();
+                    du0 = mv.lo >> 5, du1 = mv.hi >> 5;
+                } else if (mv.kind == 2) {
+                    const uint32_t ea = ent[mv.a], eb = ent[mv.b];
+                    ow0 = ea, ow1 = eb;
+                    const uint32_t ba = (uint32_t)(((uint64_t)ea * magic) >> 32) * nn;
+                    const uint32_t bb = (uint32_t)(((uint64_t)eb * magic) >> 32) * nn;
+                    __syncwarp();
+                    if (lane == 0) ent[mv.a] = (uint16_t)(ba + (eb - bb)), ent[mv.b] = (uint16_t)(bb + (ea - ba));
+                    __syncwarp();
+                    du0 = mv.a >> 5, du1 = mv.b >> 5;
+                }
+                // owners park the summaries of the dirty units (restored on reject)
+#pragma unroll
+                for (int kk = 0; kk < UPL; ++kk) {
+                    if (du0 >= 0 && lane == du0 / UPL && kk == du0 % UPL) saved[0] = cs.s[kk];
+                    if (du1 >= 0 && du1 != du0 && lane == du1 / UPL && kk == du1 % UPL) saved[1] = cs.s[kk];
+                }
+                double tot, E[UPL], fmk[UPL];
+                int nm, nN[UPL];
+                evaluate_chain<UPL>(cs, ent, bits, tab, n, mb, lane, full, du0, du1, tot, nm, E, fmk, nN, sc1, sc2);
+                const double f_new = tot > 0.0 ? (double)nm / tot : 0.0;
+                bool accept;
+                if (full) {
+                    accept = true;
+                } else {
+                    ++props;
+                    accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
+                    if (!accept) {
+                        const double x = (f - f_new) * scale / t;
+                        const double u = (double)((((uint64_t)rw[6] << 32) | rw[7]) >> 11) * 0x1.0p-53;
+                        accept = x < 38.0 ? u < exp(-x) : u == 0.0;
+                    }
+                }
+                if (accept) {
+                    accs += full ? 0 : 1;
+#pragma unroll
+                    for (int kk = 0; kk < UPL; ++kk) cs.wE[kk] = E[kk], cs.wF[kk] = fmk[kk], cs.wN[kk] = nN[kk];
+                    f = f_new;
+                    if (full && lev == 0) best_f = -1.0, props = 0, accs = 0;
+                    if (f > best_f) {
+                        best_f = f;
+                        copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,
+                                        lane);
+                        if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
+                    }
+                } else {
+                    if (mv.kind == 1) {
+                        if (q <= mv.hi) ent[q] = old_q;
+                        if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
+                    } else if (mv.kind == 2) {
+                        if (lane == 0) ent[mv.a] = (uint16_t)ow0, ent[mv.b] = (uint16_t)ow1;
+                    }
+#pragma unroll
+                    for (int kk = 0; kk < UPL; ++kk) {
+                        if (du0 >= 0 && lane == du0 / UPL && kk == du0 % UPL) cs.s[kk] = saved[0];
+                        if (du1 >= 0 && du1 != du0 && lane == du1 / UPL && kk == du1 % UPL) cs.s[kk] = saved[1];
+                    }
+                    __syncwarp();
+                }
+            }
+            if (n_my > 1) {  // park the chain until the next level
+                copy_state<UPL>(p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, ent, bits, lane);
+                __syncwarp();
+            }
+            if (lane == 0) {
+                rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
+                rc->scan1 += sc1, rc->scan2 += sc2;
+            }
+        }
+    }
+}

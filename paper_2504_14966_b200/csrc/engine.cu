@@ -364,362 +364,7 @@ __global__ void k_replay(const ReplayParams p) {
 }
 
 // ================================================================ K3: chains
-struct ChainParams {
-    int n, mb;
-    const double2* tab;  // global [mb][n]
-    int smem_tab;
-    double t0, tau, scale;
-    int iter, levels;
-    const double* scale_mult;
-    int n_mult;
-    uint32_t key0, key1;
-    int chain_begin, chain_count;
-    long long budget_ns;
-    const uint16_t* start_ent;   // [32P]
-    const uint32_t* start_bits;  // [P]
-    uint16_t* st_ent;            // [chain_count][32P] state between levels (multi chains/warp)
-    uint32_t* st_bits;           // [chain_count][P]
-    uint16_t* best_ent;          // [chain_count][32P]
-    uint32_t* best_bits;         // [chain_count][P]
-    ChainRec* rec;               // [chain_count]
-};
-
-struct LaneSum {  // per-lane summary of its P positions (pass 1)
-    double hm;     // max exec from lane start through the first batch end (whole lane if none)
-    double tm;     // max exec after the last batch end in the lane
-    double inner;  // summed makespans of batches that start and end inside the lane
-    int fe;        // lane contains a batch end
-};
-
-template <int P>
-struct Lane {
-    static constexpr int LOGP = P == 1 ? 0 : P == 2 ? 1 : P == 4 ? 2 : P == 8 ? 3 : P == 16 ? 4 : P == 32 ? 5 : P == 64 ? 6 : 7;
-    __device__ static __forceinline__ int phys(int q) { return ((q & (P - 1)) << 5) | (q >> LOGP); }
-    __device__ static __forceinline__ int lane_of(int q) { return q >> LOGP; }
-
-    __device__ static void pass1(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int lane,
-                                 LaneSum& s) {
-        double run = 0.0, hm = 0.0, inner = 0.0;
-        int fe = 0;
-        const int q0 = lane * P;
-        uint32_t w = 0;
-#pragma unroll 4
-        for (int j = 0; j < P; ++j) {
-            const int q = q0 + j;
-            if (q >= n) break;
-            if ((j & 31) == 0) w = bits[q >> 5] >> (q & 31);
-            const uint32_t e16 = ent[(j << 5) | lane];
-            const double e = tab[(e16 >> 12) * n + (e16 & 0xFFFu)].x;
-            run = dmax(run, e);
-            if ((w >> (j & 31)) & 1u) {
-                if (fe) inner += run;
-                else hm = run, fe = 1;
-                run = 0.0;
-            }
-        }
-        s.fe = fe;
-        s.hm = fe ? hm : run;
-        s.tm = run;
-        s.inner = inner;
-    }
-
-    // warp-wide: elapsed at each lane's first position (E) and makespan of the batch
-    // open at the lane start (fmk), from the lane summaries
-    __device__ static void combine(const LaneSum& s, int lane, double& E, double& fmk) {
-        int F = s.fe;
-        double M = s.fe ? s.tm : s.hm;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {  // segmented max scan of open-run maxima
-            const double Mu = __shfl_up_sync(FULL, M, d);
-            const int Fu = __shfl_up_sync(FULL, F, d);
-            if (lane >= d) {
-                if (!F) M = dmax(Mu, M);
-                F |= Fu;
-            }
-        }
-        double carry = __shfl_up_sync(FULL, M, 1);
-        if (lane == 0) carry = 0.0;
-        fmk = dmax(carry, s.hm);
-        double S = s.fe ? fmk + s.inner : 0.0;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {  // inclusive sum scan of owned makespans
-            const double v = __shfl_up_sync(FULL, S, d);
-            if (lane >= d) S += v;
-        }
-        E = __shfl_up_sync(FULL, S, 1);
-        if (lane == 0) E = 0.0;
-    }
-
-    __device__ static void pass2(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int lane,
-                                 double E, double fmk, double& ltot, int& lnm) {
-        double el = E, run = 0.0, tot = 0.0;
-        int nm = 0, first = 1;
-        const int q0 = lane * P;
-        uint32_t w = 0;
-#pragma unroll 4
-        for (int j = 0; j < P; ++j) {
-            const int q = q0 + j;
-            if (q >= n) break;
-            if ((j & 31) == 0) w = bits[q >> 5] >> (q & 31);
-            const uint32_t e16 = ent[(j << 5) | lane];
-            const double2 v = tab[(e16 >> 12) * n + (e16 & 0xFFFu)];
-            tot += el + v.x;
-            nm += el <= v.y;
-            run = dmax(run, v.x);
-            if ((w >> (j & 31)) & 1u) {
-                el += first ? fmk : run;
-                first = 0;
-                run = 0.0;
-            }
-        }
-        ltot = tot;
-        lnm = nm;
-    }
-};
-
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
-    return v;
-}
-
-struct Move {
-    int kind;                // 0 none, 1 range (squeeze/delay), 2 swap
-    int lo, hi, split, sz1, sz2;
-    int ra, rb, dir;         // rotation on [ra, rb]; dir +1 right, -1 left
-    int clr, set;            // bitmask edits (-1 = none)
-    int a, b;                // swap positions
-};
-
-template <int P>
-__device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, uint32_t prop, uint32_t cid,
-                                          uint32_t k0, uint32_t k1) {
-    Move mv;
-    mv.kind = 0;
-    if (n == 0) return mv;
-    for (int attempt = 0; attempt <= 8; ++attempt) {
-        uint32_t r[4] = {prop, cid, (uint32_t)attempt, kTagMove};
-        philox10(r, k0, k1);
-        const uint32_t op = attempt < 8 ? lemire32(r[0], 3) : 2u;  // forced swap after 8 misses
-        if (op == 0) {  // squeeze (P:src/priority_mapper.cpp:141-153)
-            const int first = next_end(bits, 0) + 1;
-            if (first >= n) continue;
-            const int pos = first + (int)lemire32(r[1], (uint32_t)(n - first));
-            const int sk = prev_end(bits, pos) + 1;
-            const int skm1 = prev_end(bits, sk - 1) + 1;
-            if (sk - skm1 >= mb) continue;
-            const int ek = next_end(bits, pos);
-            mv.kind = 1;
-            mv.lo = skm1, mv.hi = ek, mv.split = sk;
-            mv.sz1 = sk - skm1 + 1, mv.sz2 = ek - sk;
-            mv.ra = sk, mv.rb = pos, mv.dir = 1;
-            mv.clr = sk - 1, mv.set = sk;
-            return mv;
-        } else if (op == 1) {  // delay (:155-170)
-            const int pos = (int)lemire32(r[1], (uint32_t)n);
-            const int sk = prev_end(bits, pos) + 1;
-            const int ek = next_end(bits, pos);
-            if (ek < n - 1) {
-                const int ek1 = next_end(bits, ek + 1);
-                if (ek1 - ek >= mb) continue;
-                mv.kind = 1;
-                mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
-                mv.sz1 = ek - sk, mv.sz2 = ek1 - ek + 1;
-                mv.ra = pos, mv.rb = ek1, mv.dir = -1;
-                mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
-            } else {
-                mv.kind = 1;
-                mv.lo = sk, mv.hi = n - 1, mv.split = n - 2;
-                mv.sz1 = n - 1 - sk, mv.sz2 = 1;
-                mv.ra = pos, mv.rb = n - 1, mv.dir = -1;
-                mv.clr = -1, mv.set = n >= 2 ? n - 2 : -1;
-            }
-            return mv;
-        } else {  // swap (:172-180)
-            if (n < 2) continue;
-            const int a = (int)lemire32(r[1], (uint32_t)n);
-            int b = (int)lemire32(r[2], (uint32_t)(n - 1));
-            if (b >= a) ++b;
-            mv.kind = 2;
-            mv.a = a, mv.b = b;
-            return mv;
-        }
-    }
-    return mv;
-}
-
-template <int P>
-__global__ void __launch_bounds__(1024, 1) k_chains(const ChainParams p) {
-    using L = Lane<P>;
-    extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
-    const int n = p.n, mb = p.mb;
-
-    const double2* tab = p.tab;
-    size_t off = 0;
-    if (p.smem_tab) {  // stage the (exec, deadline) table once per block
-        double2* st = reinterpret_cast<double2*>(smem);
-        const int total = mb * n;
-        for (int i = threadIdx.x; i < total; i += blockDim.x) st[i] = p.tab[i];
-        __syncthreads();
-        tab = st;
-        off = ((size_t)total * sizeof(double2) + 15) & ~(size_t)15;
-    }
-    constexpr int kSlot = ((64 * P + 4 * P) + 15) & ~15;
-    uint16_t* ent = reinterpret_cast<uint16_t*>(smem + off + (size_t)wid * kSlot);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(ent + 32 * P);
-
-    const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
-    if (gw >= p.chain_count) return;
-    const int n_my = (p.chain_count - gw + TW - 1) / TW;
-
-    uint64_t deadline = ~0ull;
-    if (p.budget_ns > 0) deadline = __shfl_sync(FULL, gtimer(), 0) + (uint64_t)p.budget_ns;
-
-    // per-chain registers (valid across levels when n_my == 1)
-    LaneSum cs;
-    const unsigned long long lane_pos = (unsigned long long)max(0, min(P, n - lane * P));
-    double cE = 0.0, cfmk = 0.0, cltot = 0.0, f = 0.0, best_f = 0.0;
-    int clnm = 0;
-    unsigned long long props = 0, accs = 0;
-    int stop = 0;
-
-    double t = p.t0;
-    for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
-        for (int k = 0; k < n_my; ++k) {
-            if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
-                stop = 1;
-                break;
-            }
-            const int c = gw + k * TW;
-            const uint32_t cid = (uint32_t)(p.chain_begin + c);
-            ChainRec* rc = p.rec + c;
-            if (lev == 0 || n_my > 1) {  // (re)load chain state
-                const uint16_t* se = lev == 0 ? p.start_ent : p.st_ent + (size_t)c * 32 * P;
-                const uint32_t* sb = lev == 0 ? p.start_bits : p.st_bits + (size_t)c * P;
-                for (int i = lane; i < 32 * P; i += 32) ent[i] = se[i];
-                for (int i = lane; i < P; i += 32) bits[i] = sb[i];
-                __syncwarp();
-                L::pass1(ent, bits, tab, n, lane, cs);
-                L::combine(cs, lane, cE, cfmk);
-                L::pass2(ent, bits, tab, n, lane, cE, cfmk, cltot, clnm);
-                const double tot = warp_sum(cltot);
-                const int nm = __reduce_add_sync(FULL, clnm);
-                f = tot > 0.0 ? (double)nm / tot : 0.0;
-                if (lev == 0) {
-                    best_f = f, props = 0, accs = 0;
-                    for (int i = lane; i < 32 * P; i += 32) p.best_ent[(size_t)c * 32 * P + i] = ent[i];
-                    for (int i = lane; i < P; i += 32) p.best_bits[(size_t)c * P + i] = bits[i];
-                    if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
-                } else {
-                    best_f = rc->g, props = rc->proposals, accs = rc->accepted;
-                }
-            }
-            const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
-            unsigned long long sc1 = 0, sc2 = 0;
-
-            for (int it = 0; it < p.iter; ++it) {
-                const uint32_t prop = (uint32_t)(lev * p.iter + it);
-                const Move mv = draw_move<P>(bits, n, mb, prop, cid, p.key0, p.key1);
-                // ---- apply the move in place (undo on reject)
-                int q = 0;
-                uint16_t old_q = 0;
-                uint32_t ow0 = 0, ow1 = 0;
-                int w0 = 0, w1 = 0;
-                int dlo = 0, dhi = -1, dx = -1;  // dirty lanes [dlo, dhi] plus dx
-                if (mv.kind == 1) {
-                    q = mv.lo + lane;
-                    const bool act = q <= mv.hi;
-                    uint16_t nw = 0;
-                    if (act) {
-                        int src = q;
-                        if (mv.dir > 0) src = q == mv.ra ? mv.rb : (q > mv.ra && q <= mv.rb ? q - 1 : q);
-                        else src = q == mv.rb ? mv.ra : (q >= mv.ra && q < mv.rb ? q + 1 : q);
-                        old_q = ent[L::phys(q)];
-                        const uint32_t s16 = ent[L::phys(src)];
-                        const int sz = q <= mv.split ? mv.sz1 : mv.sz2;
-                        nw = (uint16_t)((s16 & 0xFFFu) | ((uint32_t)(sz - 1) << 12));
-                    }
-                    w0 = mv.clr >= 0 ? mv.clr >> 5 : 0;
-                    w1 = mv.set >= 0 ? mv.set >> 5 : 0;
-                    ow0 = bits[w0], ow1 = bits[w1];
-                    __syncwarp();
-                    if (act) ent[L::phys(q)] = nw;
-                    if (lane == 0) {
-                        if (mv.clr >= 0) bits[mv.clr >> 5] &= ~(1u << (mv.clr & 31));
-                        if (mv.set >= 0) bits[mv.set >> 5] |= 1u << (mv.set & 31);
-                    }
-                    __syncwarp();
-                    dlo = L::lane_of(mv.lo), dhi = L::lane_of(mv.hi);
-                } else if (mv.kind == 2) {
-                    const uint32_t ea = ent[L::phys(mv.a)], eb = ent[L::phys(mv.b)];
-                    ow0 = ea, ow1 = eb;
-                    __syncwarp();
-                    if (lane == 0) {
-                        ent[L::phys(mv.a)] = (uint16_t)((ea & 0xF000u) | (eb & 0xFFFu));
-                        ent[L::phys(mv.b)] = (uint16_t)((eb & 0xF000u) | (ea & 0xFFFu));
-                    }
-                    __syncwarp();
-                    dlo = dhi = L::lane_of(mv.a);
-                    dx = L::lane_of(mv.b);
-                }
-                // ---- incremental objective: only dirty lanes redo pass 1; lanes whose inputs
-                //      are unchanged keep their cached pass-2 contribution
-                LaneSum ns = cs;
-                const bool dirty = (lane >= dlo && lane <= dhi) || lane == dx;
-                if (dirty) L::pass1(ent, bits, tab, n, lane, ns), sc1 += lane_pos;
-                double nE, nfmk;
-                L::combine(ns, lane, nE, nfmk);
-                double nltot = cltot;
-                int nlnm = clnm;
-                if (dirty || nE != cE || nfmk != cfmk)
-                    L::pass2(ent, bits, tab, n, lane, nE, nfmk, nltot, nlnm), sc2 += lane_pos;
-                const double tot = warp_sum(nltot);
-                const int nm = __reduce_add_sync(FULL, nlnm);
-                const double f_new = tot > 0.0 ? (double)nm / tot : 0.0;
-                ++props;
-                // ---- Metropolis (P:src/priority_mapper.cpp:385-391)
-                bool accept = f_new > f;
-                if (!accept) {
-                    const double x = (f - f_new) * scale / t;
-                    uint32_t r[4] = {prop, cid, (uint32_t)kAcceptAttempt, kTagMove};
-                    philox10(r, p.key0, p.key1);
-                    const double u = (double)((((uint64_t)r[0] << 32) | r[1]) >> 11) * 0x1.0p-53;
-                    accept = x < 38.0 ? u < exp(-x) : u == 0.0;
-                }
-                if (accept) {
-                    ++accs;
-                    cs = ns, cE = nE, cfmk = nfmk, cltot = nltot, clnm = nlnm, f = f_new;
-                    if (f > best_f) {
-                        best_f = f;
-                        for (int i = lane; i < 32 * P; i += 32) p.best_ent[(size_t)c * 32 * P + i] = ent[i];
-                        for (int i = lane; i < P; i += 32) p.best_bits[(size_t)c * P + i] = bits[i];
-                        if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
-                    }
-                } else if (mv.kind == 1) {
-                    if (q <= mv.hi) ent[L::phys(q)] = old_q;
-                    if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
-                    __syncwarp();
-                } else if (mv.kind == 2) {
-                    if (lane == 0) ent[L::phys(mv.a)] = (uint16_t)ow0, ent[L::phys(mv.b)] = (uint16_t)ow1;
-                    __syncwarp();
-                }
-            }
-            if (n_my > 1) {  // park the chain until the next level
-                for (int i = lane; i < 32 * P; i += 32) p.st_ent[(size_t)c * 32 * P + i] = ent[i];
-                for (int i = lane; i < P; i += 32) p.st_bits[(size_t)c * P + i] = bits[i];
-                __syncwarp();
-            }
-#pragma unroll
-            for (int d = 16; d; d >>= 1)
-                sc1 += __shfl_xor_sync(FULL, sc1, d), sc2 += __shfl_xor_sync(FULL, sc2, d);
-            if (lane == 0) {
-                rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
-                rc->scan1 += sc1, rc->scan2 += sc2;
-            }
-        }
-    }
-}
+#include "chains.cuh"
 
 // ================================================================ K4: argmax
 __device__ __forceinline__ bool better(double g, double t, int c, double bg, double bt, int bc) {
@@ -833,10 +478,10 @@ struct DevBuf {
     }
 };
 
-int pick_P(int n) {
-    int P = 1;
-    while (32 * P < n) P <<= 1;
-    return P;
+// units of 32 positions per lane: 1 (n <= 1024), 2 (<= 2048), 4 (<= 4096)
+int pick_upl(int n) {
+    const int units = (n + 31) / 32;
+    return units <= 32 ? 1 : (units <= 64 ? 2 : 4);
 }
 
 }  // namespace
@@ -857,7 +502,7 @@ struct slo_ctx {
     DevBuf e_perms, e_bits, e_n, e_t, e_g;
     bool prepared = false;
     slo_chain_params prm{};
-    int P = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
+    int UPL = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
     size_t smem = 0;
     bool smem_tab = false;
     double replay_scale = 0.0;
@@ -992,52 +637,44 @@ int count_levels(double t0, double t_thres, double tau) {
     return L;
 }
 
-template <int P>
+template <int UPL>
 int configure_chains(slo_ctx* c) {
     const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(double2);
-    const size_t slot = ((64 * P + 4 * P) + 15) & ~(size_t)15;
+    const size_t slot = slot_bytes<UPL>();
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
+    const int max_w = UPL == 1 ? 32 : 16;
     c->smem_tab = tab_smem + slot <= c->smem_optin;
     const size_t base = c->smem_tab ? tab_smem : 0;
-    int W = (int)std::min<size_t>(32, (c->smem_optin - base) / slot);
+    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
     W = std::max(1, std::min(W, c->chain_count));
     c->smem = base + (size_t)W * slot;
-    CK(cudaFuncSetAttribute(k_chains<P>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    CK(cudaFuncSetAttribute(k_chains<UPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<P>, W * 32, c->smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL>, W * 32, c->smem));
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
     c->block = W * 32;
     c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
     return SLO_OK;
 }
 
-int launch_chains_P(slo_ctx* c) {
-    switch (c->P) {
-#define CASE(PP)                                                                                   \
-    case PP:                                                                                       \
-        k_chains<PP><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);                            \
-        break;
-        CASE(1) CASE(2) CASE(4) CASE(8) CASE(16) CASE(32) CASE(64) CASE(128)
-#undef CASE
-        default:
-            return fail(SLO_ERR_CAPACITY, "bad P");
+int launch_chains_U(slo_ctx* c) {
+    switch (c->UPL) {
+        case 1: k_chains<1><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
+        case 2: k_chains<2><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
+        case 4: k_chains<4><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
+        default: return fail(SLO_ERR_CAPACITY, "bad units-per-lane");
     }
     CK(cudaGetLastError());
     return SLO_OK;
 }
 
-int configure_P(slo_ctx* c) {
-    switch (c->P) {
+int configure_U(slo_ctx* c) {
+    switch (c->UPL) {
         case 1: return configure_chains<1>(c);
         case 2: return configure_chains<2>(c);
         case 4: return configure_chains<4>(c);
-        case 8: return configure_chains<8>(c);
-        case 16: return configure_chains<16>(c);
-        case 32: return configure_chains<32>(c);
-        case 64: return configure_chains<64>(c);
-        case 128: return configure_chains<128>(c);
     }
-    return fail(SLO_ERR_CAPACITY, "bad P");
+    return fail(SLO_ERR_CAPACITY, "bad units-per-lane");
 }
 
 }  // namespace
@@ -1100,19 +737,17 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     }
     if (prm->rng_mode != SLO_RNG_PHILOX) return fail(SLO_ERR_ARG, "slo_chains_prepare: unknown rng_mode");
 
-    const int P = pick_P(n);
-    c->P = P;
-    const size_t ent_words = 32 * (size_t)P, bit_words = P;
-    // start state in the lane-major entry layout
+    const int UPL = pick_upl(n);
+    c->UPL = UPL;
+    const size_t ent_words = 1024 * (size_t)UPL, bit_words = 32 * (size_t)UPL;
+    // start state: linear entries (batch_size-1)*n + dense index, linear batch-end bitmask
     std::vector<uint16_t> ent(ent_words, 0);
     std::vector<uint32_t> bits(bit_words, 0);
     {
         int pos = 0;
         for (int k = 0; k < start_nb; ++k) {
-            for (int j = 0; j < start_sizes[k]; ++j, ++pos) {
-                const int phys = ((pos & (P - 1)) << 5) | (pos / P);
-                ent[phys] = (uint16_t)(start_perm[pos] | ((start_sizes[k] - 1) << 12));
-            }
+            for (int j = 0; j < start_sizes[k]; ++j, ++pos)
+                ent[pos] = (uint16_t)(start_perm[pos] + (start_sizes[k] - 1) * n);
             bits[(pos - 1) >> 5] |= 1u << ((pos - 1) & 31);
         }
     }
@@ -1126,7 +761,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     CK(c->win_ent.reserve(ent_words * sizeof(uint16_t)));
     CK(c->win_bits.reserve(bit_words * sizeof(uint32_t)));
     CK(c->scale_mult.reserve(std::max<size_t>(1, prm->n_scale_mult) * sizeof(double)));
-    if (int rc = configure_P(c)) return rc;
+    if (int rc = configure_U(c)) return rc;
     const int TW = c->grid * (c->block / 32);
     const bool multi = (int)cc > TW;
     if (multi) {
@@ -1141,6 +776,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
 
     ChainParams& kp = c->kp;
     kp.n = n, kp.mb = c->mb, kp.tab = c->tab.as<double2>(), kp.smem_tab = c->smem_tab ? 1 : 0;
+    kp.magic = (1ull << 32) / (uint64_t)n + 1;
     kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;
     kp.iter = prm->iter, kp.levels = c->levels;
     kp.scale_mult = c->scale_mult.as<double>(), kp.n_mult = prm->n_scale_mult;
@@ -1170,10 +806,10 @@ int slo_chains_launch(slo_ctx* c) {
         CK(cudaGetLastError());
         return SLO_OK;
     }
-    int rc = launch_chains_P(c);
+    int rc = launch_chains_U(c);
     if (rc) return rc;
     CK(cudaEventRecord(c->ev1, c->stream));
-    k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), 32 * c->P, c->P,
+    k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), 1024 * c->UPL, 32 * c->UPL,
                                         c->best_ent.as<uint16_t>(), c->best_bits.as<uint32_t>(),
                                         c->win_ent.as<uint16_t>(), c->win_bits.as<uint32_t>());
     CK(cudaGetLastError());
@@ -1190,8 +826,8 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     std::vector<uint32_t> bits;
     const bool replay = c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY;
     if (!replay) {
-        ent.resize(32 * (size_t)c->P);
-        bits.resize(c->P);
+        ent.resize(1024 * (size_t)c->UPL);
+        bits.resize(32 * (size_t)c->UPL);
         CK(cudaMemcpyAsync(ent.data(), c->win_ent.p, ent.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
         CK(cudaMemcpyAsync(bits.data(), c->win_bits.p, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     }
@@ -1206,10 +842,9 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
         CK(cudaMemcpy(best_sizes, c->r_best_sizes.as<int>() + (size_t)r.chain * n, (size_t)nb * sizeof(int), cudaMemcpyDeviceToHost));
         *best_nb = nb;
     } else {
-        const int P = c->P;
         int nb = 0, run = 0;
         for (int q = 0; q < n; ++q) {
-            best_perm[q] = ent[((q & (P - 1)) << 5) | (q / P)] & 0xFFF;
+            best_perm[q] = ent[q] % n;
             ++run;
             if ((bits[q >> 5] >> (q & 31)) & 1u) best_sizes[nb++] = run, run = 0;
         }
