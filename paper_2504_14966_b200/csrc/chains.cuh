@@ -2,7 +2,8 @@
 // Included by engine.cu inside its anonymous namespace.
 //
 // Chain state (shared memory, per warp):
-//   ent[q]   u16, q = position: combined table index (batch_size-1) * n + dense_index
+//   ent[q]   u16, q = position: combined table index (batch_size-1) * n + dense_index, so the
+//            table gather needs no index arithmetic and every entry carries its batch size
 //   bits[w]  u32 linear batch-end bitmask (bit q set iff q is the last position of a batch)
 //   rnd      the Philox words of the next 32 proposals, drawn lane-parallel
 // Objective: the schedule is cut into units of 32 consecutive positions. Each unit has a
@@ -14,6 +15,26 @@
 // move only the (<= 2) dirty units are re-summarised.
 
 #define kNegInf (-static_cast<double>(INFINITY))
+constexpr int kRndWords = 16;  // per proposal: attempts 0-3 (3 words each) + acceptance (2)
+constexpr int kPreAttempts = 4;
+
+struct UnitSum {
+    double hm;    // max exec from the unit start through its first batch end (whole unit if none)
+    double tm;    // max exec after the unit's last batch end
+    double inner; // summed makespans of batches that start and end inside the unit
+    double bs;    // sum of exec over the unit + sum over inner batches of makespan * positions after it
+    float dmax;   // upper bound of the unit's deadlines (rounded up; -inf if none)
+    int fe;       // unit contains a batch end
+    int cnt;      // positions in the unit
+    int A;        // positions after the first batch end
+};
+
+template <int UPL>
+struct __align__(16) ChainState {  // per-lane registers: this lane's unit summaries + SLO-walk cache
+    UnitSum s[UPL];
+    double wE[UPL], wF[UPL];
+    int wN[UPL];
+};
 
 struct ChainParams {
     int n, mb;
@@ -29,28 +50,29 @@ struct ChainParams {
     long long budget_ns;
     const uint16_t* start_ent;   // [1024*UPL]
     const uint32_t* start_bits;  // [32*UPL]
-    uint16_t* st_ent;            // [chain_count][1024*UPL]  parked state (several chains per warp)
+    const void* start_sum;       // ChainState<UPL>[32]: the start state's summaries (k_start)
+    const double* start_obj;     // {f, total, n_met} of the start state (k_start)
+    uint16_t* st_ent;            // [chain_count][1024*UPL]  parked chains (several chains per warp)
     uint32_t* st_bits;           // [chain_count][32*UPL]
+    void* st_sum;                // [chain_count][32] ChainState<UPL>
     uint16_t* best_ent;          // [chain_count][1024*UPL]
     uint32_t* best_bits;         // [chain_count][32*UPL]
     ChainRec* rec;
-};
-
-struct UnitSum {
-    double hm;    // max exec from the unit start through its first batch end (whole unit if none)
-    double tm;    // max exec after the unit's last batch end
-    double inner; // summed makespans of batches that start and end inside the unit
-    double bs;    // sum of exec over the unit + sum over inner batches of makespan * positions after it
-    float dmax;   // upper bound of the unit's deadlines (rounded up; -inf if none)
-    int fe;       // unit contains a batch end
-    int cnt;      // positions in the unit
-    int A;        // positions after the first batch end
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
     return v;
+}
+
+// order-preserving map float -> u32 (for REDUX max)
+__device__ __forceinline__ uint32_t f2key(float f) {
+    const uint32_t b = __float_as_uint(f);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+__device__ __forceinline__ float key2f(uint32_t k) {
+    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
 }
 
 // segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
@@ -86,12 +108,10 @@ __device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint3
     const bool inner_end = ((w >> lane) & 1u) && lane != f;
     const double mk = inner_end ? m : 0.0;
     double inner = mk, bs = e + mk * (double)(cnt - 1 - lane);
-    float dm = __double2float_ru(D);
 #pragma unroll
-    for (int d = 16; d; d >>= 1) {  // three interleaved butterfly reductions
+    for (int d = 16; d; d >>= 1) {  // two interleaved butterfly reductions
         inner += __shfl_xor_sync(FULL, inner, d);
         bs += __shfl_xor_sync(FULL, bs, d);
-        dm = fmaxf(dm, __shfl_xor_sync(FULL, dm, d));
     }
     s.fe = w != 0;
     s.cnt = cnt;
@@ -100,7 +120,7 @@ __device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint3
     s.tm = (w == 0 || la < cnt - 1) ? m_last : 0.0;
     s.inner = inner;
     s.bs = bs;
-    s.dmax = dm;
+    s.dmax = key2f(__reduce_max_sync(FULL, f2key(__double2float_ru(D))));
     return s;
 }
 
@@ -130,7 +150,7 @@ __device__ __noinline__ int unit_met(const uint16_t* ent, const uint32_t* bits, 
     return __popc(__ballot_sync(FULL, met));
 }
 
-// Philox words of (proposal, chain, attempt) -- out of line: only retries >= 2 need it
+// Philox words of (proposal, chain, attempt) -- out of line: only retries >= kPreAttempts need it
 __device__ __noinline__ uint4 philox_draw(uint32_t prop, uint32_t cid, uint32_t attempt, uint32_t k0, uint32_t k1) {
     uint32_t r[4] = {prop, cid, attempt, kTagMove};
     philox10(r, k0, k1);
@@ -145,17 +165,20 @@ struct Move {
     int a, b;        // swap positions
 };
 
-// The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the bitmask
-// representation. Attempts 0 and 1 read the lane-parallel Philox block (rw[0..5]); further
-// retries draw directly. Counter = (proposal, chain, attempt, tag): geometry-independent.
-__device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, uint32_t prop, uint32_t cid,
-                                          uint32_t k0, uint32_t k1, const uint32_t* rw) {
+// The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the entry /
+// bitmask representation: batch sizes come from the entries, batch starts from one bit search.
+// Attempts < kPreAttempts read the lane-parallel Philox block; later retries draw directly.
+// Counter = (proposal, chain, attempt, tag): results do not depend on the launch geometry.
+__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint32_t nn,
+                                          uint64_t magic, uint32_t prop, uint32_t cid, uint32_t k0, uint32_t k1,
+                                          const uint32_t* rw) {
+    auto size_at = [&](int q) { return (int)(((uint64_t)ent[q] * magic) >> 32) + 1; };
     Move mv;
     mv.kind = 0;
     if (n == 0) return mv;
     for (int attempt = 0; attempt <= 8; ++attempt) {
         uint32_t r0, r1, r2;
-        if (attempt < 2) {
+        if (attempt < kPreAttempts) {
             r0 = rw[3 * attempt], r1 = rw[3 * attempt + 1], r2 = rw[3 * attempt + 2];
         } else {
             const uint4 r = philox_draw(prop, cid, (uint32_t)attempt, k0, k1);
@@ -163,29 +186,30 @@ __device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, u
         }
         const uint32_t op = attempt < 8 ? lemire32(r0, 3) : 2u;  // forced swap after 8 misses
         if (op == 0) {  // squeeze (:141-153)
-            const int first = next_end(bits, 0) + 1;
+            const int first = size_at(0);
             if (first >= n) continue;
             const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
             const int sk = prev_end(bits, pos) + 1;
-            const int skm1 = prev_end(bits, sk - 1) + 1;
-            if (sk - skm1 >= mb) continue;
-            const int ek = next_end(bits, pos);
+            const int prev_size = size_at(sk - 1);
+            if (prev_size >= mb) continue;
+            const int ek = sk + size_at(sk) - 1;
             mv.kind = 1;
-            mv.lo = skm1, mv.hi = ek, mv.split = sk;
-            mv.sz1 = sk - skm1 + 1, mv.sz2 = ek - sk;
+            mv.lo = sk - prev_size, mv.hi = ek, mv.split = sk;
+            mv.sz1 = prev_size + 1, mv.sz2 = ek - sk;
             mv.ra = sk, mv.rb = pos, mv.dir = 1;
             mv.clr = sk - 1, mv.set = sk;
             return mv;
         } else if (op == 1) {  // delay (:155-170)
             const int pos = (int)lemire32(r1, (uint32_t)n);
             const int sk = prev_end(bits, pos) + 1;
-            const int ek = next_end(bits, pos);
+            const int ek = sk + size_at(pos) - 1;
             if (ek < n - 1) {
-                const int ek1 = next_end(bits, ek + 1);
-                if (ek1 - ek >= mb) continue;
+                const int next_size = size_at(ek + 1);
+                if (next_size >= mb) continue;
+                const int ek1 = ek + next_size;
                 mv.kind = 1;
                 mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
-                mv.sz1 = ek - sk, mv.sz2 = ek1 - ek + 1;
+                mv.sz1 = ek - sk, mv.sz2 = next_size + 1;
                 mv.ra = pos, mv.rb = ek1, mv.dir = -1;
                 mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
             } else {
@@ -208,13 +232,6 @@ __device__ __forceinline__ Move draw_move(const uint32_t* bits, int n, int mb, u
     }
     return mv;
 }
-
-template <int UPL>
-struct ChainState {  // per-lane registers: summaries of this lane's units + SLO-walk cache
-    UnitSum s[UPL];
-    double wE[UPL], wF[UPL];
-    int wN[UPL];
-};
 
 // Warp-wide scan over unit summaries: E[k] (start elapsed) and fmk[k] for this lane's units.
 template <int UPL>
@@ -317,8 +334,8 @@ __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
-    // entries + bitmask + two parked unit summaries + Philox block (32 proposals x 8 words)
-    return 1024 * UPL * 2 + 32 * UPL * 4 + 2 * (int)sizeof(UnitSum) + 32 * 8 * 4;
+    // entries + bitmask + two parked unit summaries + Philox block (32 proposals)
+    return 1024 * UPL * 2 + 32 * UPL * 4 + 2 * (int)sizeof(UnitSum) + 32 * kRndWords * 4;
 }
 
 template <int UPL>
@@ -327,6 +344,32 @@ __device__ __forceinline__ void copy_state(uint16_t* de, uint32_t* db, const uin
     constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
     for (int i = lane; i < kEnt / 8; i += 32) reinterpret_cast<uint4*>(de)[i] = reinterpret_cast<const uint4*>(se)[i];
     for (int i = lane; i < kBits; i += 32) db[i] = sb[i];
+}
+
+// Prologue: one warp evaluates the start schedule shared by every chain and publishes its
+// unit summaries, so the chains start without a full evaluation each.
+template <int UPL>
+__global__ void __launch_bounds__(32) k_start(const ChainParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int lane = threadIdx.x;
+    uint16_t* ent = reinterpret_cast<uint16_t*>(smem);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 1024 * UPL * 2);
+    copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
+    __syncwarp();
+    ChainState<UPL> cs;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) cs.wE[k] = 0.0, cs.wF[k] = 0.0, cs.wN[k] = 0;
+    double tot, E[UPL], fmk[UPL];
+    int nm, nN[UPL];
+    unsigned long long sc1 = 0, sc2 = 0;
+    evaluate_chain<UPL>(cs, ent, bits, p.tab, p.n, p.mb, lane, true, -1, -1, tot, nm, E, fmk, nN, sc1, sc2);
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) cs.wE[k] = E[k], cs.wF[k] = fmk[k], cs.wN[k] = nN[k];
+    reinterpret_cast<ChainState<UPL>*>(const_cast<void*>(p.start_sum))[lane] = cs;
+    if (lane == 0) {
+        double* o = const_cast<double*>(p.start_obj);
+        o[0] = tot > 0.0 ? (double)nm / tot : 0.0, o[1] = tot, o[2] = (double)nm;
+    }
 }
 
 template <int UPL>
@@ -360,13 +403,12 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
     if (p.budget_ns > 0) deadline = __shfl_sync(FULL, gtimer(), 0) + (uint64_t)p.budget_ns;
 
     ChainState<UPL> cs;
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) cs.wE[k] = 0.0, cs.wF[k] = 0.0, cs.wN[k] = 0;
     double f = 0.0, best_f = 0.0;
     unsigned long long props = 0, accs = 0;
     int stop = 0;
     const uint32_t nn = (uint32_t)n;
     const uint64_t magic = p.magic;
+    auto* parked = reinterpret_cast<ChainState<UPL>*>(p.st_sum);
 
     double t = p.t0;
     for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
@@ -379,33 +421,41 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
             const uint32_t cid = (uint32_t)(p.chain_begin + c);
             ChainRec* rc = p.rec + c;
             unsigned long long sc1 = 0, sc2 = 0;
-            const bool load = lev == 0 || n_my > 1;
-            if (load) {  // (re)load the chain state; it is evaluated in full below (it = -1)
-                copy_state<UPL>(ent, bits, lev == 0 ? p.start_ent : p.st_ent + (size_t)c * kEnt,
-                                lev == 0 ? p.start_bits : p.st_bits + (size_t)c * kBits, lane);
+            if (lev == 0) {  // every chain starts from the shared start state
+                copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
+                cs = reinterpret_cast<const ChainState<UPL>*>(p.start_sum)[lane];
+                f = best_f = p.start_obj[0], props = 0, accs = 0;
                 __syncwarp();
-                if (lev > 0) best_f = rc->g, props = rc->proposals, accs = rc->accepted;
+                copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits, lane);
+                if (lane == 0) rc->g = f, rc->t = p.start_obj[1], rc->n_met = (int)p.start_obj[2];
+            } else if (n_my > 1) {  // resume a parked chain
+                copy_state<UPL>(ent, bits, p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, lane);
+                cs = parked[(size_t)c * 32 + lane];
+                f = rc->cur_f, best_f = rc->g, props = rc->proposals, accs = rc->accepted;
+                __syncwarp();
             }
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
 
-            for (int it = load ? -1 : 0; it < p.iter; ++it) {
-                const bool full = it < 0;
-                const uint32_t prop = (uint32_t)(lev * p.iter + max(it, 0));
-                if (!full && (it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0, 1 and accept
-                    uint32_t r[4] = {prop + (uint32_t)lane, cid, 0u, kTagMove};
+            for (int it = 0; it < p.iter; ++it) {
+                const uint32_t prop = (uint32_t)(lev * p.iter + it);
+                if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..3 and acceptance
+                    uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
+                    uint32_t w[kRndWords];
+#pragma unroll
+                    for (int a = 0; a < kPreAttempts; ++a) {
+                        uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)a, kTagMove};
+                        philox10(r, p.key0, p.key1);
+                        w[3 * a] = r[0], w[3 * a + 1] = r[1], w[3 * a + 2] = r[2];
+                    }
+                    uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)kAcceptAttempt, kTagMove};
                     philox10(r, p.key0, p.key1);
-                    uint32_t r1[4] = {prop + (uint32_t)lane, cid, 1u, kTagMove};
-                    philox10(r1, p.key0, p.key1);
-                    uint32_t a[4] = {prop + (uint32_t)lane, cid, (uint32_t)kAcceptAttempt, kTagMove};
-                    philox10(a, p.key0, p.key1);
-                    reinterpret_cast<uint4*>(rnd)[2 * lane] = make_uint4(r[0], r[1], r[2], r1[0]);
-                    reinterpret_cast<uint4*>(rnd)[2 * lane + 1] = make_uint4(r1[1], r1[2], a[0], a[1]);
+                    w[12] = r[0], w[13] = r[1], w[14] = 0, w[15] = 0;
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
                     __syncwarp();
                 }
-                const uint32_t* rw = rnd + 8 * (max(it, 0) & 31);
-                Move mv;
-                mv.kind = 0;
-                if (!full) mv = draw_move(bits, n, mb, prop, cid, p.key0, p.key1, rw);
+                const uint32_t* rw = rnd + kRndWords * (it & 31);
+                const Move mv = draw_move(ent, bits, n, mb, nn, magic, prop, cid, p.key0, p.key1, rw);
 
                 // ---- apply in place (undo on reject)
                 int q = 0;
@@ -455,26 +505,20 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
                 }
                 double tot, E[UPL], fmk[UPL];
                 int nm, nN[UPL];
-                evaluate_chain<UPL>(cs, ent, bits, tab, n, mb, lane, full, du0, du1, tot, nm, E, fmk, nN, sc1, sc2);
+                evaluate_chain<UPL>(cs, ent, bits, tab, n, mb, lane, false, du0, du1, tot, nm, E, fmk, nN, sc1, sc2);
                 const double f_new = tot > 0.0 ? (double)nm / tot : 0.0;
-                bool accept;
-                if (full) {
-                    accept = true;
-                } else {
-                    ++props;
-                    accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
-                    if (!accept) {
-                        const double x = (f - f_new) * scale / t;
-                        const double u = (double)((((uint64_t)rw[6] << 32) | rw[7]) >> 11) * 0x1.0p-53;
-                        accept = x < 38.0 ? u < exp(-x) : u == 0.0;
-                    }
+                ++props;
+                bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
+                if (!accept) {
+                    const double x = (f - f_new) * scale / t;
+                    const double u = (double)((((uint64_t)rw[12] << 32) | rw[13]) >> 11) * 0x1.0p-53;
+                    accept = x < 38.0 ? u < exp(-x) : u == 0.0;
                 }
                 if (accept) {
-                    accs += full ? 0 : 1;
+                    ++accs;
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) cs.wE[kk] = E[kk], cs.wF[kk] = fmk[kk], cs.wN[kk] = nN[kk];
                     f = f_new;
-                    if (full && lev == 0) best_f = -1.0, props = 0, accs = 0;
                     if (f > best_f) {
                         best_f = f;
                         copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,
@@ -496,8 +540,9 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
                     __syncwarp();
                 }
             }
-            if (n_my > 1) {  // park the chain until the next level
+            if (n_my > 1) {  // park the chain (state + summaries) until the next level
                 copy_state<UPL>(p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, ent, bits, lane);
+                parked[(size_t)c * 32 + lane] = cs;
                 __syncwarp();
             }
             if (lane == 0) {

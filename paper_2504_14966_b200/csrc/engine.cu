@@ -495,7 +495,8 @@ struct slo_ctx {
     int n = 0, mb = 0;
     DevBuf tab, exec_soa, dl_soa;
     // chains
-    DevBuf st_ent, st_bits, best_ent, best_bits, rec, start_ent, start_bits, scale_mult, result, win_ent, win_bits;
+    DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
+        result, win_ent, win_bits;
     // replay
     DevBuf r_scratch, r_best_perm, r_best_sizes, r_best_nb, r_start_perm, r_start_sizes;
     // K1
@@ -657,15 +658,30 @@ int configure_chains(slo_ctx* c) {
     return SLO_OK;
 }
 
+// prologue (start-state summaries, one warp) then the chain kernel
 int launch_chains_U(slo_ctx* c) {
+    const size_t ss = 1024 * (size_t)c->UPL * 2 + 32 * (size_t)c->UPL * 4;
     switch (c->UPL) {
-        case 1: k_chains<1><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
-        case 2: k_chains<2><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
-        case 4: k_chains<4><<<c->grid, c->block, c->smem, c->stream>>>(c->kp); break;
+        case 1:
+            k_start<1><<<1, 32, ss, c->stream>>>(c->kp);
+            k_chains<1><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+            break;
+        case 2:
+            k_start<2><<<1, 32, ss, c->stream>>>(c->kp);
+            k_chains<2><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+            break;
+        case 4:
+            k_start<4><<<1, 32, ss, c->stream>>>(c->kp);
+            k_chains<4><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+            break;
         default: return fail(SLO_ERR_CAPACITY, "bad units-per-lane");
     }
     CK(cudaGetLastError());
     return SLO_OK;
+}
+
+size_t chain_state_bytes(int upl) {
+    return upl == 1 ? sizeof(ChainState<1>) : (upl == 2 ? sizeof(ChainState<2>) : sizeof(ChainState<4>));
 }
 
 int configure_U(slo_ctx* c) {
@@ -764,9 +780,13 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     if (int rc = configure_U(c)) return rc;
     const int TW = c->grid * (c->block / 32);
     const bool multi = (int)cc > TW;
+    const size_t csb = chain_state_bytes(UPL);
+    CK(c->start_sum.reserve(32 * csb));
+    CK(c->start_obj.reserve(4 * sizeof(double)));
     if (multi) {
         CK(c->st_ent.reserve(cc * ent_words * sizeof(uint16_t)));
         CK(c->st_bits.reserve(cc * bit_words * sizeof(uint32_t)));
+        CK(c->st_sum.reserve(cc * 32 * csb));
     }
     CK(cudaMemcpyAsync(c->start_ent.p, ent.data(), ent_words * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->start_bits.p, bits.data(), bit_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
@@ -785,6 +805,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     kp.budget_ns = prm->budget_ns;
     kp.start_ent = c->start_ent.as<uint16_t>(), kp.start_bits = c->start_bits.as<uint32_t>();
     kp.st_ent = multi ? c->st_ent.as<uint16_t>() : nullptr, kp.st_bits = multi ? c->st_bits.as<uint32_t>() : nullptr;
+    kp.st_sum = multi ? c->st_sum.p : nullptr;
+    kp.start_sum = c->start_sum.p, kp.start_obj = c->start_obj.as<double>();
     kp.best_ent = c->best_ent.as<uint16_t>(), kp.best_bits = c->best_bits.as<uint32_t>();
     kp.rec = c->rec.as<ChainRec>();
     c->prepared = true;
