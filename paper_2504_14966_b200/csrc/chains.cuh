@@ -15,8 +15,9 @@
 // move only the (<= 2) dirty units are re-summarised.
 
 #define kNegInf (-static_cast<double>(INFINITY))
-constexpr int kRndWords = 16;  // per proposal: attempts 0-3 (3 words each) + acceptance (2)
-constexpr int kPreAttempts = 4;
+constexpr int kPreAttempts = 6;                      // move attempts drawn ahead (3 words each)
+constexpr int kRndWords = 3 * kPreAttempts + 2;      // + the acceptance uniform (2 words)
+static_assert(kRndWords % 4 == 0, "Philox block rows are stored as uint4");
 
 struct UnitSum {
     double hm;    // max exec from the unit start through its first batch end (whole unit if none)
@@ -234,36 +235,18 @@ __device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* b
 }
 
 // Warp-wide scan over unit summaries: E[k] (start elapsed) and fmk[k] for this lane's units.
+// Batches hold at most 16 positions, so every non-empty unit of 32 contains a batch end (the
+// last, partial unit ends at position n-1): the batch open at a unit's start is exactly the
+// previous unit's tail, and only the elapsed times need a scan.
 template <int UPL>
 __device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lane, double (&E)[UPL],
                                               double (&fmk)[UPL]) {
-    int F = 0;
-    double M = 0.0, head = 0.0, rest = 0.0;
+    double rest = cs.s[0].inner;
 #pragma unroll
-    for (int k = 0; k < UPL; ++k) {
-        const UnitSum& s = cs.s[k];
-        if (!F) {
-            if (s.fe) head = fmax(M, s.hm), rest = s.inner, M = s.tm, F = 1;
-            else M = fmax(M, s.hm);
-        } else {
-            if (s.fe) rest = rest + fmax(M, s.hm), rest = rest + s.inner, M = s.tm;
-            else M = fmax(M, s.hm);
-        }
-    }
-    int Fs = F;
-    double Ms = M;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // segmented max scan of open-batch maxima
-        const double Mu = __shfl_up_sync(FULL, Ms, d);
-        const int Fu = __shfl_up_sync(FULL, Fs, d);
-        if (lane >= d) {
-            if (!Fs) Ms = fmax(Mu, Ms);
-            Fs |= Fu;
-        }
-    }
-    double carry = __shfl_up_sync(FULL, Ms, 1);
+    for (int k = 1; k < UPL; ++k) rest = rest + fmax(cs.s[k - 1].tm, cs.s[k].hm), rest = rest + cs.s[k].inner;
+    double carry = __shfl_up_sync(FULL, cs.s[UPL - 1].tm, 1);
     if (lane == 0) carry = 0.0;
-    double S = F ? fmax(carry, head) + rest : 0.0;
+    double S = cs.s[0].fe ? fmax(carry, cs.s[0].hm) + rest : 0.0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {  // sum scan of the makespans closed in each lane
         const double v = __shfl_up_sync(FULL, S, d);
@@ -277,9 +260,13 @@ __device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lan
         const UnitSum& s = cs.s[k];
         E[k] = el;
         fmk[k] = fmax(cm, s.hm);
-        if (s.fe) el = el + fmk[k], el = el + s.inner, cm = s.tm;
-        else cm = fmax(cm, s.hm);
+        el = el + fmk[k], el = el + s.inner, cm = s.tm;
     }
+}
+
+// objective G = n / t (reference :278); the reciprocal form is used identically everywhere
+__device__ __forceinline__ double objective(int nm, double tot) {
+    return tot > 0.0 ? (double)nm * __drcp_rn(tot) : 0.0;
 }
 
 // Objective of the current state. full: re-summarise every unit and re-walk every live unit;
@@ -368,12 +355,12 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     reinterpret_cast<ChainState<UPL>*>(const_cast<void*>(p.start_sum))[lane] = cs;
     if (lane == 0) {
         double* o = const_cast<double*>(p.start_obj);
-        o[0] = tot > 0.0 ? (double)nm / tot : 0.0, o[1] = tot, o[2] = (double)nm;
+        o[0] = objective(nm, tot), o[1] = tot, o[2] = (double)nm;
     }
 }
 
 template <int UPL>
-__global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const ChainParams p) {
+__global__ void __launch_bounds__(UPL == 1 ? 768 : 512, 1) k_chains(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = p.n, mb = p.mb;
@@ -412,6 +399,7 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
 
     double t = p.t0;
     for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
+        const double inv_t = 1.0 / t;
         for (int k = 0; k < n_my; ++k) {
             if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
                 stop = 1;
@@ -449,9 +437,10 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
                     }
                     uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)kAcceptAttempt, kTagMove};
                     philox10(r, p.key0, p.key1);
-                    w[12] = r[0], w[13] = r[1], w[14] = 0, w[15] = 0;
+                    w[3 * kPreAttempts] = r[0], w[3 * kPreAttempts + 1] = r[1];
 #pragma unroll
-                    for (int v = 0; v < 4; ++v) dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
+                    for (int v = 0; v < kRndWords / 4; ++v)
+                        dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
                     __syncwarp();
                 }
                 const uint32_t* rw = rnd + kRndWords * (it & 31);
@@ -506,13 +495,16 @@ __global__ void __launch_bounds__(UPL == 1 ? 1024 : 512, 1) k_chains(const Chain
                 double tot, E[UPL], fmk[UPL];
                 int nm, nN[UPL];
                 evaluate_chain<UPL>(cs, ent, bits, tab, n, mb, lane, false, du0, du1, tot, nm, E, fmk, nN, sc1, sc2);
-                const double f_new = tot > 0.0 ? (double)nm / tot : 0.0;
+                const double f_new = objective(nm, tot);
                 ++props;
                 bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
                 if (!accept) {
-                    const double x = (f - f_new) * scale / t;
-                    const double u = (double)((((uint64_t)rw[12] << 32) | rw[13]) >> 11) * 0x1.0p-53;
-                    accept = x < 38.0 ? u < exp(-x) : u == 0.0;
+                    // x = (f - f_new) * scale / t; the test u < exp(-x) runs on the SFU in fp32
+                    // (relative error ~1e-7 on the acceptance probability)
+                    const double x = (f - f_new) * scale * inv_t;
+                    const uint32_t* ru = rw + 3 * kPreAttempts;
+                    const double u = (double)((((uint64_t)ru[0] << 32) | ru[1]) >> 11) * 0x1.0p-53;
+                    accept = x < 38.0 ? (float)u < __expf(-(float)x) : u == 0.0;
                 }
                 if (accept) {
                     ++accs;

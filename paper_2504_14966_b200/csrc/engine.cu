@@ -643,7 +643,7 @@ int configure_chains(slo_ctx* c) {
     const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(double2);
     const size_t slot = slot_bytes<UPL>();
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
-    const int max_w = UPL == 1 ? 32 : 16;
+    const int max_w = UPL == 1 ? 24 : 16;
     c->smem_tab = tab_smem + slot <= c->smem_optin;
     const size_t base = c->smem_tab ? tab_smem : 0;
     int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
