@@ -255,18 +255,7 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
 
-    def exchange(res):
-        """best-of-GPUs: all-gather (g, t, chain) and broadcast the winner's schedule."""
-        if world == 1:
-            return res.g, res.chain
-        rec = torch.tensor([res.g, res.t, float(res.chain)], dtype=torch.float64, device=f"cuda:{local}")
-        allrec = torch.empty(world, 3, dtype=torch.float64, device=f"cuda:{local}")
-        dist.all_gather_into_tensor(allrec, rec)
-        a = allrec.cpu().numpy()
-        win = max(range(world), key=lambda r_: (a[r_, 0], -a[r_, 1], -a[r_, 2]))
-        perm = torch.zeros(n, dtype=torch.int32, device=f"cuda:{local}")
-        dist.broadcast(perm, src=win)
-        return a[win, 0], int(a[win, 2])
+    from paper_2504_14966_b200.distributed import LocalBest, exchange_best
 
     def step():
         with torch.cuda.stream(stream):
@@ -276,7 +265,9 @@ def run_ours(args):
         eng.launch()
         e1.record(stream)
         bp, bs, res = eng.fetch()
-        exchange(res)
+        if world > 1:  # best-of-GPUs: all-gather (g, t, chain), broadcast the winner's schedule
+            exchange_best(LocalBest(res.g, res.t, res.chain, np.asarray(ids, dtype=np.int32)[bp], bs), n,
+                          device=f"cuda:{local}")
         return e0, e1, res
 
     for _ in range(args.warmup):
@@ -326,14 +317,9 @@ def run_ours(args):
         t0 = time.perf_counter()
         seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids, c, cfg, mb)
         if dist:
-            rec = torch.tensor([g, t_ms, float(n_met)], dtype=torch.float64, device=f"cuda:{local}")
-            allrec = torch.empty(world, 3, dtype=torch.float64, device=f"cuda:{local}")
-            dist.all_gather_into_tensor(allrec, rec)
-            a = allrec.cpu().numpy()
-            win = max(range(world), key=lambda r_: (a[r_, 0], -a[r_, 1], -r_))
-            buf = torch.from_numpy(np.ascontiguousarray(seq)).to(f"cuda:{local}")
-            dist.broadcast(buf, src=win)
-            g, n_met = float(a[win, 0]), int(a[win, 2])
+            _, seq, sizes, (g, n_met) = exchange_best(
+                LocalBest(st.engine_g, st.engine_t, st.best_chain, seq, sizes, g, n_met), n, device=f"cuda:{local}",
+                return_record=True)
         e2e_s += time.perf_counter() - t0
         e2e_props += st.proposals
         final = (n_met, g, st)
@@ -355,17 +341,28 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (k_chains): bytes the incremental evaluator walks
-    # per position: pass 1 = 2 B entry + 8 B exec, pass 2 = 2 B entry + 16 B (exec, deadline)
-    alg_bytes = 10.0 * pos1 + 18.0 * pos2
-    achieved_gbs = alg_bytes / (kern_ms / 1e3) / 1e9
-    roof = {"bound": "smem", "achieved": achieved_gbs, "peak": smem_peak_gbs, "unit": "GB/s",
-            "frac": (achieved_gbs / smem_peak_gbs) if smem_peak_gbs else None, "traffic": None,
-            "peak_source": "measured in-process: slo_probe_smem_bandwidth (conflict-free LDS.128 on all SMs); "
-                           "MEASURED_PEAKS.json has no shared-memory figure",
+    # ---- roofline of the dominant kernel (k_chains). It is instruction-issue bound (ncu: ~76%
+    # issue slots busy, DRAM ~1%, L1 ~52%), so the roofline is warp-instruction issue:
+    # achieved = (ncu-measured instructions per proposal, profiles/r1) x proposals this run
+    # evaluated / the kernel's CUDA-event time; peak = 4 issue slots x SMs x the SM clock sampled
+    # during the timed region. The shared-memory view (bytes the evaluator gathers) is kept beside.
+    prof = load_profile_summary()
+    clk = clocks.summary()
+    sm_mhz = clk.get("sm_mhz") or measured_peaks().get("sm_max_mhz") or 1965.0
+    n_sms = eng.sm_count
+    peak_ginst = 4 * n_sms * sm_mhz * 1e6 / 1e9
+    ipp = prof.get("instr_per_proposal") if prof else None
+    achieved_ginst = (ipp * props / (kern_ms / 1e3) / 1e9) if ipp else None
+    smem_bytes = 18.0 * (pos1 + pos2)  # 2 B entry + 16 B (exec, deadline) per gathered position
+    roof = {"bound": "issue", "achieved": achieved_ginst, "peak": peak_ginst, "unit": "Gwarp-inst/s",
+            "frac": (achieved_ginst / peak_ginst) if achieved_ginst else None,
+            "traffic": (prof["dram_bytes_per_proposal"] * props / args.steps) if prof else None,
             "kernel": "k_chains", "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
-            "bytes_per_launch": alg_bytes / args.steps,
-            "positions_per_proposal": (pos1 + pos2) / props if props else None}
+            "instr_per_proposal": ipp, "instr_source": "profiles/r1/k_chains_summary.json (ncu --set full)",
+            "peak_source": f"4 warp-inst/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz (sampled under load)",
+            "smem_view": {"achieved_gbs": smem_bytes / (kern_ms / 1e3) / 1e9, "peak_gbs": smem_peak_gbs,
+                          "peak_source": "slo_probe_smem_bandwidth (conflict-free LDS.128, all SMs, measured here)",
+                          "positions_gathered_per_proposal": (pos1 + pos2) / props if props else None}}
     attain_n, attain_g, st = final
     cpu = None
     if not args.no_cpu_baseline and world == 1:
@@ -401,6 +398,23 @@ def run_ours(args):
     print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
+
+
+def load_profile_summary():
+    path = os.path.join(ROOT, "profiles", "r1", "k_chains_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except OSError:
+        return None
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {}
 
 
 def eng_probe(eng):

@@ -54,7 +54,7 @@ typedef struct {
     int32_t shortcut;
     double g_sorted_start, g_input_start, objective_scale_used;
     int32_t chains_run, levels_run, best_chain;
-    double engine_g, kernel_ms;
+    double engine_g, engine_t, kernel_ms;
 } slosched_anneal_stats;
 
 const char* slosched_last_error(void);

@@ -218,6 +218,7 @@ struct AnnealStats {
     int levels_run = 0;
     int best_chain = -1;
     double engine_g = 0.0;    // best score as computed on the device
+    double engine_t = 0.0;    // its summed latency (tie-break of the best-of-chains argmax)
     double kernel_ms = 0.0;   // device time of the annealing launch
 };
 

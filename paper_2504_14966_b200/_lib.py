@@ -36,7 +36,7 @@ class SloAnnealStats(Structure):
     _fields_ = [("proposals", c_uint64), ("accepted", c_uint64), ("shortcut", c_int32),
                 ("g_sorted_start", c_double), ("g_input_start", c_double), ("objective_scale_used", c_double),
                 ("chains_run", c_int32), ("levels_run", c_int32), ("best_chain", c_int32),
-                ("engine_g", c_double), ("kernel_ms", c_double)]
+                ("engine_g", c_double), ("engine_t", c_double), ("kernel_ms", c_double)]
 
 
 class SloChainParams(Structure):

@@ -112,6 +112,7 @@ void stats_out(const AnnealStats& s, slosched_anneal_stats* o) {
     o->levels_run = s.levels_run;
     o->best_chain = s.best_chain;
     o->engine_g = s.engine_g;
+    o->engine_t = s.engine_t;
     o->kernel_ms = s.kernel_ms;
 }
 

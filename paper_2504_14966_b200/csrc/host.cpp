@@ -595,6 +595,7 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     res.stats.levels_run = cr.levels_run;
     res.stats.best_chain = cr.chain;
     res.stats.engine_g = cr.g;
+    res.stats.engine_t = cr.t;
     res.stats.kernel_ms = cr.kernel_ms;
 
     Schedule best;

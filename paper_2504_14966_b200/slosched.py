@@ -331,12 +331,14 @@ class AnnealStats:
     levels_run: int = 0
     best_chain: int = -1
     engine_g: float = 0.0
+    engine_t: float = 0.0
     kernel_ms: float = 0.0
 
     @staticmethod
     def _from(s: SloAnnealStats) -> "AnnealStats":
         return AnnealStats(int(s.proposals), int(s.accepted), bool(s.shortcut), s.g_sorted_start, s.g_input_start,
-                           s.objective_scale_used, s.chains_run, s.levels_run, s.best_chain, s.engine_g, s.kernel_ms)
+                           s.objective_scale_used, s.chains_run, s.levels_run, s.best_chain, s.engine_g, s.engine_t,
+                           s.kernel_ms)
 
 
 @dataclass
