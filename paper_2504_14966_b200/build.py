@@ -66,7 +66,9 @@ def build(verbose=False, force=False, ptxas_info=False) -> str:
         objs.append(o)
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        log += _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread"], verbose)
+        # -Bsymbolic: the library's own C++ calls bind inside it even when a process also loads
+        # the reference's slosched:: symbols (the integration shim does exactly that)
+        log += _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-Xlinker", "-Bsymbolic"], verbose)
         os.replace(tmp, LIB)
     return log
 

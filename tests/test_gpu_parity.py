@@ -164,6 +164,24 @@ def test_replay_many_chains_in_one_launch(eng, port):
     assert res.chain == best
 
 
+def test_reference_binding_drop_in(ref):
+    """integration/reference_anneal_gpu.cpp compiled into the unmodified reference: the
+    reference's own anneal() types routed through the C ABI give the reference's result
+    (replay) and a dominant result (chains)."""
+    from oracle import refshim
+    if not refshim.available():
+        pytest.skip("oracle/_ref/libslosched_refshim.so not built")
+    for n, mb, seed in [(16, 2, 0), (64, 4, 3), (200, 8, 7)]:
+        fw = ref.generate_mixed(n, 50 + n, 1)
+        ids = list(fw.id)
+        want = ref.anneal(fw, TABLE_COEFFS, ids, mb, seed=seed, t0=200.0, iter=50)
+        got = refshim.anneal_gpu(fw, TABLE_COEFFS, ids, mb, seed=seed, mode=1, t0=200.0, iter=50)
+        assert got["batches"] == want["batches"] and got["g"] == want["g"] and got["n"] == want["n"]
+        assert (got["proposals"], got["accepted"]) == (want["proposals"], want["accepted"])
+        many = refshim.anneal_gpu(fw, TABLE_COEFFS, ids, mb, seed=seed, mode=0, chains=512, t0=200.0, iter=50)
+        assert many["g"] >= max(want["g_sorted_start"], want["g_input_start"])
+
+
 def test_schedule_all_replay_matches_golden():
     c = S.table_coefficients()
     for case in golden("schedule_all"):
