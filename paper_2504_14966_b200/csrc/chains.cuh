@@ -61,6 +61,25 @@ struct ChainParams {
     ChainRec* rec;
 };
 
+// The (exec, deadline) table: staged in shared memory (s = its 32-bit shared address) or read
+// from global memory (g). A compile-time choice, so the gather is an LDS.128 / LDG.128 rather
+// than a generic load.
+struct TabRef {
+    const double2* g;
+    uint32_t s;
+};
+
+template <bool SMEM>
+__device__ __forceinline__ double2 tab_ld(const TabRef& t, uint32_t i) {
+    if constexpr (SMEM) {
+        double2 v;
+        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(t.s + i * 16u));
+        return v;
+    } else {
+        return __ldg(t.g + i);
+    }
+}
+
 __device__ __forceinline__ double warp_sum(double v) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
@@ -79,18 +98,19 @@ __device__ __forceinline__ float key2f(uint32_t k) {
 // segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
 // and are at most mb long, so log2(mb) shuffle steps suffice
 __device__ __forceinline__ double seg_max(double e, uint32_t w, int lane, int mb) {
-    double m = fmax(e, 0.0);  // makespans start at 0 (reference P:src/priority_mapper.cpp:266)
+    double m = dmax(e, 0.0);  // makespans start at 0 (reference P:src/priority_mapper.cpp:266)
     int head = lane == 0 ? 1 : (int)((w >> (lane - 1)) & 1u);
     for (int d = 1; d < mb; d <<= 1) {
         const double mu = __shfl_up_sync(FULL, m, d);
         const int hu = __shfl_up_sync(FULL, head, d);
-        if (lane >= d && !head) m = fmax(m, mu), head = hu;
+        if (lane >= d && !head) m = dmax(m, mu), head = hu;
     }
     return m;
 }
 
 // cooperative summary of unit u (all 32 lanes; every lane receives the result)
-__device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n,
+template <bool SMEM>
+__device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint32_t* bits, const TabRef& tab, int n,
                                                 int mb, int u, int lane) {
     UnitSum s;
     const int q0 = u << 5;
@@ -98,7 +118,7 @@ __device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint3
     const uint32_t w = bits[u];
     double e = 0.0, D = kNegInf;
     if (lane < cnt) {
-        const double2 v = tab[ent[q0 + lane]];
+        const double2 v = tab_ld<SMEM>(tab, ent[q0 + lane]);
         e = v.x, D = v.y;
     }
     const double m = seg_max(e, w, lane, mb);
@@ -127,14 +147,15 @@ __device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint3
 
 // cooperative SLO count of unit u whose first position starts at elapsed E, the batch open at
 // the unit start having makespan fmk. Rare (live units whose inputs changed): kept out of line.
-__device__ __noinline__ int unit_met(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n, int mb,
-                                     int u, int lane, double E, double fmk) {
+template <bool SMEM>
+__device__ __noinline__ int unit_met(const uint16_t* ent, const uint32_t* bits, TabRef tab, int n, int mb, int u,
+                                     int lane, double E, double fmk) {
     const int q0 = u << 5;
     const int cnt = min(32, n - q0);
     const uint32_t w = bits[u];
     double e = 0.0, D = kNegInf;
     if (lane < cnt) {
-        const double2 v = tab[ent[q0 + lane]];
+        const double2 v = tab_ld<SMEM>(tab, ent[q0 + lane]);
         e = v.x, D = v.y;
     }
     const double m = seg_max(e, w, lane, mb);
@@ -243,10 +264,10 @@ __device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lan
                                               double (&fmk)[UPL]) {
     double rest = cs.s[0].inner;
 #pragma unroll
-    for (int k = 1; k < UPL; ++k) rest = rest + fmax(cs.s[k - 1].tm, cs.s[k].hm), rest = rest + cs.s[k].inner;
+    for (int k = 1; k < UPL; ++k) rest = rest + dmax(cs.s[k - 1].tm, cs.s[k].hm), rest = rest + cs.s[k].inner;
     double carry = __shfl_up_sync(FULL, cs.s[UPL - 1].tm, 1);
     if (lane == 0) carry = 0.0;
-    double S = cs.s[0].fe ? fmax(carry, cs.s[0].hm) + rest : 0.0;
+    double S = cs.s[0].fe ? dmax(carry, cs.s[0].hm) + rest : 0.0;
 #pragma unroll
     for (int d = 1; d < 32; d <<= 1) {  // sum scan of the makespans closed in each lane
         const double v = __shfl_up_sync(FULL, S, d);
@@ -259,7 +280,7 @@ __device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lan
     for (int k = 0; k < UPL; ++k) {
         const UnitSum& s = cs.s[k];
         E[k] = el;
-        fmk[k] = fmax(cm, s.hm);
+        fmk[k] = dmax(cm, s.hm);
         el = el + fmk[k], el = el + s.inner, cm = s.tm;
     }
 }
@@ -272,9 +293,9 @@ __device__ __forceinline__ double objective(int nm, double tot) {
 // Objective of the current state. full: re-summarise every unit and re-walk every live unit;
 // otherwise only units du0/du1 (-1 = none). Outputs the total latency, the SLO count and the
 // per-unit (E, fmk, walk result) to commit when the state is accepted.
-template <int UPL>
+template <int UPL, bool SMEM>
 __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16_t* ent, const uint32_t* bits,
-                                               const double2* tab, int n, int mb, int lane, bool full, int du0,
+                                               const TabRef& tab, int n, int mb, int lane, bool full, int du0,
                                                int du1, double& tot_out, int& nm_out, double (&E)[UPL],
                                                double (&fmk)[UPL], int (&nN)[UPL], unsigned long long& sc1,
                                                unsigned long long& sc2) {
@@ -283,7 +304,7 @@ __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16
     for (int i = 0; i < todo; ++i) {  // one inlined copy of the unit summary
         const int u = full ? i : (i == 0 ? du0 : du1);
         UnitSum v{0.0, 0.0, 0.0, 0.0, -INFINITY, 0, 0, 0};
-        if (u < U) v = unit_summary(ent, bits, tab, n, mb, u, lane), sc1 += lane == 0 ? 32 : 0;
+        if (u < U) v = unit_summary<SMEM>(ent, bits, tab, n, mb, u, lane), sc1 += lane == 0 ? 32 : 0;
         if (lane == u / UPL) {
 #pragma unroll
             for (int k = 0; k < UPL; ++k)
@@ -309,7 +330,7 @@ __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16
             mask &= mask - 1;
             const double Eu = __shfl_sync(FULL, E[k], ln);
             const double Fu = __shfl_sync(FULL, fmk[k], ln);
-            const int cntm = unit_met(ent, bits, tab, n, mb, ln * UPL + k, lane, Eu, Fu);
+            const int cntm = unit_met<SMEM>(ent, bits, tab, n, mb, ln * UPL + k, lane, Eu, Fu);
             if (lane == ln) nN[k] = cntm;
             sc2 += lane == 0 ? 32 : 0;
         }
@@ -349,7 +370,8 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     double tot, E[UPL], fmk[UPL];
     int nm, nN[UPL];
     unsigned long long sc1 = 0, sc2 = 0;
-    evaluate_chain<UPL>(cs, ent, bits, p.tab, p.n, p.mb, lane, true, -1, -1, tot, nm, E, fmk, nN, sc1, sc2);
+    const TabRef tab{p.tab, 0u};
+    evaluate_chain<UPL, false>(cs, ent, bits, tab, p.n, p.mb, lane, true, -1, -1, tot, nm, E, fmk, nN, sc1, sc2);
 #pragma unroll
     for (int k = 0; k < UPL; ++k) cs.wE[k] = E[k], cs.wF[k] = fmk[k], cs.wN[k] = nN[k];
     reinterpret_cast<ChainState<UPL>*>(const_cast<void*>(p.start_sum))[lane] = cs;
@@ -359,20 +381,20 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     }
 }
 
-template <int UPL>
+template <int UPL, bool SMEM>
 __global__ void __launch_bounds__(UPL == 1 ? 768 : 512, 1) k_chains(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = p.n, mb = p.mb;
 
-    const double2* tab = p.tab;
+    TabRef tab{p.tab, 0u};
     size_t off = 0;
-    if (p.smem_tab) {  // stage the (exec, deadline) table once per block: coalesced 16 B loads
+    if constexpr (SMEM) {  // stage the (exec, deadline) table once per block: coalesced 16 B loads
         double2* st = reinterpret_cast<double2*>(smem);
         const int total = mb * n;
         for (int i = threadIdx.x; i < total; i += blockDim.x) st[i] = p.tab[i];
         __syncthreads();
-        tab = st;
+        tab.s = (uint32_t)__cvta_generic_to_shared(st);
         off = ((size_t)total * sizeof(double2) + 15) & ~(size_t)15;
     }
     constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
@@ -494,7 +516,8 @@ __global__ void __launch_bounds__(UPL == 1 ? 768 : 512, 1) k_chains(const ChainP
                 }
                 double tot, E[UPL], fmk[UPL];
                 int nm, nN[UPL];
-                evaluate_chain<UPL>(cs, ent, bits, tab, n, mb, lane, false, du0, du1, tot, nm, E, fmk, nN, sc1, sc2);
+                evaluate_chain<UPL, SMEM>(cs, ent, bits, tab, n, mb, lane, false, du0, du1, tot, nm, E, fmk, nN, sc1,
+                                          sc2);
                 const double f_new = objective(nm, tot);
                 ++props;
                 bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)

@@ -638,6 +638,20 @@ int count_levels(double t0, double t_thres, double tau) {
     return L;
 }
 
+template <int UPL, bool SMEM>
+int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
+    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
+    W = std::max(1, std::min(W, c->chain_count));
+    c->smem = base + (size_t)W * slot;
+    CK(cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL, SMEM>, W * 32, c->smem));
+    if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
+    c->block = W * 32;
+    c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
+    return SLO_OK;
+}
+
 template <int UPL>
 int configure_chains(slo_ctx* c) {
     const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(double2);
@@ -645,35 +659,24 @@ int configure_chains(slo_ctx* c) {
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
     const int max_w = UPL == 1 ? 24 : 16;
     c->smem_tab = tab_smem + slot <= c->smem_optin;
-    const size_t base = c->smem_tab ? tab_smem : 0;
-    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
-    W = std::max(1, std::min(W, c->chain_count));
-    c->smem = base + (size_t)W * slot;
-    CK(cudaFuncSetAttribute(k_chains<UPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
-    int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL>, W * 32, c->smem));
-    if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
-    c->block = W * 32;
-    c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
-    return SLO_OK;
+    return c->smem_tab ? configure_chains_t<UPL, true>(c, tab_smem, slot, max_w)
+                       : configure_chains_t<UPL, false>(c, 0, slot, max_w);
+}
+
+template <int UPL>
+void launch_t(slo_ctx* c) {
+    const size_t ss = 1024 * (size_t)UPL * 2 + 32 * (size_t)UPL * 4;
+    k_start<UPL><<<1, 32, ss, c->stream>>>(c->kp);
+    if (c->smem_tab) k_chains<UPL, true><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+    else k_chains<UPL, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
 }
 
 // prologue (start-state summaries, one warp) then the chain kernel
 int launch_chains_U(slo_ctx* c) {
-    const size_t ss = 1024 * (size_t)c->UPL * 2 + 32 * (size_t)c->UPL * 4;
     switch (c->UPL) {
-        case 1:
-            k_start<1><<<1, 32, ss, c->stream>>>(c->kp);
-            k_chains<1><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
-            break;
-        case 2:
-            k_start<2><<<1, 32, ss, c->stream>>>(c->kp);
-            k_chains<2><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
-            break;
-        case 4:
-            k_start<4><<<1, 32, ss, c->stream>>>(c->kp);
-            k_chains<4><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
-            break;
+        case 1: launch_t<1>(c); break;
+        case 2: launch_t<2>(c); break;
+        case 4: launch_t<4>(c); break;
         default: return fail(SLO_ERR_CAPACITY, "bad units-per-lane");
     }
     CK(cudaGetLastError());
