@@ -193,6 +193,8 @@ struct EngineOptions {
     std::vector<double> scale_ladder;   // per-chain objective_scale multipliers (chain c uses [c % size])
     int device = -1;                    // -1: SLOSCHED_DEVICE env or 0
     int chain_begin = 0, chain_end = -1;  // slice of [0, chains) run by this call (multi-GPU sharding)
+    int max_blocks = 0;                 // > 0: cap the chain grid (concurrent launches share the GPU)
+    bool concurrent_instances = true;   // schedule_all: anneal the instances concurrently (Chains mode)
 };
 
 struct AnnealConfig {

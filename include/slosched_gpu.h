@@ -90,6 +90,7 @@ typedef struct {
     int64_t budget_ns;       /* 0 = run the whole ladder; else stop after this much device time */
     int32_t n_scale_mult;    /* optional per-chain scale ladder: chain c uses */
     const double* scale_mult;/*   objective_scale * scale_mult[c % n_scale_mult] */
+    int32_t max_blocks;      /* > 0: cap the chain grid (share the GPU with concurrent launches) */
 } slo_chain_params;
 
 typedef struct {

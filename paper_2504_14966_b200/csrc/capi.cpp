@@ -97,6 +97,7 @@ AnnealConfig config_of(const slosched_anneal_config* c) {
     a.engine.device = c->device;
     a.engine.chain_begin = c->chain_begin;
     a.engine.chain_end = c->chain_end;
+    a.engine.concurrent_instances = c->sequential_instances == 0;
     return a;
 }
 

@@ -649,6 +649,7 @@ int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
     c->block = W * 32;
     c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
+    if (c->prm.max_blocks > 0) c->grid = std::min(c->grid, c->prm.max_blocks);
     return SLO_OK;
 }
 

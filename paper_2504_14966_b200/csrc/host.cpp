@@ -12,6 +12,7 @@
 #include <memory>
 #include <mutex>
 #include <numeric>
+#include <thread>
 
 #include "slosched_b200.hpp"
 #include "slosched_gpu.h"
@@ -577,6 +578,7 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     prm.budget_ns = static_cast<int64_t>(eo.budget_ms * 1e6);
     prm.n_scale_mult = static_cast<int32_t>(eo.scale_ladder.size());
     prm.scale_mult = eo.scale_ladder.empty() ? nullptr : eo.scale_ladder.data();
+    prm.max_blocks = eo.max_blocks;
 
     const int device = resolve_device(eo.device);
     CtxPtr ctx = CtxPool::get().acquire(device);
@@ -682,12 +684,44 @@ ScheduleAllResult schedule_all(const Workload& w, const std::vector<InstanceStat
     res.per_instance.resize(k);
     res.stats.resize(k);
     res.queues.resize(k);
+    // Per-instance anneals are independent (disjoint request sets, own derived seeds; the
+    // reference runs them one after another, P:src/scheduler.cpp:109-123, SPEC:377-378 allows
+    // concurrency). In Chains mode each instance gets its own host thread, engine context and
+    // stream, and a 1/k share of the SMs, so the k launches run side by side on the GPU.
+    std::vector<AnnealConfig> per(k, cfg);
+    const bool concurrent = k > 1 && cfg.engine.mode == SearchMode::Chains && cfg.engine.concurrent_instances;
+    if (concurrent && cfg.engine.max_blocks <= 0) {
+        const int device = resolve_device(cfg.engine.device);
+        CtxPtr ctx = CtxPool::get().acquire(device);
+        const int sms = slo_ctx_sm_count(ctx.get());
+        CtxPool::get().release(device, std::move(ctx));
+        for (auto& p : per) p.engine.max_blocks = std::max(1, sms / static_cast<int>(k));
+    }
+    for (std::size_t i = 0; i < k; ++i) per[i].seed = Rng::derive(cfg.seed, static_cast<std::uint64_t>(instances[i].id));
+    std::vector<AnnealResult> out(k);
+    auto run_one = [&](std::size_t i) {
+        out[i] = anneal(w, res.assignment.per_instance[i], c, per[i], instances[i].max_batch_size);
+    };
+    if (concurrent) {
+        std::vector<std::exception_ptr> errs(k);
+        std::vector<std::thread> pool;
+        for (std::size_t i = 0; i < k; ++i)
+            pool.emplace_back([&, i] {
+                try {
+                    run_one(i);
+                } catch (...) {
+                    errs[i] = std::current_exception();
+                }
+            });
+        for (auto& t : pool) t.join();
+        for (auto& e : errs)
+            if (e) std::rethrow_exception(e);
+    } else {
+        for (std::size_t i = 0; i < k; ++i) run_one(i);
+    }
     for (std::size_t i = 0; i < k; ++i) {
-        AnnealConfig per = cfg;
-        per.seed = Rng::derive(cfg.seed, static_cast<std::uint64_t>(instances[i].id));
-        AnnealResult ar = anneal(w, res.assignment.per_instance[i], c, per, instances[i].max_batch_size);
-        res.per_instance[i] = std::move(ar.best);
-        res.stats[i] = ar.stats;
+        res.per_instance[i] = std::move(out[i].best);
+        res.stats[i] = out[i].stats;
         for (const auto& b : res.per_instance[i].schedule.batches) res.queues[i].pending.push_back(b);
     }
     res.overhead_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();

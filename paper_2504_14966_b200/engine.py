@@ -90,12 +90,13 @@ class Engine:
         return n_met, t, g
 
     def _params(self, t0=500.0, t_thres=20.0, iter=100, tau=0.95, seed=0, objective_scale=1.0, replay=False,
-                chains=1, chain_begin=0, chain_end=None, budget_ms=0.0, scale_ladder=()):
+                chains=1, chain_begin=0, chain_end=None, budget_ms=0.0, scale_ladder=(), max_blocks=0):
         ladder = _f64(list(scale_ladder)) if len(scale_ladder) else None
         prm = SloChainParams(t0, t_thres, iter, tau, seed & (2**64 - 1), objective_scale,
                              _lib.SLO_RNG_XOSHIRO_REPLAY if replay else _lib.SLO_RNG_PHILOX, chains, chain_begin,
                              chains if chain_end is None else chain_end, int(budget_ms * 1e6),
-                             0 if ladder is None else len(ladder), None if ladder is None else _p(ladder, c_double))
+                             0 if ladder is None else len(ladder), None if ladder is None else _p(ladder, c_double),
+                             max_blocks)
         return prm, ladder
 
     def prepare(self, start_perm, start_sizes, **kw):

@@ -194,6 +194,23 @@ def test_schedule_all_replay_matches_golden():
             assert got.n == want["n_met"] and got.g == unhex(want["g"])
 
 
+def test_schedule_all_concurrent_instances_equal_sequential():
+    """Chains mode: the k per-instance anneals run concurrently (own thread, context, stream and
+    1/k of the SMs); chain results do not depend on the grid, so the schedules are identical to
+    one-after-another runs, and every instance result dominates its starts."""
+    c = S.table_coefficients()
+    w = _three_class(160, 12)
+    insts = [S.InstanceState(i, 2**35, 2**35, 0.9, 262144.0, 4) for i in range(4)]
+    base = dict(seed=5, chains=1024, t0=100.0, iter=30, scale_ladder=(1.0, 100.0, 1e4))
+    conc = S.schedule_all(w, insts, c, S.AnnealConfig(**base))
+    seq = S.schedule_all(w, insts, c, S.AnnealConfig(**base, sequential_instances=True))
+    assert conc.epochs == seq.epochs
+    for a, b in zip(conc.per_instance, seq.per_instance):
+        assert a.schedule.batches == b.schedule.batches and a.g == b.g
+    ids = sorted(i for ev in conc.per_instance for i in ev.schedule.flatten())
+    assert ids == sorted(w.ids())
+
+
 # ---------------------------------------------------------------- K3/K4 chains
 @pytest.mark.parametrize("n,mb,chains", [(2, 2, 8), (9, 3, 64), (64, 4, 512), (256, 4, 1024), (1024, 4, 256),
                                          (200, 16, 128), (4096, 4, 32)])
