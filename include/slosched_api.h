@@ -81,6 +81,11 @@ int slosched_anneal(const slosched_workload* w, const double* coeffs8, const int
                     const slosched_anneal_config* cfg, int32_t max_batch, int32_t* out_ids, int32_t* out_sizes,
                     int32_t* out_nb, int32_t* n_met, double* t, double* g, slosched_anneal_stats* stats);
 
+/* exhaustive() (P:include/slosched/priority_mapper.hpp:74-82): the GPU small-n oracle. */
+int slosched_exhaustive(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
+                        int32_t max_batch, int32_t n_cap, int32_t* out_ids, int32_t* out_sizes, int32_t* out_nb,
+                        int32_t* n_met, double* t, double* g, uint64_t* evaluated);
+
 /* Instances as arrays; per-instance outputs concatenated in instance order. */
 int slosched_schedule_all(const slosched_workload* w, const double* coeffs8, int32_t n_inst, const int32_t* inst_id,
                           const double* total_mem, const double* remaining_mem, const double* mu, const double* sigma,

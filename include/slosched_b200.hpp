@@ -237,6 +237,17 @@ Schedule neighbor(const Schedule& schedule, Rng& rng, int max_batch);
 AnnealResult anneal(const Workload&, const std::vector<int>& request_ids, const LatencyCoefficients&,
                     const AnnealConfig&, int max_batch);
 
+struct ExhaustiveResult {
+    EvaluatedSchedule best;
+    std::uint64_t schedules_evaluated = 0;
+};
+
+// Small-n oracle on the GPU: every permutation x every ordered batch-size composition with
+// parts <= max_batch; ties broken by lower t, then lexicographic request order, then batch-size
+// sequence (P:include/slosched/priority_mapper.hpp:74-82). CapacityError when n > n_cap.
+ExhaustiveResult exhaustive(const Workload& workload, const std::vector<int>& request_ids,
+                            const LatencyCoefficients& coeffs, int max_batch, int n_cap = 10);
+
 // Largest d with fl(d + c) <= s (the deadline convention of include/slosched_gpu.h).
 double latest_start(double s, double c);
 

@@ -123,6 +123,14 @@ int slo_chains_launch(slo_ctx* ctx);
 int slo_chains_fetch(slo_ctx* ctx, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
                      slo_chain_result* result);
 
+/* Exhaustive search of the current problem: every permutation x every ordered batch-size
+ * composition with parts <= mb, one candidate stream per thread, best by the reference's order
+ * (G desc, t asc, flattened ids, composition) -- P:src/priority_mapper.cpp:440-517. Fails with
+ * SLO_ERR_CAPACITY when n > n_cap (reference message) or n > 16. Outputs the winner in dense
+ * indices, its G and t, and the number of schedules evaluated (n! x compositions). */
+int slo_exhaustive(slo_ctx* ctx, int32_t n_cap, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
+                   double* g, double* t, uint64_t* evaluated);
+
 /* Achievable shared-memory bandwidth of the device (GB/s): conflict-free 16-byte loads on
  * every SM -- the roofline denominator of the smem-bound chain kernel. */
 int slo_probe_smem_bandwidth(slo_ctx* ctx, double* gbytes_per_s);

@@ -88,6 +88,9 @@ _SIGNATURES = [
     ("slosched_schedule_all", c_int32, [POINTER(SloWorkload), _D, c_int32, _I, _D, _D, _D, _D, _I,
                                         POINTER(SloAnnealConfig), _I, _I, _I, _I, _I, _D, _D, _I, _D]),
     ("slosched_build_tables", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, c_int32, _D, _D]),
+    ("slosched_exhaustive", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, c_int32, c_int32, _I, _I, _I, _I, _D,
+                                      _D, POINTER(c_uint64)]),
+    ("slo_exhaustive", c_int32, [c_void_p, c_int32, _I, _I, _I, _D, _D, POINTER(c_uint64)]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

@@ -251,6 +251,20 @@ int slosched_schedule_all(const slosched_workload* w, const double* c, int32_t n
     });
 }
 
+int slosched_exhaustive(const slosched_workload* w, const double* c, const int32_t* ids, int32_t n, int32_t max_batch,
+                        int32_t n_cap, int32_t* out_ids, int32_t* out_sizes, int32_t* out_nb, int32_t* n_met,
+                        double* t, double* g, uint64_t* evaluated) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        const ExhaustiveResult r = exhaustive(wl, std::vector<int>(ids, ids + n), coeffs_of(c), max_batch, n_cap);
+        *out_nb = emit(r.best.schedule, out_ids, out_sizes);
+        *n_met = r.best.n;
+        *t = r.best.t_ms;
+        *g = r.best.g;
+        *evaluated = r.schedules_evaluated;
+    });
+}
+
 int slosched_build_tables(const slosched_workload* w, const double* c, const int32_t* ids, int32_t n,
                           int32_t max_batch, double* exec, double* deadline) {
     return guarded([&] {

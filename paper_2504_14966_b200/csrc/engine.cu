@@ -366,6 +366,9 @@ __global__ void k_replay(const ReplayParams p) {
 // ================================================================ K3: chains
 #include "chains.cuh"
 
+// ================================================================ exhaustive oracle
+#include "exhaustive.cuh"
+
 // ================================================================ K4: argmax
 __device__ __forceinline__ bool better(double g, double t, int c, double bg, double bt, int bc) {
     if (g != bg) return g > bg;
@@ -643,7 +646,9 @@ int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
     int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
     W = std::max(1, std::min(W, c->chain_count));
     c->smem = base + (size_t)W * slot;
-    CK(cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem));
+    // the attribute is per function (process-wide): always raise it to the device maximum so
+    // concurrent contexts launching different smem sizes never race on it
+    CK(cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_optin));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL, SMEM>, W * 32, c->smem));
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
@@ -885,6 +890,79 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
         out->positions_pass1 = r.scan1;
         out->positions_pass2 = r.scan2;
     }
+    return SLO_OK;
+}
+
+int slo_exhaustive(slo_ctx* c, int32_t n_cap, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
+                   double* g, double* t, uint64_t* evaluated) {
+    if (!c) return fail(SLO_ERR_ARG, "slo_exhaustive: null context");
+    if (c->n == 0) return fail(SLO_ERR_STATE, "slo_exhaustive: no problem set");
+    const int n = c->n, mb = c->mb;
+    if (n > n_cap)
+        return fail(SLO_ERR_CAPACITY, "exhaustive: " + std::to_string(n) + " requests exceed cap of " +
+                                          std::to_string(n_cap) + " (search space is O(N! * 2^N))");
+    if (n > kExMaxN) return fail(SLO_ERR_CAPACITY, "exhaustive: the engine enumerates at most 16 requests");
+    // ordered compositions of n with parts <= mb, lexicographic (P:src/priority_mapper.cpp:416-436)
+    std::vector<uint8_t> comps, lens;
+    std::vector<uint8_t> cur;
+    auto rec = [&](auto&& self, int remaining) -> void {
+        if (remaining == 0) {
+            std::vector<uint8_t> row(kExMaxN, 0);
+            std::copy(cur.begin(), cur.end(), row.begin());
+            comps.insert(comps.end(), row.begin(), row.end());
+            lens.push_back((uint8_t)cur.size());
+            return;
+        }
+        for (int part = 1; part <= std::min(remaining, mb); ++part) {
+            cur.push_back((uint8_t)part);
+            self(self, remaining - part);
+            cur.pop_back();
+        }
+    };
+    rec(rec, n);
+    const int n_comps = (int)lens.size();
+    unsigned long long nfact = 1;
+    for (int i = 2; i <= n; ++i) nfact *= (unsigned long long)i;
+    const unsigned long long target = (unsigned long long)c->sm_count * 2048ull * 4ull;
+    const unsigned long long total = nfact * (unsigned long long)n_comps;
+    const unsigned long long chunk = std::max<unsigned long long>(1ull, (total + target - 1) / target);
+    const unsigned long long cpc = (nfact + chunk - 1) / chunk;
+    const unsigned long long items = cpc * (unsigned long long)n_comps;
+    const unsigned long long blocks = (items + 255) / 256;
+    if (blocks > 0x7fffffffull) return fail(SLO_ERR_CAPACITY, "exhaustive: search space too large");
+    CK(cudaSetDevice(c->device));
+    DevBuf d_comps, d_lens, d_best, d_out;
+    CK(d_comps.reserve(comps.size()));
+    CK(d_lens.reserve(lens.size()));
+    CK(d_best.reserve(blocks * sizeof(ExKey)));
+    CK(d_out.reserve(sizeof(ExKey)));
+    CK(cudaMemcpyAsync(d_comps.p, comps.data(), comps.size(), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(d_lens.p, lens.data(), lens.size(), cudaMemcpyHostToDevice, c->stream));
+    k_exhaustive<<<(unsigned)blocks, 256, 0, c->stream>>>(n, c->tab.as<double2>(), n_comps, d_comps.as<uint8_t>(),
+                                                           d_lens.as<uint8_t>(), nfact, chunk, cpc, d_best.as<ExKey>());
+    CK(cudaGetLastError());
+    k_exhaustive_reduce<<<1, 1024, 0, c->stream>>>((int)blocks, d_best.as<ExKey>(), d_out.as<ExKey>());
+    CK(cudaGetLastError());
+    ExKey best;
+    CK(cudaMemcpyAsync(&best, d_out.p, sizeof best, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!best.valid) return fail(SLO_ERR_STATE, "slo_exhaustive: no candidate evaluated");
+    // unrank the winning permutation (lexicographic order over dense indices)
+    std::vector<int> avail(n);
+    for (int i = 0; i < n; ++i) avail[i] = i;
+    unsigned long long r = best.prank, f = nfact;
+    for (int i = 0; i < n; ++i) {
+        f /= (unsigned long long)(n - i);
+        const int d = (int)(r / f);
+        r -= (unsigned long long)d * f;
+        best_perm[i] = avail[d];
+        avail.erase(avail.begin() + d);
+    }
+    *best_nb = lens[best.comp];
+    for (int k = 0; k < lens[best.comp]; ++k) best_sizes[k] = comps[(size_t)best.comp * kExMaxN + k];
+    *g = best.g;
+    *t = best.t;
+    *evaluated = total;
     return SLO_OK;
 }
 

@@ -614,6 +614,44 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     return res;
 }
 
+ExhaustiveResult exhaustive(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
+                            int max_batch, int n_cap) {
+    const int n = static_cast<int>(ids.size());
+    if (n > n_cap)
+        throw CapacityError("exhaustive: " + std::to_string(n) + " requests exceed cap of " + std::to_string(n_cap) +
+                            " (search space is O(N! * 2^N))");
+    if (max_batch < 1) throw DataError("exhaustive: max_batch must be >= 1");
+    ExhaustiveResult res;
+    if (n == 0) {  // the single (empty) schedule
+        res.best = evaluate(Schedule{}, c, w);
+        res.schedules_evaluated = 1;
+        return res;
+    }
+    std::vector<int> sorted_ids = ids;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    std::vector<double> exec, deadline;
+    const int mb = std::min(max_batch, n);  // compositions never use parts above n
+    cost_tables(w, ids, c, mb, exec, deadline);
+    const int device = resolve_device(-1);
+    CtxPtr ctx = CtxPool::get().acquire(device);
+    std::vector<int> perm(n), sizes(n);
+    int nb = 0;
+    double g = 0.0, t = 0.0;
+    std::uint64_t evaluated = 0;
+    engine_check(slo_problem_set(ctx.get(), n, mb, exec.data(), deadline.data()));
+    engine_check(slo_exhaustive(ctx.get(), n_cap, perm.data(), sizes.data(), &nb, &g, &t, &evaluated));
+    CtxPool::get().release(device, std::move(ctx));
+    Schedule best;
+    for (int k = 0, pos = 0; k < nb; ++k) {
+        Batch b;
+        for (int j = 0; j < sizes[k]; ++j) b.push_back(sorted_ids[perm[pos++]]);
+        best.batches.push_back(std::move(b));
+    }
+    res.best = evaluate(best, c, w);
+    res.schedules_evaluated = evaluated;
+    return res;
+}
+
 // ================================================================ scheduler (P:src/scheduler.cpp)
 long long token_capacity(std::uint64_t remaining, double mu, double sigma) {
     if (!(sigma > 0.0)) throw std::invalid_argument("token_capacity: sigma must be > 0");
@@ -673,10 +711,8 @@ std::optional<Batch> dispatch(InstanceQueue& q, bool ready) {
 
 ScheduleAllResult schedule_all(const Workload& w, const std::vector<InstanceState>& instances,
                                const LatencyCoefficients& c, const AnnealConfig& cfg, Policy policy,
-                               int /*exhaustive_cap*/) {
+                               int exhaustive_cap) {
     if (policy == Policy::FCFS) throw std::invalid_argument("schedule_all: FCFS is a simulator baseline, not a mapper policy");
-    if (policy == Policy::EXHAUSTIVE)
-        throw std::invalid_argument("schedule_all: the exhaustive oracle is not part of the B200 engine (see DESIGN.md)");
     const auto t_start = std::chrono::steady_clock::now();
     ScheduleAllResult res;
     res.assignment = assign_instances(w, instances, c);
@@ -700,7 +736,11 @@ ScheduleAllResult schedule_all(const Workload& w, const std::vector<InstanceStat
     for (std::size_t i = 0; i < k; ++i) per[i].seed = Rng::derive(cfg.seed, static_cast<std::uint64_t>(instances[i].id));
     std::vector<AnnealResult> out(k);
     auto run_one = [&](std::size_t i) {
-        out[i] = anneal(w, res.assignment.per_instance[i], c, per[i], instances[i].max_batch_size);
+        if (policy == Policy::EXHAUSTIVE)  // P:src/scheduler.cpp:118-120: no stats for the oracle
+            out[i].best = exhaustive(w, res.assignment.per_instance[i], c, instances[i].max_batch_size,
+                                     exhaustive_cap).best;
+        else
+            out[i] = anneal(w, res.assignment.per_instance[i], c, per[i], instances[i].max_batch_size);
     };
     if (concurrent) {
         std::vector<std::exception_ptr> errs(k);

@@ -410,6 +410,26 @@ def anneal_flat(workload: Workload, request_ids, coeffs: LatencyCoefficients, co
     return oi[:n], osz[:nb.value], n_met.value, t.value, g.value, AnnealStats._from(st)
 
 
+@dataclass
+class ExhaustiveResult:
+    best: EvaluatedSchedule
+    schedules_evaluated: int
+
+
+def exhaustive(workload: Workload, request_ids, coeffs: LatencyCoefficients, max_batch: int,
+               n_cap: int = 10) -> ExhaustiveResult:
+    """Small-n oracle on the GPU (P:src/priority_mapper.cpp:440-517): every permutation x every
+    batch-size composition, the reference's tie-breaking; CapacityError beyond n_cap."""
+    ids = _i32(request_ids)
+    n = len(ids)
+    oi, osz = np.zeros(max(n, 1), dtype=np.int32), np.zeros(max(n, 1), dtype=np.int32)
+    nb, n_met, t, g, ev = c_int32(), c_int32(), c_double(), c_double(), ctypes.c_uint64()
+    _check_api(lib().slosched_exhaustive(byref(workload._view), _p(coeffs.as_array(), c_double), _p(ids), n,
+                                         max_batch, n_cap, _p(oi), _p(osz), byref(nb), byref(n_met), byref(t),
+                                         byref(g), byref(ev)))
+    return ExhaustiveResult(_evaluated_from_flat(workload, coeffs, oi, osz, nb.value), int(ev.value))
+
+
 # ------------------------------------------------------------------ scheduler
 @dataclass
 class InstanceState:
