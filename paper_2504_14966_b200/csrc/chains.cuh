@@ -448,7 +448,8 @@ __global__ void __launch_bounds__(UPL == 1 ? 768 : 512, 1) k_chains(const ChainP
 
             for (int it = 0; it < p.iter; ++it) {
                 const uint32_t prop = (uint32_t)(lev * p.iter + it);
-                if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..3 and acceptance
+                if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..5 and acceptance
+                    __syncwarp();      // every lane is done reading the previous block
                     uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
                     uint32_t w[kRndWords];
 #pragma unroll
