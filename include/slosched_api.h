@@ -48,6 +48,7 @@ typedef struct {
     int32_t device;         /* -1 = SLOSCHED_DEVICE or 0 */
     int32_t chain_begin, chain_end; /* chain_end < 0: all chains */
     int32_t sequential_instances;   /* schedule_all: 1 = one instance after another (default concurrent) */
+    int32_t max_blocks;             /* > 0: cap the chain grid (concurrent callers share the GPU) */
 } slosched_anneal_config;
 
 typedef struct {

@@ -29,7 +29,7 @@ class SloAnnealConfig(Structure):
                 ("has_objective_scale", c_int32), ("objective_scale", c_double), ("mode", c_int32),
                 ("chains", c_int32), ("budget_ms", c_double), ("n_scale_ladder", c_int32),
                 ("scale_ladder", POINTER(c_double)), ("device", c_int32), ("chain_begin", c_int32),
-                ("chain_end", c_int32), ("sequential_instances", c_int32)]
+                ("chain_end", c_int32), ("sequential_instances", c_int32), ("max_blocks", c_int32)]
 
 
 class SloAnnealStats(Structure):

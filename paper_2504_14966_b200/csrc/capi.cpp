@@ -98,6 +98,7 @@ AnnealConfig config_of(const slosched_anneal_config* c) {
     a.engine.chain_begin = c->chain_begin;
     a.engine.chain_end = c->chain_end;
     a.engine.concurrent_instances = c->sequential_instances == 0;
+    a.engine.max_blocks = c->max_blocks;
     return a;
 }
 

@@ -641,14 +641,26 @@ int count_levels(double t0, double t_thres, double tau) {
     return L;
 }
 
+// The max-dynamic-smem attribute is per function and device (process-wide). Raise it to the
+// device maximum once: concurrent contexts then never race on it, and no call blocks behind a
+// running instance of the kernel (setting it while the kernel runs serialises the callers).
+template <int UPL, bool SMEM>
+cudaError_t ensure_smem_attr(int device, int bytes) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
+    const cudaError_t e = cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
+    return e;
+}
+
 template <int UPL, bool SMEM>
 int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
     int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
     W = std::max(1, std::min(W, c->chain_count));
     c->smem = base + (size_t)W * slot;
-    // the attribute is per function (process-wide): always raise it to the device maximum so
-    // concurrent contexts launching different smem sizes never race on it
-    CK(cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_optin));
+    CK((ensure_smem_attr<UPL, SMEM>(c->device, (int)c->smem_optin)));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL, SMEM>, W * 32, c->smem));
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");

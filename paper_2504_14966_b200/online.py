@@ -1,0 +1,222 @@
+"""Online rolling-window rescheduling over a Poisson request stream (BASELINE configs[4]).
+
+The reference has no online mode (it schedules in synchronous waves); this driver
+is the §8(f) row 2 extension, built on the public entry points:
+
+* stream    -- request lengths from the reference's synthetic generator (generate_mixed, with
+              estimator-predicted output lengths), Poisson arrivals at a stated rate;
+* instances -- k serving instances (one per GPU in production; here they share the visible
+              GPUs), requests assigned on arrival to the least-loaded instance;
+* windows   -- every window_ms of simulated time each instance's queue (arrived, not yet
+              started) is re-planned with anneal() under a per-window device budget; the plan's
+              batches are dispatched until the next window boundary, the rest is re-planned;
+* planning  -- the objective sees each request's remaining slack: its SLO minus the time it has
+              already waited (a per-request SLO class), exactly the reference objective otherwise;
+* execution -- realized times from the latency model with the TRUE output lengths plus the
+              reference simulator's 0.1 ms dispatch gap (P:src/simulator.cpp:49-74, noise 0).
+
+Policies: "sa" (GPU chains), "fcfs" (arrival order, greedy batches -- the reference's FCFS
+baseline, P:src/simulator.cpp:76-123).
+"""
+from __future__ import annotations
+
+import time
+from concurrent.futures import ThreadPoolExecutor
+from dataclasses import dataclass, field
+from typing import Dict, List, Optional
+
+import numpy as np
+
+from .slosched import (AnnealConfig, LatencyCoefficients, Request, SloKind, SloSpec, TaskClass, Workload,
+                       anneal_flat, generate_mixed, table_coefficients)
+
+_IMPOSSIBLE_MS = 1e-9  # an SLO whose slack is already gone: positive (valid) but unreachable
+
+
+def _coeffs(c: LatencyCoefficients):
+    return (c.alpha_p, c.beta_p, c.gamma_p, c.delta_p, c.alpha_d, c.beta_d, c.gamma_d, c.delta_d)
+
+
+def prefill_ms(c, b, li):
+    ap, bp, gp, dp = _coeffs(c)[:4]
+    return ap * b * li + bp * b + gp * li + dp
+
+
+def decode_total_ms(c, b, li, lo):
+    ad, bd, gd, dd = _coeffs(c)[4:]
+    return (ad * b + gd) * (lo * li + lo * (lo + 1.0) / 2.0) + lo * (bd * b + dd)
+
+
+@dataclass
+class Stream:
+    arrival_ms: np.ndarray
+    cls: np.ndarray          # 0 = code (E2E 30 s), 1 = chat (TTFT 10 s + TPOT 50 ms)
+    input_len: np.ndarray
+    true_out: np.ndarray
+    pred_out: np.ndarray
+    rate_per_s: float
+
+    @property
+    def n(self):
+        return len(self.arrival_ms)
+
+
+def service_rate_per_s(coeffs=None, max_batch=4, samples=4096, seed=7):
+    """Requests/s one instance completes when always busy with full batches: max_batch over the
+    mean makespan of random batches drawn from the synthetic length distribution."""
+    c = coeffs or table_coefficients()
+    w = generate_mixed(samples, seed)
+    li = w.arrays["in_len"].astype(np.float64)
+    lo = w.arrays["true_out"].astype(np.float64)
+    ex = prefill_ms(c, max_batch, li) + decode_total_ms(c, max_batch, li, lo)
+    ex = ex[: (samples // max_batch) * max_batch].reshape(-1, max_batch)
+    return max_batch / (ex.max(axis=1).mean() / 1000.0)
+
+
+def make_stream(n: int, rate_per_s: float, seed: int = 0) -> Stream:
+    w = generate_mixed(n, seed)  # reference synthetic lengths + estimator predictions
+    a = w.arrays
+    rs = np.random.default_rng(seed + 1)
+    arrivals = np.cumsum(rs.exponential(1000.0 / rate_per_s, size=n))
+    return Stream(arrivals, a["cls"].copy(), a["in_len"].copy(), a["true_out"].copy(), a["pred_out"].copy(),
+                  rate_per_s)
+
+
+@dataclass
+class OnlineResult:
+    policy: str
+    n: int
+    n_met: int
+    total_latency_ms: float
+    windows: int
+    decisions: int
+    proposals: int
+    overhead_ms: List[float] = field(default_factory=list)
+
+    def summary(self) -> Dict:
+        ov = np.asarray(self.overhead_ms) if self.overhead_ms else np.zeros(1)
+        return {"policy": self.policy, "requests": self.n, "attainment": self.n_met / self.n,
+                "avg_latency_ms": self.total_latency_ms / self.n,
+                "g_req_per_ms": self.n_met / self.total_latency_ms if self.total_latency_ms > 0 else 0.0,
+                "windows": self.windows, "decisions": self.decisions, "proposals": self.proposals,
+                "overhead_ms_mean": float(ov.mean()), "overhead_ms_p99": float(np.percentile(ov, 99)),
+                "overhead_ms_max": float(ov.max())}
+
+
+def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
+    """Plan one instance's queue with the GPU annealer; SLOs shrunk by the time already waited."""
+    classes, reqs = [], []
+    for k, i in enumerate(ids):
+        waited = start_ms - stream.arrival_ms[i]
+        if stream.cls[i] == 0:
+            slo = SloSpec.e2e(max(30000.0 - waited, _IMPOSSIBLE_MS))
+        else:
+            slo = SloSpec.ttft_tpot(max(10000.0 - waited, _IMPOSSIBLE_MS), 50.0)
+        classes.append(TaskClass(k, f"r{i}", slo))
+        reqs.append(Request(int(i), k, int(stream.input_len[i]), int(stream.true_out[i]), int(stream.pred_out[i]),
+                            float(stream.arrival_ms[i])))
+    w = Workload(reqs, classes)
+    seq, sizes, _, _, _, st = anneal_flat(w, [int(i) for i in ids], coeffs, cfg, max_batch)
+    out, pos = [], 0
+    for s in sizes:
+        out.append([int(x) for x in seq[pos:pos + s]])
+        pos += int(s)
+    return out, st.proposals
+
+
+def _plan_fcfs(stream, ids, max_batch):
+    order = sorted(ids, key=lambda i: (stream.arrival_ms[i], i))
+    return [order[k:k + max_batch] for k in range(0, len(order), max_batch)], 0
+
+
+def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_ms: float = 5000.0,
+               max_batch: int = 4, budget_ms: float = 10.0, chains: int = 4096, seed: int = 0,
+               coeffs: Optional[LatencyCoefficients] = None, dispatch_gap_ms: float = 0.1,
+               max_windows: Optional[int] = None, scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4, 1e5),
+               t0: float = 500.0, tau: float = 0.7, iter: int = 30) -> OnlineResult:
+    c = coeffs or table_coefficients()
+    n = stream.n
+    queue: List[List[int]] = [[] for _ in range(n_instances)]
+    busy_until = np.zeros(n_instances)
+    load = np.zeros(n_instances)     # outstanding predicted work per instance (assignment key)
+    next_arrival = 0
+    done = 0
+    n_met, total_lat, proposals, decisions = 0, 0.0, 0, 0
+    overhead: List[float] = []
+    share = 0
+    if policy == "sa":
+        import ctypes
+        from ._lib import lib
+        ctx = ctypes.c_void_p()
+        if lib().slo_ctx_create(0, ctypes.byref(ctx)) == 0:
+            share = max(1, int(lib().slo_ctx_sm_count(ctx)) // n_instances)
+            lib().slo_ctx_destroy(ctx)
+    pool = ThreadPoolExecutor(n_instances) if policy == "sa" else None
+    t_win = 0.0
+    windows = 0
+    while done < n and (max_windows is None or windows < max_windows):
+        t_next = t_win + window_ms
+        # arrivals up to this window start join the least-loaded instance
+        while next_arrival < n and stream.arrival_ms[next_arrival] <= t_win:
+            i = next_arrival
+            inst = int(np.argmin(np.maximum(busy_until, t_win) + load))
+            queue[inst].append(i)
+            load[inst] += prefill_ms(c, 1, stream.input_len[i]) + decode_total_ms(c, 1, stream.input_len[i],
+                                                                                  stream.pred_out[i])
+            next_arrival += 1
+        if not any(queue) and next_arrival < n:  # idle: jump to the first window holding an arrival
+            t_win = max(t_win, np.ceil(stream.arrival_ms[next_arrival] / window_ms) * window_ms)
+            continue
+        windows += 1
+        # plan every non-empty instance queue (concurrently, one engine context each)
+        active = [k for k in range(n_instances) if queue[k]]
+        t0_wall = time.perf_counter()
+        if policy == "sa":
+            kernel_budget = max(0.5, budget_ms - 0.7)  # headroom for host setup + copies per window
+
+            def plan(k):
+                cfg = AnnealConfig(t0=t0, tau=tau, iter=iter, seed=seed * 1_000_003 + windows * 131 + k,
+                                   chains=chains, budget_ms=kernel_budget, scale_ladder=scale_ladder,
+                                   max_blocks=share)
+                return _plan_sa(stream, queue[k], max(busy_until[k], t_win), c, max_batch, cfg)
+            plans = dict(zip(active, pool.map(plan, active)))
+        else:
+            plans = {k: _plan_fcfs(stream, queue[k], max_batch) for k in active}
+        overhead.append((time.perf_counter() - t0_wall) * 1e3)
+        decisions += len(active)
+        # execute each plan until the next window boundary
+        for k, (batches, props) in plans.items():
+            proposals += props
+            t = max(busy_until[k], t_win)
+            started = []
+            for b in batches:
+                if t >= t_next:
+                    break
+                start = t + dispatch_gap_ms
+                bs = len(b)
+                li = stream.input_len[b].astype(np.float64)
+                lo = stream.true_out[b].astype(np.float64)
+                pf = prefill_ms(c, bs, li)
+                dec = decode_total_ms(c, bs, li, lo)
+                ex = pf + dec
+                for j, i in enumerate(b):
+                    e2e = start + ex[j] - stream.arrival_ms[i]
+                    if stream.cls[i] == 0:
+                        ok = e2e <= 30000.0
+                    else:
+                        ok = (start + pf[j] - stream.arrival_ms[i] <= 10000.0) and (dec[j] / lo[j] <= 50.0)
+                    n_met += int(ok)
+                    total_lat += e2e
+                    load[k] -= prefill_ms(c, 1, stream.input_len[i]) + decode_total_ms(
+                        c, 1, stream.input_len[i], stream.pred_out[i])
+                started.extend(b)
+                t = start + ex.max()
+            busy_until[k] = t
+            if started:
+                s = set(started)
+                queue[k] = [i for i in queue[k] if i not in s]
+                done += len(started)
+        t_win = t_next
+    if pool:
+        pool.shutdown()
+    return OnlineResult(policy, done, n_met, total_lat, windows, decisions, proposals, overhead)

@@ -308,6 +308,7 @@ class AnnealConfig:
     chain_begin: int = 0
     chain_end: int = -1
     sequential_instances: bool = False  # schedule_all: anneal instances one after another
+    max_blocks: int = 0                 # > 0: cap the chain grid (concurrent callers share the GPU)
 
     def _c(self):
         ladder = _f64(list(self.scale_ladder)) if len(self.scale_ladder) else None
@@ -316,7 +317,7 @@ class AnnealConfig:
                               0.0 if self.objective_scale is None else self.objective_scale, int(self.mode),
                               self.chains, self.budget_ms, 0 if ladder is None else len(ladder),
                               None if ladder is None else _p(ladder, c_double), self.device, self.chain_begin,
-                              self.chain_end, 1 if self.sequential_instances else 0)
+                              self.chain_end, 1 if self.sequential_instances else 0, self.max_blocks)
         return cfg, ladder
 
 

@@ -1,0 +1,52 @@
+"""Online rolling-window driver (BASELINE configs[4])."""
+import numpy as np
+import pytest
+
+import paper_2504_14966_b200 as S
+from paper_2504_14966_b200 import online as O
+
+
+def test_stream_is_deterministic_and_poisson():
+    a = O.make_stream(4000, rate_per_s=2.0, seed=3)
+    b = O.make_stream(4000, rate_per_s=2.0, seed=3)
+    assert np.array_equal(a.arrival_ms, b.arrival_ms) and np.array_equal(a.pred_out, b.pred_out)
+    gaps = np.diff(a.arrival_ms)
+    assert abs(gaps.mean() - 500.0) < 25.0  # mean inter-arrival 1 / rate
+    w = S.generate_mixed(4000, 3)  # lengths are the reference generator's
+    assert np.array_equal(a.input_len, w.arrays["in_len"])
+
+
+def test_fcfs_completes_every_request_and_matches_a_direct_simulation():
+    s = O.make_stream(300, rate_per_s=0.5, seed=1)
+    r = O.run_online(s, "fcfs", n_instances=2, window_ms=5000.0)
+    assert r.n == 300 and 0 < r.n_met <= 300 and r.total_latency_ms > 0
+    # single instance, one huge window: FCFS = arrival-order greedy batches back to back
+    s1 = O.make_stream(40, rate_per_s=1000.0, seed=2)
+    r1 = O.run_online(s1, "fcfs", n_instances=1, window_ms=1e12, max_batch=4)
+    c = S.table_coefficients()
+    t = max(0.0, np.ceil(s1.arrival_ms[-1] / 1e12) * 1e12)  # window that holds every arrival
+    n_met = 0
+    order = list(range(40))
+    for k in range(0, 40, 4):
+        b = order[k:k + 4]
+        start = t + 0.1
+        li, lo = s1.input_len[b].astype(float), s1.true_out[b].astype(float)
+        pf, dec = O.prefill_ms(c, len(b), li), O.decode_total_ms(c, len(b), li, lo)
+        for j, i in enumerate(b):
+            if s1.cls[i] == 0:
+                n_met += start + pf[j] + dec[j] - s1.arrival_ms[i] <= 30000.0
+            else:
+                n_met += (start + pf[j] - s1.arrival_ms[i] <= 10000.0) and dec[j] / lo[j] <= 50.0
+        t = start + (pf + dec).max()
+    assert r1.n_met == n_met
+
+
+@pytest.mark.gpu
+def test_online_sa_beats_fcfs():
+    mu = O.service_rate_per_s()
+    s = O.make_stream(1500, rate_per_s=0.9 * 2 * mu, seed=4)
+    sa = O.run_online(s, "sa", n_instances=2, window_ms=5000.0, budget_ms=3.0, chains=1024)
+    fc = O.run_online(s, "fcfs", n_instances=2, window_ms=5000.0)
+    assert sa.n == fc.n == 1500
+    assert sa.n_met >= fc.n_met
+    assert max(sa.overhead_ms) < 1000.0
