@@ -62,7 +62,7 @@ def parse():
 
 # per-chain objective_scale multipliers: the reference default (x1) walks randomly at N=1024
 # (SURVEY 6.3); larger factors make greedier chains. Chain c uses ladder[c % len].
-SCALE_LADDER = (1.0, 10.0, 100.0, 1000.0, 1e4, 1e5)
+SCALE_LADDER = (1e4, 1e5, 1e6, 1e7, 1e8)  # best of tools/quality_sweep.py (profiles/r1/quality_sweep.jsonl)
 
 
 # ---------------------------------------------------------------- helpers
