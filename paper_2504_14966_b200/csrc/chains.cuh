@@ -28,6 +28,7 @@ struct UnitSum {
     int fe;       // unit contains a batch end
     int cnt;      // positions in the unit
     int A;        // positions after the first batch end
+    int always;   // positions whose deadline is +inf (met in every schedule; excluded from dmax)
 };
 
 template <int UPL>
@@ -141,7 +142,9 @@ __device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint3
     s.tm = (w == 0 || la < cnt - 1) ? m_last : 0.0;
     s.inner = inner;
     s.bs = bs;
-    s.dmax = key2f(__reduce_max_sync(FULL, f2key(__double2float_ru(D))));
+    const bool inf = D == INFINITY;  // host marks deadlines no schedule can miss as +inf
+    s.always = __popc(__ballot_sync(FULL, inf));
+    s.dmax = key2f(__reduce_max_sync(FULL, f2key(__double2float_ru(inf ? kNegInf : D))));
     return s;
 }
 
@@ -303,7 +306,7 @@ __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16
     const int todo = full ? 32 * UPL : (du0 < 0 ? 0 : (du1 >= 0 && du1 != du0 ? 2 : 1));
     for (int i = 0; i < todo; ++i) {  // one inlined copy of the unit summary
         const int u = full ? i : (i == 0 ? du0 : du1);
-        UnitSum v{0.0, 0.0, 0.0, 0.0, -INFINITY, 0, 0, 0};
+        UnitSum v{0.0, 0.0, 0.0, 0.0, -INFINITY, 0, 0, 0, 0};
         if (u < U) v = unit_summary<SMEM>(ent, bits, tab, n, mb, u, lane), sc1 += lane == 0 ? 32 : 0;
         if (lane == u / UPL) {
 #pragma unroll
@@ -323,7 +326,7 @@ __device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16
         const bool live = E[k] <= (double)s.dmax;
         const bool dirty = full || u == du0 || u == du1;
         const bool need = live && (dirty || E[k] != cs.wE[k] || fmk[k] != cs.wF[k]);
-        nN[k] = live ? cs.wN[k] : 0;
+        nN[k] = live ? cs.wN[k] : s.always;
         unsigned mask = __ballot_sync(FULL, need);
         while (mask) {  // cooperative SLO walks of the units that need one
             const int ln = __ffs(mask) - 1;

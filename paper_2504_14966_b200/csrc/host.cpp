@@ -522,6 +522,20 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
             deadline[(std::size_t)(b - 1) * n + i] = d;
         }
     }
+    // No batch can start later than the sum of every request's largest exec (a makespan is at
+    // most the sum of its members'). A deadline at or beyond that bound is met in every schedule:
+    // store +inf, which leaves every exact compare unchanged and lets the chain kernel count such
+    // requests without walking them (loose classes such as "offline" would otherwise keep every
+    // unit live). The margin covers the engine's reassociated sums.
+    double horizon = 0.0;
+    for (int i = 0; i < n; ++i) {
+        double m = 0.0;
+        for (int b = 1; b <= max_batch; ++b) m = std::max(m, exec[(std::size_t)(b - 1) * n + i]);
+        horizon += m;
+    }
+    const double never_late = horizon * (1.0 + 1e-9) + 1.0;
+    for (double& d : deadline)
+        if (d >= never_late) d = std::numeric_limits<double>::infinity();
 }
 
 AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,

@@ -7,6 +7,11 @@ n = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 chains = int(sys.argv[2]) if len(sys.argv) > 2 else 16384
 reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
 w = S.generate_mixed(n, 0); c = S.table_coefficients(); ids = sorted(w.ids())
+if len(sys.argv) > 4 and sys.argv[4] == "3class":  # configs[0] mix: code / chat / offline (E2E 1e9 ms)
+    code, chat = S.default_slo_classes()
+    reqs = [S.Request(r.id, 2 if r.id % 3 == 2 else r.task_class_id, r.input_len, r.true_output_len,
+                      r.predicted_output_len) for r in w.requests]
+    w = S.Workload(reqs, [code, chat, S.TaskClass(2, "offline", S.SloSpec.e2e(1e9))])
 s, i = S.initial_candidates(w, ids, c, 4)
 ev = S.evaluate(s, c, w)
 pos = {r: k for k, r in enumerate(ids)}
