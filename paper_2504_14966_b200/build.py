@@ -23,6 +23,7 @@ LIB = os.path.join(PKG, "libslosched_b200.so")
 NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompiler", "-fPIC", f"-I{INC}"]
+NVCC_FLAGS += os.environ.get("SLO_EXTRA_NVCC", "").split()  # e.g. -DSLO_CHAIN_THREADS=640 (tuning runs)
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", f"-I{INC}"]
 
 HOST_SRCS = ["host.cpp", "capi.cpp"]

@@ -15,6 +15,9 @@
 // move only the (<= 2) dirty units are re-summarised.
 
 #define kNegInf (-static_cast<double>(INFINITY))
+#ifndef SLO_CHAIN_THREADS
+#define SLO_CHAIN_THREADS 768  // k_chains<1> block size: 24 warps, 80 registers per thread
+#endif
 constexpr int kPreAttempts = 6;                      // move attempts drawn ahead (3 words each)
 constexpr int kRndWords = 3 * kPreAttempts + 2;      // + the acceptance uniform (2 words)
 static_assert(kRndWords % 4 == 0, "Philox block rows are stored as uint4");
@@ -385,7 +388,7 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
 }
 
 template <int UPL, bool SMEM>
-__global__ void __launch_bounds__(UPL == 1 ? 768 : 512, 1) k_chains(const ChainParams p) {
+__global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chains(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = p.n, mb = p.mb;
