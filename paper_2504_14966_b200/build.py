@@ -71,6 +71,13 @@ def build(verbose=False, force=False, ptxas_info=False) -> str:
         # the reference's slosched:: symbols (the integration shim does exactly that)
         log += _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-Xlinker", "-Bsymbolic"], verbose)
         os.replace(tmp, LIB)
+    # the C++ example (a reference-style caller of include/slosched_b200.hpp)
+    ex_src = os.path.join(ROOT, "examples", "anneal_example.cpp")
+    ex_bin = os.path.join(ROOT, "examples", "_build", "anneal_example")
+    if os.path.exists(ex_src) and (force or _stale(ex_bin, [ex_src, LIB] + headers)):
+        os.makedirs(os.path.dirname(ex_bin), exist_ok=True)
+        log += _run(["g++", "-std=c++17", "-O2", f"-I{INC}", ex_src, "-o", ex_bin, f"-L{PKG}", "-lslosched_b200",
+                     f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_2504_14966_b200"], verbose)
     return log
 
 

@@ -211,6 +211,54 @@ def test_schedule_all_concurrent_instances_equal_sequential():
     assert ids == sorted(w.ids())
 
 
+def test_cpp_example_runs_against_the_cpp_api(port):
+    """examples/anneal_example.cpp: a C++ caller of include/slosched_b200.hpp (no Python)."""
+    import os
+    import re
+    import subprocess
+
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "examples", "_build", "anneal_example")
+    if not os.path.exists(exe):
+        pytest.skip("example not built")
+    out = subprocess.run([exe, "256"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stderr
+    rep = re.search(r"replay: n_met=(\d+) g=(\S+) proposals=(\d+) accepted=(\d+)", out.stdout)
+    w = S.generate_mixed(256, 0)
+    o = port.anneal(_flat(w), TABLE_COEFFS, w.ids(), 4, seed=0)
+    assert int(rep.group(1)) == o["n"] and float(rep.group(2)) == float(f"{o['g']:.9e}")
+    assert (int(rep.group(3)), int(rep.group(4))) == (o["proposals"], o["accepted"])
+    assert "schedule_all: instances=4" in out.stdout
+
+
+def test_distributed_path_over_nccl_single_rank():
+    """The multi-GPU exchange on real NCCL (one rank here: the box has one GPU per call): CUDA
+    tensors through all_gather / broadcast, and anneal_distributed == anneal over the same chains."""
+    import os
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2504_14966_b200.distributed import anneal_distributed
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        c = S.table_coefficients()
+        w = _three_class(96, 31)
+        cfg = S.AnnealConfig(seed=2, chains=512, t0=80.0, iter=20, scale_ladder=(1.0, 1e3), device=0)
+        got = anneal_distributed(w, w.ids(), c, cfg, 4)
+        want = S.anneal(w, w.ids(), c, cfg, 4)
+        assert got.best.schedule.batches == want.best.schedule.batches and got.best.g == want.best.g
+        assert got.stats.proposals == want.stats.proposals
+    finally:
+        dist.destroy_process_group()
+
+
 # ---------------------------------------------------------------- exhaustive oracle
 def test_exhaustive_matches_golden():
     c = S.table_coefficients()
