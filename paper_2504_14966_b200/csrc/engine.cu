@@ -13,7 +13,7 @@
 //
 // Kernels:
 //   k_eval_exact   K1: one candidate per thread, sequential reference arithmetic.
-//   k_replay       K2: one chain per thread, xoshiro256++ and FlatSchedule moves, exact.
+//   k_replay       K2: one chain per warp, xoshiro256++ and FlatSchedule moves, exact.
 //   k_chains<P>    K3: one chain per warp, Philox4x32-10 moves, incremental objective.
 //   k_argmax       K4: best-of-chains (g desc, t asc, chain asc) + winner copy.
 // P: = /root/reference/proj/.
@@ -132,239 +132,11 @@ __global__ void k_eval_exact(int count, int n, int words, const uint16_t* __rest
     g_out[c] = total > 0.0 ? (double)met / total : 0.0;
 }
 
-// ================================================================ K2: exact replay
-// xoshiro256++ / splitmix64 (P:include/slosched/rng.hpp:14-57)
-struct Xoshiro {
-    uint64_t s[4];
-    __device__ static uint64_t mix(uint64_t z) {
-        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
-        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
-        return z ^ (z >> 31);
-    }
-    __device__ explicit Xoshiro(uint64_t seed) {
-        uint64_t z = seed;
-        for (int i = 0; i < 4; ++i) {
-            z += 0x9e3779b97f4a7c15ULL;
-            s[i] = mix(z);
-        }
-    }
-    __device__ static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-    __device__ uint64_t next() {
-        const uint64_t out = rotl(s[0] + s[3], 23) + s[0];
-        const uint64_t t = s[1] << 17;
-        s[2] ^= s[0];
-        s[3] ^= s[1];
-        s[1] ^= s[2];
-        s[0] ^= s[3];
-        s[2] ^= t;
-        s[3] = rotl(s[3], 45);
-        return out;
-    }
-    __device__ double uniform() { return (double)(next() >> 11) * 0x1.0p-53; }
-    __device__ uint64_t index(uint64_t n) {
-        uint64_t x = next();
-        uint64_t lo = x * n, hi = __umul64hi(x, n);
-        if (lo < n) {
-            const uint64_t thr = (0 - n) % n;
-            while (lo < thr) {
-                x = next();
-                lo = x * n;
-                hi = __umul64hi(x, n);
-            }
-        }
-        return hi;
-    }
-};
-
-struct Flat {  // FlatSchedule (P:src/priority_mapper.cpp:104-199) over global scratch
-    int* perm;
-    int* sizes;
-    int nb;
-};
-
-__device__ int fl_batch_of(const Flat& f, int pos) {
-    int k = 0;
-    for (int acc = f.sizes[0]; pos >= acc; acc += f.sizes[++k]) {
-    }
-    return k;
-}
-
-__device__ int fl_batch_start(const Flat& f, int k) {
-    int acc = 0;
-    for (int i = 0; i < k; ++i) acc += f.sizes[i];
-    return acc;
-}
-
-__device__ void fl_erase(Flat& f, int k) {
-    for (int i = k; i + 1 < f.nb; ++i) f.sizes[i] = f.sizes[i + 1];
-    f.nb--;
-}
-
-__device__ bool fl_squeeze(Flat& f, int n, Xoshiro& r, int mb) {
-    if (f.nb < 2) return false;
-    const int first = f.sizes[0];
-    const int pos = first + (int)r.index((uint64_t)(n - first));
-    const int k = fl_batch_of(f, pos);
-    if (f.sizes[k - 1] >= mb) return false;
-    const int dst = fl_batch_start(f, k);
-    const int v = f.perm[pos];
-    for (int q = pos; q > dst; --q) f.perm[q] = f.perm[q - 1];
-    f.perm[dst] = v;
-    f.sizes[k - 1]++;
-    if (--f.sizes[k] == 0) fl_erase(f, k);
-    return true;
-}
-
-__device__ bool fl_delay(Flat& f, int n, Xoshiro& r, int mb) {
-    if (n == 0) return false;
-    const int pos = (int)r.index((uint64_t)n);
-    const int k = fl_batch_of(f, pos);
-    const bool has_next = k + 1 < f.nb;
-    if (has_next && f.sizes[k + 1] >= mb) return false;
-    const int dst = has_next ? fl_batch_start(f, k + 2) : n;
-    const int v = f.perm[pos];
-    for (int q = pos; q + 1 < dst; ++q) f.perm[q] = f.perm[q + 1];
-    f.perm[dst - 1] = v;
-    if (has_next) f.sizes[k + 1]++;
-    else f.sizes[f.nb++] = 1;
-    if (--f.sizes[k] == 0) fl_erase(f, k);
-    return true;
-}
-
-__device__ bool fl_swap(Flat& f, int n, Xoshiro& r) {
-    if (n < 2) return false;
-    const uint64_t a = r.index((uint64_t)n);
-    uint64_t b = r.index((uint64_t)(n - 1));
-    if (b >= a) ++b;
-    const int t = f.perm[a];
-    f.perm[a] = f.perm[b];
-    f.perm[b] = t;
-    return true;
-}
-
-__device__ bool fl_propose(Flat& f, int n, Xoshiro& r, int mb) {
-    if (n == 0) return false;
-    for (int attempt = 0; attempt < 8; ++attempt) {
-        const uint64_t op = r.index(3);
-        if (op == 0) {
-            if (fl_squeeze(f, n, r, mb)) return true;
-        } else if (op == 1) {
-            if (fl_delay(f, n, r, mb)) return true;
-        } else {
-            if (fl_swap(f, n, r)) return true;
-        }
-    }
-    return fl_swap(f, n, r);
-}
-
-__device__ double fl_score(const Flat& f, int n, const double2* __restrict__ tab, int* n_met_out,
-                           double* t_out) {
-    int met = 0;
-    double total = 0.0, elapsed = 0.0;
-    int pos = 0;
-    for (int k = 0; k < f.nb; ++k) {
-        const int part = f.sizes[k], bidx = part - 1;
-        double makespan = 0.0;
-        for (int j = 0; j < part; ++j) {
-            const double2 v = __ldg(&tab[bidx * n + f.perm[pos + j]]);
-            const double e2e = elapsed + v.x;
-            total += e2e;
-            met += elapsed <= v.y;
-            makespan = dmax(makespan, v.x);
-        }
-        elapsed += makespan;
-        pos += part;
-    }
-    if (n_met_out) *n_met_out = met;
-    if (t_out) *t_out = total;
-    return total > 0.0 ? (double)met / total : 0.0;
-}
-
-__device__ void fl_copy(Flat& dst, const Flat& src, int n) {
-    for (int i = 0; i < n; ++i) dst.perm[i] = src.perm[i];
-    for (int i = 0; i < src.nb; ++i) dst.sizes[i] = src.sizes[i];
-    dst.nb = src.nb;
-}
-
-struct ReplayParams {
-    int n, mb, chains;
-    const double2* tab;
-    double t0, t_thres, tau, scale;
-    int iter;
-    uint64_t seed;
-    const int* start_perm;
-    const int* start_sizes;
-    int start_nb;
-    int* scratch;  // [chains][6n]
-    int* best_perm;   // [chains][n]
-    int* best_sizes;  // [chains][n]
-    int* best_nb;     // [chains]
-    ChainRec* rec;
-};
-
-// One thread = one reference chain (seed + chain id), the loop of P:src/priority_mapper.cpp:377-402.
-__global__ void k_replay(const ReplayParams p) {
-    const int c = blockIdx.x * blockDim.x + threadIdx.x;
-    if (c >= p.chains) return;
-    const int n = p.n;
-    // three FlatSchedules per chain; each sizes array has n + 1 slots because delay appends a
-    // trailing batch before erasing an emptied one (all-singleton schedules briefly hold n + 1)
-    const size_t stride = 2 * (size_t)n + 1;
-    int* base = p.scratch + (size_t)c * 3 * stride;
-    Flat cur{base, base + n, p.start_nb}, scr{base + stride, base + stride + n, 0},
-        best{base + 2 * stride, base + 2 * stride + n, 0};
-    for (int i = 0; i < n; ++i) cur.perm[i] = p.start_perm[i];
-    for (int i = 0; i < p.start_nb; ++i) cur.sizes[i] = p.start_sizes[i];
-    double f = fl_score(cur, n, p.tab, nullptr, nullptr);
-    fl_copy(best, cur, n);
-    double best_f = f;
-    Xoshiro rng(p.seed + (uint64_t)c);
-    unsigned long long props = 0, accs = 0;
-    int levels = 0;
-    for (double t = p.t0; t >= p.t_thres; t *= p.tau, ++levels) {
-        for (int k = 0; k < p.iter; ++k) {
-            fl_copy(scr, cur, n);
-            fl_propose(scr, n, rng, p.mb);
-            const double f_new = fl_score(scr, n, p.tab, nullptr, nullptr);
-            props++;
-            bool accept = f_new > f;
-            if (!accept) {
-                const double x = (f - f_new) * p.scale / t;
-                const double u = rng.uniform();
-                accept = x < 38.0 ? u < exp(-x) : u == 0.0;
-            }
-            if (accept) {
-                accs++;
-                const Flat tmp = cur;
-                cur = scr;
-                scr = tmp;
-                f = f_new;
-                if (f > best_f) {
-                    fl_copy(best, cur, n);
-                    best_f = f;
-                }
-            }
-        }
-    }
-    int nm;
-    double tt;
-    fl_score(best, n, p.tab, &nm, &tt);
-    for (int i = 0; i < n; ++i) p.best_perm[(size_t)c * n + i] = best.perm[i];
-    for (int i = 0; i < best.nb; ++i) p.best_sizes[(size_t)c * n + i] = best.sizes[i];
-    p.best_nb[c] = best.nb;
-    ChainRec r;
-    r.g = best_f;
-    r.t = tt;
-    r.cur_f = f;
-    r.n_met = nm;
-    r.levels = levels;
-    r.proposals = props;
-    r.accepted = accs;
-    p.rec[c] = r;
-}
-
 // ================================================================ K3: chains
 #include "chains.cuh"
+
+// ================================================================ K2: exact replay
+#include "replay.cuh"
 
 // ================================================================ exhaustive oracle
 #include "exhaustive.cuh"
@@ -500,8 +272,6 @@ struct slo_ctx {
     // chains
     DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
         result, win_ent, win_bits;
-    // replay
-    DevBuf r_scratch, r_best_perm, r_best_sizes, r_best_nb, r_start_perm, r_start_sizes;
     // K1
     DevBuf e_perms, e_bits, e_n, e_t, e_g;
     bool prepared = false;
@@ -750,25 +520,47 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     c->start_nb = start_nb;
     c->prepared = false;
 
-    if (prm->rng_mode == SLO_RNG_XOSHIRO_REPLAY) {
+    if (prm->rng_mode == SLO_RNG_XOSHIRO_REPLAY) {  // K2: one warp per chain, state in shared memory
         const int chains = c->chain_count;
-        CK(c->r_scratch.reserve((size_t)chains * 3 * (2 * (size_t)n + 1) * sizeof(int)));
-        CK(c->r_best_perm.reserve((size_t)chains * n * sizeof(int)));
-        CK(c->r_best_sizes.reserve((size_t)chains * n * sizeof(int)));
-        CK(c->r_best_nb.reserve((size_t)chains * sizeof(int)));
+        const int npad = (n + 31) & ~31;
+        std::vector<uint16_t> ent(npad, 0);
+        std::vector<uint32_t> bits(npad / 32, 0);
+        int pos = 0;
+        for (int k = 0; k < start_nb; ++k) {
+            for (int j = 0; j < start_sizes[k]; ++j, ++pos) ent[pos] = (uint16_t)(start_perm[pos] + (start_sizes[k] - 1) * n);
+            bits[(pos - 1) >> 5] |= 1u << ((pos - 1) & 31);
+        }
+        CK(c->start_ent.reserve((size_t)npad * sizeof(uint16_t)));
+        CK(c->start_bits.reserve((size_t)(npad / 32) * sizeof(uint32_t)));
+        CK(c->best_ent.reserve((size_t)chains * npad * sizeof(uint16_t)));
+        CK(c->best_bits.reserve((size_t)chains * (npad / 32) * sizeof(uint32_t)));
         CK(c->rec.reserve((size_t)chains * sizeof(ChainRec)));
-        CK(c->r_start_perm.reserve((size_t)n * sizeof(int)));
-        CK(c->r_start_sizes.reserve((size_t)n * sizeof(int)));
         CK(c->result.reserve(sizeof(ChainResult)));
-        CK(cudaMemcpyAsync(c->r_start_perm.p, start_perm, (size_t)n * sizeof(int), cudaMemcpyHostToDevice, c->stream));
-        CK(cudaMemcpyAsync(c->r_start_sizes.p, start_sizes, (size_t)start_nb * sizeof(int), cudaMemcpyHostToDevice, c->stream));
+        CK(c->win_ent.reserve((size_t)npad * sizeof(uint16_t)));
+        CK(c->win_bits.reserve((size_t)(npad / 32) * sizeof(uint32_t)));
+        CK(cudaMemcpyAsync(c->start_ent.p, ent.data(), (size_t)npad * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(c->start_bits.p, bits.data(), bits.size() * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+        CK(cudaStreamSynchronize(c->stream));
+        const size_t slot = replay_slot_bytes(npad);
+        if (slot > c->smem_optin) return fail(SLO_ERR_CAPACITY, "replay: schedule too large for shared memory");
+        // one warp per block: the rest of the SM's 256 KB stays L1 for the table gathers
+        c->block = 32;
+        c->smem = (size_t)(c->block / 32) * slot;
+        c->grid = (chains + c->block / 32 - 1) / (c->block / 32);
+        CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_optin));
+        // carve out only the shared memory the slot needs: the rest of the SM's 256 KB stays L1,
+        // which holds the (exec, deadline) table for the per-proposal gathers
+        CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                (int)std::min<size_t>(100, (c->smem * 100 + c->smem_optin - 1) / c->smem_optin + 1)));
+        c->UPL = npad / 32;  // words of the state, for fetch
         ReplayParams& rp = c->rp;
-        rp.n = n, rp.mb = c->mb, rp.chains = chains, rp.tab = c->tab.as<double2>();
+        rp.n = n, rp.mb = c->mb, rp.chains = chains, rp.magic = (1ull << 32) / (uint64_t)n + 1;
+        rp.tab = c->tab.as<double2>();
         rp.t0 = prm->t0, rp.t_thres = prm->t_thres, rp.tau = prm->tau, rp.scale = prm->objective_scale;
         rp.iter = prm->iter, rp.seed = prm->seed + (uint64_t)cb;
-        rp.start_perm = c->r_start_perm.as<int>(), rp.start_sizes = c->r_start_sizes.as<int>(), rp.start_nb = start_nb;
-        rp.scratch = c->r_scratch.as<int>(), rp.best_perm = c->r_best_perm.as<int>();
-        rp.best_sizes = c->r_best_sizes.as<int>(), rp.best_nb = c->r_best_nb.as<int>(), rp.rec = c->rec.as<ChainRec>();
+        rp.start_ent = c->start_ent.as<uint16_t>(), rp.start_bits = c->start_bits.as<uint32_t>();
+        rp.best_ent = c->best_ent.as<uint16_t>(), rp.best_bits = c->best_bits.as<uint32_t>();
+        rp.rec = c->rec.as<ChainRec>(), rp.npad = npad;
         c->prepared = true;
         return SLO_OK;
     }
@@ -844,11 +636,12 @@ int slo_chains_launch(slo_ctx* c) {
     CK(cudaMemsetAsync(c->rec.p, 0, cc * sizeof(ChainRec), c->stream));
     CK(cudaEventRecord(c->ev0, c->stream));
     if (c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY) {
-        k_replay<<<((int)cc + 31) / 32, 32, 0, c->stream>>>(c->rp);
+        k_replay<<<c->grid, c->block, c->smem, c->stream>>>(c->rp);
         CK(cudaGetLastError());
         CK(cudaEventRecord(c->ev1, c->stream));
-        k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), 0, 0, nullptr,
-                                            nullptr, nullptr, nullptr);
+        k_argmax<<<1, 512, 0, c->stream>>>((int)cc, c->rec.as<ChainRec>(), c->result.as<ChainResult>(), c->rp.npad,
+                                            c->rp.npad / 32, c->best_ent.as<uint16_t>(), c->best_bits.as<uint32_t>(),
+                                            c->win_ent.as<uint16_t>(), c->win_bits.as<uint32_t>());
         CK(cudaGetLastError());
         return SLO_OK;
     }
@@ -871,23 +664,17 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     std::vector<uint16_t> ent;
     std::vector<uint32_t> bits;
     const bool replay = c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY;
-    if (!replay) {
-        ent.resize(1024 * (size_t)c->UPL);
-        bits.resize(32 * (size_t)c->UPL);
-        CK(cudaMemcpyAsync(ent.data(), c->win_ent.p, ent.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(bits.data(), c->win_bits.p, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
-    }
+    // winner entries: npad words for replay, 1024 * UPL for the chain kernel
+    const size_t ent_n = replay ? (size_t)c->rp.npad : 1024 * (size_t)c->UPL;
+    ent.resize(ent_n);
+    bits.resize(replay ? (size_t)c->rp.npad / 32 : 32 * (size_t)c->UPL);
+    CK(cudaMemcpyAsync(ent.data(), c->win_ent.p, ent.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(bits.data(), c->win_bits.p, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
     if (r.chain < 0) return fail(SLO_ERR_STATE, "slo_chains_fetch: no chain ran (budget too small?)");
-    if (replay) {
-        int nb = 0;
-        CK(cudaMemcpy(&nb, c->r_best_nb.as<int>() + r.chain, sizeof(int), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(best_perm, c->r_best_perm.as<int>() + (size_t)r.chain * n, (size_t)n * sizeof(int), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(best_sizes, c->r_best_sizes.as<int>() + (size_t)r.chain * n, (size_t)nb * sizeof(int), cudaMemcpyDeviceToHost));
-        *best_nb = nb;
-    } else {
+    {
         int nb = 0, run = 0;
         for (int q = 0; q < n; ++q) {
             best_perm[q] = ent[q] % n;
