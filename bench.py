@@ -235,6 +235,10 @@ def run_ours(args):
     ev_s, ev_i = S.evaluate(s_sched, c, w), S.evaluate(i_sched, c, w)
     start = s_sched if ev_s.g >= ev_i.g else i_sched
     f0 = max(ev_s.g, ev_i.g)
+    d_sched = S.deadline_first_candidate(w, ids, c, mb)  # the chains' third start (anneal() does the same)
+    ev_d = S.evaluate(d_sched, c, w)
+    if ev_d.g > f0:
+        start, f0 = d_sched, ev_d.g
     scale = args.t0 / f0 if f0 > 0 else args.t0
     pos = {rid: k for k, rid in enumerate(ids)}
     start_perm = [pos[x] for x in start.flatten()]
@@ -385,7 +389,8 @@ def run_ours(args):
                    "scale_ladder": list(SCALE_LADDER), "l2": "flushed between steps (512 MiB write)",
                    "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather argmax"},
         "attainment": attain_n / n, "g_req_per_ms": attain_g,
-        "attainment_start": max(ev_s.n, ev_i.n) / n,
+        "attainment_start": max(ev_s, ev_i, ev_d, key=lambda e: e.g).n / n,
+        "attainment_reference_starts": max(ev_s, ev_i, key=lambda e: e.g).n / n,
         "levels_run": int(min(r[6] for r in results)), "chains_run": int(min(r[7] for r in results)),
         "wall_s_timed": wall_s,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

@@ -49,6 +49,8 @@ typedef struct {
     int32_t chain_begin, chain_end; /* chain_end < 0: all chains */
     int32_t sequential_instances;   /* schedule_all: 1 = one instance after another (default concurrent) */
     int32_t max_blocks;             /* > 0: cap the chain grid (concurrent callers share the GPU) */
+    int32_t start_policy;           /* chains: 0 = best of the reference's two starts and the deadline-first
+                                       candidate (default), 1 = the reference's two only */
 } slosched_anneal_config;
 
 typedef struct {
@@ -57,6 +59,7 @@ typedef struct {
     double g_sorted_start, g_input_start, objective_scale_used;
     int32_t chains_run, levels_run, best_chain;
     double engine_g, engine_t, kernel_ms;
+    double g_deadline_start;
 } slosched_anneal_stats;
 
 const char* slosched_last_error(void);
@@ -74,6 +77,11 @@ int slosched_evaluate(const slosched_workload* w, const double* coeffs8, const i
 int slosched_initial_candidates(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
                                 int32_t max_batch, int32_t* sorted_ids, int32_t* sorted_sizes, int32_t* sorted_nb,
                                 int32_t* input_ids, int32_t* input_sizes, int32_t* input_nb);
+
+/* Engine extension (no reference counterpart): the deadline-first start of the chains. */
+int slosched_deadline_first_candidate(const slosched_workload* w, const double* coeffs8, const int32_t* ids,
+                                      int32_t n, int32_t max_batch, int32_t* out_ids, int32_t* out_sizes,
+                                      int32_t* out_nb);
 
 int slosched_neighbor_walk(const int32_t* ids, const int32_t* sizes, int32_t nb, uint64_t seed, int32_t steps,
                            int32_t max_batch, int32_t* out_ids, int32_t* out_sizes, int32_t* out_nb);

@@ -195,6 +195,7 @@ struct EngineOptions {
     int chain_begin = 0, chain_end = -1;  // slice of [0, chains) run by this call (multi-GPU sharding)
     int max_blocks = 0;                 // > 0: cap the chain grid (concurrent launches share the GPU)
     bool concurrent_instances = true;   // schedule_all: anneal the instances concurrently (Chains mode)
+    bool deadline_start = true;         // Chains mode: the deadline-first candidate joins the two starts
 };
 
 struct AnnealConfig {
@@ -222,6 +223,7 @@ struct AnnealStats {
     double engine_g = 0.0;    // best score as computed on the device
     double engine_t = 0.0;    // its summed latency (tie-break of the best-of-chains argmax)
     double kernel_ms = 0.0;   // device time of the annealing launch
+    double g_deadline_start = 0.0;  // G of the deadline-first candidate (Chains mode; 0 if not built)
 };
 
 struct AnnealResult {
@@ -231,6 +233,13 @@ struct AnnealResult {
 
 std::pair<Schedule, Schedule> initial_candidates(const Workload&, const std::vector<int>& request_ids,
                                                  const LatencyCoefficients&, int max_batch);
+// Engine extension: a third start for the chains. Requests are taken in order of their latest
+// feasible start (full batches); a request joins the kept set -- held in ascending exec order and
+// cut into batches of max_batch -- when every kept request still starts in time, otherwise the
+// longest kept request is dropped (Moore-Hodgson with batching). Kept batches run first, the
+// rest follow shortest first.
+Schedule deadline_first_candidate(const Workload&, const std::vector<int>& request_ids, const LatencyCoefficients&,
+                                  int max_batch);
 std::optional<EvaluatedSchedule> shortcut_check(const Schedule& sorted_schedule, const LatencyCoefficients&,
                                                 const Workload&);
 Schedule neighbor(const Schedule& schedule, Rng& rng, int max_batch);

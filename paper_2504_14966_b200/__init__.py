@@ -6,7 +6,7 @@ touch the GPU; the first anneal()/Engine() call does, and fails loudly without o
 """
 from .slosched import (  # noqa: F401
     AnnealConfig, AnnealResult, AnnealStats, CapacityError, DataError, EngineError, EvaluatedSchedule,
-    ExhaustiveResult, exhaustive,
+    ExhaustiveResult, deadline_first_candidate, exhaustive,
     InstanceState, LatencyCoefficients, Request, RequestMetrics, Schedule, ScheduleAllResult, SearchMode, SloKind,
     SloSpec, TaskClass, Workload, anneal, anneal_flat, default_slo_classes, default_synth_classes, evaluate,
     generate_mixed, initial_candidates, latest_start, neighbor_walk, predict_decode_total, predict_exec,

@@ -9,7 +9,7 @@ import os
 from ctypes import POINTER, Structure, c_char_p, c_double, c_float, c_int32, c_int64, c_uint32, c_uint64, c_void_p
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libslosched_b200.so")
+LIB_PATH = os.environ.get("SLOSCHED_LIB") or os.path.join(PKG, "libslosched_b200.so")  # override: A/B runs
 
 # slo_status codes (include/slosched_gpu.h)
 SLO_OK, SLO_ERR_DATA, SLO_ERR_CAPACITY, SLO_ERR_CUDA, SLO_ERR_COMM, SLO_ERR_STATE, SLO_ERR_ARG = range(7)
@@ -29,14 +29,16 @@ class SloAnnealConfig(Structure):
                 ("has_objective_scale", c_int32), ("objective_scale", c_double), ("mode", c_int32),
                 ("chains", c_int32), ("budget_ms", c_double), ("n_scale_ladder", c_int32),
                 ("scale_ladder", POINTER(c_double)), ("device", c_int32), ("chain_begin", c_int32),
-                ("chain_end", c_int32), ("sequential_instances", c_int32), ("max_blocks", c_int32)]
+                ("chain_end", c_int32), ("sequential_instances", c_int32), ("max_blocks", c_int32),
+                ("start_policy", c_int32)]
 
 
 class SloAnnealStats(Structure):
     _fields_ = [("proposals", c_uint64), ("accepted", c_uint64), ("shortcut", c_int32),
                 ("g_sorted_start", c_double), ("g_input_start", c_double), ("objective_scale_used", c_double),
                 ("chains_run", c_int32), ("levels_run", c_int32), ("best_chain", c_int32),
-                ("engine_g", c_double), ("engine_t", c_double), ("kernel_ms", c_double)]
+                ("engine_g", c_double), ("engine_t", c_double), ("kernel_ms", c_double),
+                ("g_deadline_start", c_double)]
 
 
 class SloChainParams(Structure):
@@ -82,6 +84,7 @@ _SIGNATURES = [
                                     _I]),
     ("slosched_initial_candidates", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, c_int32, _I, _I, _I, _I, _I,
                                               _I]),
+    ("slosched_deadline_first_candidate", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, c_int32, _I, _I, _I]),
     ("slosched_neighbor_walk", c_int32, [_I, _I, c_int32, c_uint64, c_int32, c_int32, _I, _I, _I]),
     ("slosched_anneal", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, POINTER(SloAnnealConfig), c_int32, _I, _I,
                                   _I, _I, _D, _D, POINTER(SloAnnealStats)]),

@@ -99,6 +99,7 @@ AnnealConfig config_of(const slosched_anneal_config* c) {
     a.engine.chain_end = c->chain_end;
     a.engine.concurrent_instances = c->sequential_instances == 0;
     a.engine.max_blocks = c->max_blocks;
+    a.engine.deadline_start = c->start_policy == 0;
     return a;
 }
 
@@ -116,6 +117,7 @@ void stats_out(const AnnealStats& s, slosched_anneal_stats* o) {
     o->engine_g = s.engine_g;
     o->engine_t = s.engine_t;
     o->kernel_ms = s.kernel_ms;
+    o->g_deadline_start = s.g_deadline_start;
 }
 
 }  // namespace
@@ -190,6 +192,15 @@ int slosched_initial_candidates(const slosched_workload* w, const double* c, con
         auto [s, i] = initial_candidates(wl, std::vector<int>(ids, ids + n), coeffs_of(c), max_batch);
         *sorted_nb = emit(s, sorted_ids, sorted_sizes);
         *input_nb = emit(i, input_ids, input_sizes);
+    });
+}
+
+int slosched_deadline_first_candidate(const slosched_workload* w, const double* c, const int32_t* ids, int32_t n,
+                                      int32_t max_batch, int32_t* out_ids, int32_t* out_sizes, int32_t* out_nb) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        *out_nb = emit(deadline_first_candidate(wl, std::vector<int>(ids, ids + n), coeffs_of(c), max_batch), out_ids,
+                       out_sizes);
     });
 }
 

@@ -100,14 +100,15 @@ __device__ __forceinline__ float key2f(uint32_t k) {
 }
 
 // segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
-// and are at most mb long, so log2(mb) shuffle steps suffice
+// (and at the unit start) and are at most mb long, so log2(mb) shuffle steps suffice. The
+// segment start comes from the bitmask, so only the value is shuffled.
 __device__ __forceinline__ double seg_max(double e, uint32_t w, int lane, int mb) {
     double m = dmax(e, 0.0);  // makespans start at 0 (reference P:src/priority_mapper.cpp:266)
-    int head = lane == 0 ? 1 : (int)((w >> (lane - 1)) & 1u);
+    const uint32_t below = w & ((1u << lane) - 1u);
+    const int span = lane - (below ? 32 - __clz(below) : 0);  // positions before lane in its segment
     for (int d = 1; d < mb; d <<= 1) {
         const double mu = __shfl_up_sync(FULL, m, d);
-        const int hu = __shfl_up_sync(FULL, head, d);
-        if (lane >= d && !head) m = dmax(m, mu), head = hu;
+        if (d <= span) m = dmax(m, mu);
     }
     return m;
 }

@@ -8,6 +8,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
+#include <future>
 #include <limits>
 #include <memory>
 #include <mutex>
@@ -538,11 +539,117 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
         if (d >= never_late) d = std::numeric_limits<double>::infinity();
 }
 
+namespace {
+
+// Deadline-first candidate over dense indices (tables [mb][n] from cost_tables): perm + batch sizes.
+// Requests in ascending latest start at full batches; kept set in ascending (exec, index) order cut
+// into batches of mb (a trailing partial batch uses its own size's tables); a request is kept when
+// every kept request still starts by its latest start, otherwise the longest kept one (the last)
+// is dropped (as in Moore-Hodgson; with batching this is a heuristic: the kept set need not stay
+// feasible, and the exact evaluation decides). O(n * kept).
+void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const std::vector<double>& deadline,
+                          std::vector<int>& perm, std::vector<int>& sizes) {
+    const double* ef = exec.data() + (std::size_t)(mb - 1) * n;
+    const double* df = deadline.data() + (std::size_t)(mb - 1) * n;
+    std::vector<int> order(n);
+    for (int i = 0; i < n; ++i) order[i] = i;
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return df[a] < df[b]; });
+    auto by_exec = [&](int a, int b) { return ef[a] != ef[b] ? ef[a] < ef[b] : a < b; };
+    std::vector<int> kept;
+    std::vector<double> start;  // start time of kept batch k (valid for batches before `dirty`)
+    start.push_back(0.0);
+    // re-time batches from batch k0 on; false if a kept request starts after its latest start
+    // (check: stop there, leaving later start times stale)
+    auto retime = [&](int k0, bool check) {
+        const int m = static_cast<int>(kept.size());
+        const int nb = (m + mb - 1) / mb;
+        start.resize(nb + 1);
+        bool ok = true;
+        for (int k = k0; k < nb; ++k) {
+            const int b0 = k * mb, sz = std::min(mb, m - b0);
+            const double* e = exec.data() + (std::size_t)(sz - 1) * n;
+            const double* d = deadline.data() + (std::size_t)(sz - 1) * n;
+            double mk = 0.0;
+            for (int j = b0; j < b0 + sz; ++j) {
+                ok = ok && start[k] <= d[kept[j]];
+                mk = std::max(mk, e[kept[j]]);
+            }
+            if (check && !ok) return false;
+            start[k + 1] = start[k] + mk;
+        }
+        return ok;
+    };
+    for (int i : order) {
+        if (!(df[i] >= 0.0)) continue;  // cannot start in time even first
+        const auto it = std::lower_bound(kept.begin(), kept.end(), i, by_exec);
+        const int p = static_cast<int>(it - kept.begin());
+        kept.insert(it, i);
+        if (!retime(p / mb, true)) {  // Moore-Hodgson: drop the longest kept request
+            kept.pop_back();
+            retime(std::min(p, static_cast<int>(kept.size())) / mb, false);
+        }
+    }
+    std::vector<char> in(n, 0);
+    perm.clear(), sizes.clear();
+    for (int i : kept) perm.push_back(i), in[i] = 1;
+    for (int b0 = 0; b0 < static_cast<int>(kept.size()); b0 += mb)
+        sizes.push_back(std::min(mb, static_cast<int>(kept.size()) - b0));
+    std::vector<int> rest;
+    for (int i = 0; i < n; ++i)
+        if (!in[i]) rest.push_back(i);
+    std::stable_sort(rest.begin(), rest.end(), by_exec);
+    for (std::size_t b0 = 0; b0 < rest.size(); b0 += mb) {
+        const int sz = static_cast<int>(std::min<std::size_t>(mb, rest.size() - b0));
+        for (int j = 0; j < sz; ++j) perm.push_back(rest[b0 + j]);
+        sizes.push_back(sz);
+    }
+}
+
+Schedule schedule_of(const std::vector<int>& perm, const std::vector<int>& sizes, const std::vector<int>& sorted_ids) {
+    Schedule s;
+    int pos = 0;
+    for (int sz : sizes) {
+        Batch b;
+        for (int j = 0; j < sz; ++j) b.push_back(sorted_ids[perm[pos++]]);
+        s.batches.push_back(std::move(b));
+    }
+    return s;
+}
+
+}  // namespace
+
+Schedule deadline_first_candidate(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
+                                  int max_batch) {
+    if (max_batch < 1) throw DataError("deadline_first_candidate: max_batch must be >= 1");
+    std::vector<double> exec, deadline;
+    cost_tables(w, ids, c, max_batch, exec, deadline);
+    std::vector<int> sorted_ids = ids, perm, sizes;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    deadline_first_dense(static_cast<int>(ids.size()), max_batch, exec, deadline, perm, sizes);
+    return schedule_of(perm, sizes, sorted_ids);
+}
+
 AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
                     const AnnealConfig& cfg, int max_batch) {
     cfg.validate();
     if (max_batch < 1) throw DataError("anneal: max_batch must be >= 1");
     AnnealResult res;
+    // The cost tables (and, for the chains, the deadline-first candidate) are built on a second
+    // host thread while this one builds and scores the reference's two candidates.
+    const int n = static_cast<int>(ids.size());
+    std::vector<int> sorted_ids = ids;
+    std::sort(sorted_ids.begin(), sorted_ids.end());
+    std::vector<double> exec, deadline;
+    std::vector<int> dl_perm, dl_sizes;
+    std::optional<EvaluatedSchedule> ev_dl;
+    const bool want_dl = cfg.engine.mode == SearchMode::Chains && cfg.engine.deadline_start;
+    auto tables = std::async(std::launch::async, [&] {
+        cost_tables(w, ids, c, max_batch, exec, deadline);
+        if (want_dl) {
+            deadline_first_dense(n, max_batch, exec, deadline, dl_perm, dl_sizes);
+            ev_dl = evaluate(schedule_of(dl_perm, dl_sizes, sorted_ids), c, w);
+        }
+    });
     auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
     EvaluatedSchedule ev_sorted = evaluate(sorted_s, c, w);
     res.stats.g_sorted_start = ev_sorted.g;
@@ -556,13 +663,9 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
 
     // CostModel tables over dense indices (rank of the sorted id), :205-231, with the SLO
     // test folded into a per-(batch size, request) deadline
-    const int n = static_cast<int>(ids.size());
     if (n > SLO_MAX_N) throw CapacityError("anneal: " + std::to_string(n) + " requests exceed the engine limit of 4096");
     if (max_batch > SLO_MAX_MB) throw CapacityError("anneal: max_batch above the engine limit of 16");
-    std::vector<int> sorted_ids = ids;
-    std::sort(sorted_ids.begin(), sorted_ids.end());
-    std::vector<double> exec, deadline;
-    cost_tables(w, ids, c, max_batch, exec, deadline);
+    tables.get();
     const bool use_sorted = ev_sorted.g >= ev_input.g;
     const Schedule& start = use_sorted ? sorted_s : input_s;
     std::vector<int> start_perm, start_sizes;
@@ -573,7 +676,12 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
             start_perm.push_back(static_cast<int>(std::lower_bound(sorted_ids.begin(), sorted_ids.end(), id) - sorted_ids.begin()));
     }
     // score(start) == evaluate(start).g bit-for-bit (same operand order), :362-370
-    const double f = use_sorted ? ev_sorted.g : ev_input.g;
+    double f = use_sorted ? ev_sorted.g : ev_input.g;
+    // engine extension: the chains start from the deadline-first candidate when it scores higher
+    if (ev_dl) {
+        res.stats.g_deadline_start = ev_dl->g;
+        if (ev_dl->g > f) f = ev_dl->g, start_perm = std::move(dl_perm), start_sizes = std::move(dl_sizes);
+    }
     const double scale = cfg.objective_scale ? *cfg.objective_scale : (f > 0.0 ? cfg.t0 / f : cfg.t0);
     res.stats.objective_scale_used = scale;
 
@@ -623,7 +731,9 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     }
     // final evaluation through the objective; both starts stay a floor, :404-410
     EvaluatedSchedule ev_best = evaluate(best, c, w);
-    if (ev_best.g >= std::max(ev_sorted.g, ev_input.g)) res.best = std::move(ev_best);
+    const double floor_g = std::max(ev_sorted.g, ev_input.g);
+    if (ev_best.g >= floor_g && (!ev_dl || ev_best.g >= ev_dl->g)) res.best = std::move(ev_best);
+    else if (ev_dl && ev_dl->g > floor_g) res.best = std::move(*ev_dl);
     else res.best = use_sorted ? std::move(ev_sorted) : std::move(ev_input);
     return res;
 }

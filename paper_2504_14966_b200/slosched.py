@@ -309,6 +309,7 @@ class AnnealConfig:
     chain_end: int = -1
     sequential_instances: bool = False  # schedule_all: anneal instances one after another
     max_blocks: int = 0                 # > 0: cap the chain grid (concurrent callers share the GPU)
+    deadline_start: bool = True         # chains: the deadline-first candidate joins the two starts
 
     def _c(self):
         ladder = _f64(list(self.scale_ladder)) if len(self.scale_ladder) else None
@@ -317,7 +318,8 @@ class AnnealConfig:
                               0.0 if self.objective_scale is None else self.objective_scale, int(self.mode),
                               self.chains, self.budget_ms, 0 if ladder is None else len(ladder),
                               None if ladder is None else _p(ladder, c_double), self.device, self.chain_begin,
-                              self.chain_end, 1 if self.sequential_instances else 0, self.max_blocks)
+                              self.chain_end, 1 if self.sequential_instances else 0, self.max_blocks,
+                              0 if self.deadline_start else 1)
         return cfg, ladder
 
 
@@ -335,12 +337,13 @@ class AnnealStats:
     engine_g: float = 0.0
     engine_t: float = 0.0
     kernel_ms: float = 0.0
+    g_deadline_start: float = 0.0
 
     @staticmethod
     def _from(s: SloAnnealStats) -> "AnnealStats":
         return AnnealStats(int(s.proposals), int(s.accepted), bool(s.shortcut), s.g_sorted_start, s.g_input_start,
                            s.objective_scale_used, s.chains_run, s.levels_run, s.best_chain, s.engine_g, s.engine_t,
-                           s.kernel_ms)
+                           s.kernel_ms, s.g_deadline_start)
 
 
 @dataclass
@@ -357,6 +360,18 @@ def initial_candidates(workload: Workload, request_ids, coeffs: LatencyCoefficie
     _check_api(lib().slosched_initial_candidates(byref(workload._view), _p(coeffs.as_array(), c_double), _p(ids), n,
                                                  max_batch, _p(si), _p(ss), byref(snb), _p(ii), _p(isz), byref(inb)))
     return _unflatten(si, ss[:snb.value]), _unflatten(ii, isz[:inb.value])
+
+
+def deadline_first_candidate(workload: Workload, request_ids, coeffs: LatencyCoefficients, max_batch: int) -> Schedule:
+    """The chains' third start (engine extension, include/slosched_b200.hpp): Moore-Hodgson with
+    batching over the latest-start tables."""
+    ids = _i32(request_ids)
+    n = len(ids)
+    oi, osz = np.zeros(max(n, 1), dtype=np.int32), np.zeros(max(n, 1), dtype=np.int32)
+    nb = c_int32()
+    _check_api(lib().slosched_deadline_first_candidate(byref(workload._view), _p(coeffs.as_array(), c_double), _p(ids),
+                                                       n, max_batch, _p(oi), _p(osz), byref(nb)))
+    return _unflatten(oi, osz[:nb.value])
 
 
 def shortcut_check(sorted_schedule: Schedule, coeffs, workload) -> Optional[EvaluatedSchedule]:

@@ -329,10 +329,11 @@ def test_chains_valid_and_dominant(n, mb, chains):
     assert res.best.schedule.is_partition_of(w.ids(), mb)
     if not res.stats.shortcut:
         assert res.best.g >= res.stats.g_sorted_start and res.best.g >= res.stats.g_input_start
+        assert res.best.g >= res.stats.g_deadline_start > 0.0  # the third start is a floor too
         assert res.stats.chains_run == chains
         assert res.stats.proposals == chains * res.stats.levels_run * cfg.iter
         # the engine's incremental objective agrees with the exact evaluation of its winner
-        if res.best.g > max(res.stats.g_sorted_start, res.stats.g_input_start):
+        if res.best.g > max(res.stats.g_sorted_start, res.stats.g_input_start, res.stats.g_deadline_start):
             assert abs(res.stats.engine_g - res.best.g) <= 1e-12 * res.best.g
 
 
@@ -384,6 +385,13 @@ def test_chains_attainment_at_least_reference(port):
         assert gpu.best.n >= ref_res["n"] or gpu.best.g >= ref_res["g"]
         wins += gpu.best.g > ref_res["g"]
     assert wins >= 3
+    # the bench configuration (configs[2]): 10 ms budget vs the reference's default single chain
+    w = S.generate_mixed(1024, 0)
+    ref_res = port.anneal(_flat(w), TABLE_COEFFS, w.ids(), 4, seed=0)
+    gpu = S.anneal(w, w.ids(), c, S.AnnealConfig(t0=500.0, tau=0.7, iter=60, chains=16384, budget_ms=9.5,
+                                                 scale_ladder=(1e4, 1e5, 1e6, 1e7, 1e8)), 4)
+    assert gpu.stats.kernel_ms < 10.0
+    assert gpu.best.n > ref_res["n"] and gpu.best.g > ref_res["g"]
 
 
 def test_chains_edge_cases():

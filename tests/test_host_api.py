@@ -152,3 +152,22 @@ def test_end_bits_layout():
     assert bits.shape == (2, 2)
     assert bits[0, 0] == (1 << 1) | (1 << 2) | (1 << 5)
     assert bits[1, 0] == 0xFFFFFFFF and bits[1, 1] == 0xFF
+
+
+def test_deadline_first_candidate():
+    """The chains' third start: a partition into batches <= mb whose leading batches were timed
+    with the exact tables (every request in them meets its SLO); on the bench workload it beats
+    the reference's sorted start (74 vs 65 SLOs)."""
+    c = S.table_coefficients()
+    for n, seed, mb in [(1, 0, 4), (7, 1, 2), (64, 2, 4), (256, 0, 4), (1024, 0, 4), (300, 3, 16)]:
+        w = S.generate_mixed(n, seed)
+        s = S.deadline_first_candidate(w, w.ids(), c, mb)
+        assert s.is_partition_of(w.ids(), mb)
+        ev = S.evaluate(s, c, w)
+        lead = ev.per_request[0]
+        assert ev.n == 0 or lead.slo_met  # the first kept request starts at 0 and was admitted
+    w = S.generate_mixed(1024, 0)
+    s_sorted, _ = S.initial_candidates(w, w.ids(), c, 4)
+    ev_dl = S.evaluate(S.deadline_first_candidate(w, w.ids(), c, 4), c, w)
+    ev_sorted = S.evaluate(s_sorted, c, w)
+    assert ev_dl.n >= 74 and ev_dl.n > ev_sorted.n and ev_dl.g > ev_sorted.g
