@@ -542,18 +542,24 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
 namespace {
 
 // Deadline-first candidate over dense indices (tables [mb][n] from cost_tables): perm + batch sizes.
-// Requests in ascending latest start at full batches; kept set in ascending (exec, index) order cut
+// Requests in ascending order of a due key (variant 0: latest start in a full batch, 1: latest
+// start alone, 2: latest completion in a full batch); kept set in ascending (exec, index) order cut
 // into batches of mb (a trailing partial batch uses its own size's tables); a request is kept when
 // every kept request still starts by its latest start, otherwise the longest kept one (the last)
 // is dropped (as in Moore-Hodgson; with batching this is a heuristic: the kept set need not stay
 // feasible, and the exact evaluation decides). O(n * kept).
+constexpr int kDeadlineVariants = 3;
+
 void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const std::vector<double>& deadline,
-                          std::vector<int>& perm, std::vector<int>& sizes) {
+                          int variant, std::vector<int>& perm, std::vector<int>& sizes) {
     const double* ef = exec.data() + (std::size_t)(mb - 1) * n;
     const double* df = deadline.data() + (std::size_t)(mb - 1) * n;
+    std::vector<double> due(n);
+    for (int i = 0; i < n; ++i)
+        due[i] = variant == 1 ? deadline[i] : (variant == 2 ? df[i] + ef[i] : df[i]);
     std::vector<int> order(n);
     for (int i = 0; i < n; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return df[a] < df[b]; });
+    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return due[a] < due[b]; });
     auto by_exec = [&](int a, int b) { return ef[a] != ef[b] ? ef[a] < ef[b] : a < b; };
     std::vector<int> kept;
     std::vector<double> start;  // start time of kept batch k (valid for batches before `dirty`)
@@ -580,7 +586,7 @@ void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const 
         return ok;
     };
     for (int i : order) {
-        if (!(df[i] >= 0.0)) continue;  // cannot start in time even first
+        if (!(df[i] >= 0.0)) continue;  // cannot start in time even first (in a full batch)
         const auto it = std::lower_bound(kept.begin(), kept.end(), i, by_exec);
         const int p = static_cast<int>(it - kept.begin());
         kept.insert(it, i);
@@ -616,6 +622,53 @@ Schedule schedule_of(const std::vector<int>& perm, const std::vector<int>& sizes
     return s;
 }
 
+// CostModel::score (P:src/priority_mapper.cpp:259-279) over the dense tables, the reference's
+// operand order (== evaluate().g bit-for-bit, as K1).
+double dense_score(int n, const std::vector<double>& exec, const std::vector<double>& deadline,
+                   const std::vector<int>& perm, const std::vector<int>& sizes) {
+    double elapsed = 0.0, total = 0.0;
+    int met = 0, pos = 0;
+    for (int sz : sizes) {
+        const double* e = exec.data() + (std::size_t)(sz - 1) * n;
+        const double* d = deadline.data() + (std::size_t)(sz - 1) * n;
+        double makespan = 0.0;
+        for (int j = 0; j < sz; ++j, ++pos) {
+            const int i = perm[pos];
+            const double e2e = elapsed + e[i];
+            total += e2e;
+            met += elapsed <= d[i];
+            makespan = std::max(makespan, e[i]);
+        }
+        elapsed += makespan;
+    }
+    return total > 0.0 ? static_cast<double>(met) / total : 0.0;
+}
+
+// All variants (one host thread each), scored exactly; the best by G (lowest variant on ties).
+void best_deadline_first(const Workload& w, const LatencyCoefficients& c, const std::vector<int>& sorted_ids, int mb,
+                         const std::vector<double>& exec, const std::vector<double>& deadline, std::vector<int>& perm,
+                         std::vector<int>& sizes, EvaluatedSchedule& ev) {
+    const int n = static_cast<int>(sorted_ids.size());
+    struct Cand {
+        std::vector<int> perm, sizes;
+        double g = 0.0;
+    };
+    std::vector<Cand> cand(kDeadlineVariants);
+    auto build = [&](int v) {
+        deadline_first_dense(n, mb, exec, deadline, v, cand[v].perm, cand[v].sizes);
+        cand[v].g = dense_score(n, exec, deadline, cand[v].perm, cand[v].sizes);
+    };
+    std::vector<std::future<void>> others;
+    for (int v = 1; v < kDeadlineVariants; ++v) others.push_back(std::async(std::launch::async, build, v));
+    build(0);
+    for (auto& f : others) f.get();
+    int best = 0;
+    for (int v = 1; v < kDeadlineVariants; ++v)
+        if (cand[v].g > cand[best].g) best = v;
+    perm = std::move(cand[best].perm), sizes = std::move(cand[best].sizes);
+    ev = evaluate(schedule_of(perm, sizes, sorted_ids), c, w);
+}
+
 }  // namespace
 
 Schedule deadline_first_candidate(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
@@ -625,8 +678,9 @@ Schedule deadline_first_candidate(const Workload& w, const std::vector<int>& ids
     cost_tables(w, ids, c, max_batch, exec, deadline);
     std::vector<int> sorted_ids = ids, perm, sizes;
     std::sort(sorted_ids.begin(), sorted_ids.end());
-    deadline_first_dense(static_cast<int>(ids.size()), max_batch, exec, deadline, perm, sizes);
-    return schedule_of(perm, sizes, sorted_ids);
+    EvaluatedSchedule ev;
+    best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, perm, sizes, ev);
+    return ev.schedule;
 }
 
 AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
@@ -646,8 +700,9 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     auto tables = std::async(std::launch::async, [&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
         if (want_dl) {
-            deadline_first_dense(n, max_batch, exec, deadline, dl_perm, dl_sizes);
-            ev_dl = evaluate(schedule_of(dl_perm, dl_sizes, sorted_ids), c, w);
+            EvaluatedSchedule ev;
+            best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, dl_perm, dl_sizes, ev);
+            ev_dl = std::move(ev);
         }
     });
     auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
