@@ -454,6 +454,12 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
 
             for (int it = 0; it < p.iter; ++it) {
+                // the device budget is checked every 8 proposals (warp-uniform), so a launch
+                // overruns it by at most ~8 proposal latencies; the chain is parked as usual
+                if (p.budget_ns > 0 && (it & 7) == 7 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
+                    stop = 1;
+                    break;
+                }
                 const uint32_t prop = (uint32_t)(lev * p.iter + it);
                 if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..5 and acceptance
                     __syncwarp();      // every lane is done reading the previous block
@@ -572,6 +578,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
                 rc->scan1 += sc1, rc->scan2 += sc2;
             }
+            if (stop) break;
         }
     }
 }

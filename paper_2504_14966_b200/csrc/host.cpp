@@ -697,8 +697,25 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     std::vector<int> dl_perm, dl_sizes;
     std::optional<EvaluatedSchedule> ev_dl;
     const bool want_dl = cfg.engine.mode == SearchMode::Chains && cfg.engine.deadline_start;
+    // the engine context is acquired and the tables uploaded on the same thread, as soon as they exist
+    const int device = resolve_device(cfg.engine.device);
+    CtxPtr ctx;
+    bool ctx_ok = false;  // ctx holds this problem and may go back to the pool
+    struct PoolReturn {
+        CtxPtr& c;
+        int dev;
+        const bool& ok;
+        ~PoolReturn() {
+            if (c && ok) CtxPool::get().release(dev, std::move(c));
+        }
+    } pool_return{ctx, device, ctx_ok};
     auto tables = std::async(std::launch::async, [&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
+        if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB) {
+            ctx = CtxPool::get().acquire(device);
+            engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
+            ctx_ok = true;
+        }
         if (want_dl) {
             EvaluatedSchedule ev;
             best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, dl_perm, dl_sizes, ev);
@@ -757,12 +774,11 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     prm.scale_mult = eo.scale_ladder.empty() ? nullptr : eo.scale_ladder.data();
     prm.max_blocks = eo.max_blocks;
 
-    const int device = resolve_device(eo.device);
-    CtxPtr ctx = CtxPool::get().acquire(device);
     std::vector<int> best_perm(n), best_sizes(n);
     int best_nb = 0;
     slo_chain_result cr{};
-    engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
+    if (!ctx) throw EngineError("B200 engine: no context for the problem");
+    ctx_ok = false;  // a failed launch destroys the context instead of pooling it
     engine_check(slo_anneal_chains(ctx.get(), &prm, start_perm.data(), start_sizes.data(),
                                    static_cast<int>(start_sizes.size()), best_perm.data(), best_sizes.data(), &best_nb,
                                    &cr));

@@ -417,5 +417,6 @@ def test_budget_stops_early():
     w = S.generate_mixed(1024, 0)
     r = S.anneal(w, w.ids(), c, S.AnnealConfig(chains=16384, budget_ms=2.0), 4)
     assert 0 < r.stats.proposals < 16384 * 63 * 100
+    assert r.stats.kernel_ms < 2.0 + 0.1  # the budget is checked every 8 proposals
     assert r.best.schedule.is_partition_of(w.ids(), 4)
     assert r.best.g >= max(r.stats.g_sorted_start, r.stats.g_input_start)
