@@ -71,6 +71,10 @@ int slo_ctx_sm_count(slo_ctx* ctx);
  * 1 <= n <= SLO_MAX_N, 1 <= mb <= SLO_MAX_MB. */
 int slo_problem_set(slo_ctx* ctx, int32_t n, int32_t mb, const double* exec, const double* deadline);
 
+/* The chain kernel (K3) scores schedules exactly in integer "ticks" of 2^-k ms: exec times rounded
+ * to that grid, deadlines compared on it. Returns the tick (ms) of the current problem, 0 if none. */
+double slo_problem_tick_ms(slo_ctx* ctx);
+
 /* Bit-exact objective of `count` candidate schedules. perms[c*n + p] = dense index at
  * position p; batch_end_bits[c*words + w] bit (p & 31) of word w = (p >> 5) set iff p is the
  * last position of its batch (words = ceil(n/32); bit n-1 must be set). Host buffers. */

@@ -68,6 +68,7 @@ _SIGNATURES = [
     ("slo_ctx_sync", c_int32, [c_void_p]),
     ("slo_ctx_sm_count", c_int32, [c_void_p]),
     ("slo_problem_set", c_int32, [c_void_p, c_int32, c_int32, _D, _D]),
+    ("slo_problem_tick_ms", c_double, [c_void_p]),
     ("slo_evaluate_batch", c_int32, [c_void_p, c_int32, POINTER(ctypes.c_uint16), POINTER(c_uint32), _I, _D, _D]),
     ("slo_anneal_chains", c_int32, [c_void_p, POINTER(SloChainParams), _I, _I, c_int32, _I, _I, _I,
                                     POINTER(SloChainResult)]),

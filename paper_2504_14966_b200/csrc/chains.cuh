@@ -1,50 +1,56 @@
-// K3: one annealing chain per warp (Philox4x32-10 moves, incremental objective).
+// K3: one annealing chain per warp (Philox4x32-10 moves) over a tick-exact incremental objective.
 // Included by engine.cu inside its anonymous namespace.
 //
+// Objective arithmetic. Exec times are rounded once to a power-of-two grid of 2^-k ms ("ticks",
+// k chosen per problem so every exec is < 2^27 ticks) and every sum is an integer: total latency
+// and elapsed times are int64 (bounded by n^2 * 2^27 < 2^51 at n = 4096), so the objective is an
+// exact function of the schedule, independent of summation order. That is what lets a move be
+// scored from the few positions it touches: the result is bit-identical to a full re-evaluation
+// (no drift, chains park and resume exactly). Deadlines compare exactly on the same grid:
+// elapsed_ms <= D  <=>  elapsed_ticks <= floor(D * 2^k). The returned schedule is always
+// re-scored by the exact reference arithmetic on the host (P:src/priority_mapper.cpp:404-410).
+//
 // Chain state (shared memory, per warp):
-//   ent[q]   u16, q = position: combined table index (batch_size-1) * n + dense_index, so the
-//            table gather needs no index arithmetic and every entry carries its batch size
-//   bits[w]  u32 linear batch-end bitmask (bit q set iff q is the last position of a batch)
+//   ent[q]   u16, q = position: combined table index (batch_size-1) * n + dense_index
+//   bits[w]  u32 batch-end bitmask (bit q set iff q is the last position of a batch)
 //   rnd      the Philox words of the next 32 proposals, drawn lane-parallel
-// Objective: the schedule is cut into units of 32 consecutive positions. Each unit has a
-// content-only summary (its batches' makespans, latency moments, deadline bound) computed
-// cooperatively by the 32 lanes. A warp-wide scan over the unit summaries gives every
-// unit's start time E and the makespan fmk of the batch open at its start; a unit's summed
-// latency is then closed-form (cnt*E + fmk*A + bs), and the SLO test walks only "live" units
-// (E <= an upper bound of the unit's deadlines) -- at N=1024 the first one or two. After a
-// move only the (<= 2) dirty units are re-summarised.
+// Per lane (registers): the anchors of its units of 32 positions -- E, the elapsed time at the
+// start of the batch holding the unit's first position; F, that batch's makespan; W, the unit's
+// met finite-deadline SLOs (kept while the unit is live, i.e. E <= the largest finite deadline).
+// Chain scalars: total latency (ticks) and A, the number of positions whose deadline is +inf
+// (met in every schedule). n_met = A + sum of W over live units.
+//
+// total = sum_q exec_q + sum_batches makespan_B * (positions after B)   (from e2e = elapsed + exec,
+// P:src/priority_mapper.cpp:266-276), so a move changes the total only through the batches it
+// rebuilds: a squeeze/delay rewrites two adjacent batches, a swap two batches. One warp pass over
+// those positions (REDUX max per batch, REDUX sum of execs) gives the new total and the elapsed
+// shift of every later batch; each lane then shifts its units' anchors, and only live units whose
+// anchors or contents changed are re-walked (at N=1024 the first one or two units).
 
-#define kNegInf (-static_cast<double>(INFINITY))
 #ifndef SLO_CHAIN_THREADS
-#define SLO_CHAIN_THREADS 768  // k_chains<1> block size: 24 warps, 80 registers per thread
+#define SLO_CHAIN_THREADS 768  // k_chains<1> block size (24 warps)
 #endif
 constexpr int kPreAttempts = 6;                      // move attempts drawn ahead (3 words each)
 constexpr int kRndWords = 3 * kPreAttempts + 2;      // + the acceptance uniform (2 words)
 static_assert(kRndWords % 4 == 0, "Philox block rows are stored as uint4");
-
-struct UnitSum {
-    double hm;    // max exec from the unit start through its first batch end (whole unit if none)
-    double tm;    // max exec after the unit's last batch end
-    double inner; // summed makespans of batches that start and end inside the unit
-    double bs;    // sum of exec over the unit + sum over inner batches of makespan * positions after it
-    float dmax;   // upper bound of the unit's deadlines (rounded up; -inf if none)
-    int fe;       // unit contains a batch end
-    int cnt;      // positions in the unit
-    int A;        // positions after the first batch end
-    int always;   // positions whose deadline is +inf (met in every schedule; excluded from dmax)
-};
+constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
+constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
+constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
 
 template <int UPL>
-struct __align__(16) ChainState {  // per-lane registers: this lane's unit summaries + SLO-walk cache
-    UnitSum s[UPL];
-    double wE[UPL], wF[UPL];
-    int wN[UPL];
+struct __align__(16) LaneState {  // this lane's unit anchors
+    long long E[UPL];  // elapsed (ticks) at the start of the batch holding the unit's first position
+    uint32_t F[UPL];   // makespan (ticks) of that batch
+    int W[UPL];        // met finite-deadline SLOs of the unit (valid while E <= dg)
 };
 
 struct ChainParams {
     int n, mb;
     uint64_t magic;      // floor(2^32 / n) + 1: (e * magic) >> 32 == e / n exactly for e < 65536
-    const double2* tab;  // global [mb][n] (exec, deadline)
+    const uint32_t* xt;  // global [mb][n] exec ticks | kAlways
+    const long long* dt; // global [mb][n] deadline ticks (-1: never met; unused where kAlways)
+    long long dg;        // largest finite deadline (ticks): units with E > dg are dead
+    double tick;         // 2^-k ms
     int smem_tab;
     double t0, tau, scale;
     int iter, levels;
@@ -55,127 +61,72 @@ struct ChainParams {
     long long budget_ns;
     const uint16_t* start_ent;   // [1024*UPL]
     const uint32_t* start_bits;  // [32*UPL]
-    const void* start_sum;       // ChainState<UPL>[32]: the start state's summaries (k_start)
-    const double* start_obj;     // {f, total, n_met} of the start state (k_start)
+    void* start_lane;            // LaneState<UPL>[32]: the start state's anchors (k_start)
+    long long* start_obj;        // {total ticks, A, n_met} of the start state (k_start)
     uint16_t* st_ent;            // [chain_count][1024*UPL]  parked chains (several chains per warp)
     uint32_t* st_bits;           // [chain_count][32*UPL]
-    void* st_sum;                // [chain_count][32] ChainState<UPL>
+    void* st_lane;               // [chain_count][32] LaneState<UPL>
     uint16_t* best_ent;          // [chain_count][1024*UPL]
     uint32_t* best_bits;         // [chain_count][32*UPL]
     ChainRec* rec;
 };
 
-// The (exec, deadline) table: staged in shared memory (s = its 32-bit shared address) or read
-// from global memory (g). A compile-time choice, so the gather is an LDS.128 / LDG.128 rather
-// than a generic load.
+// The exec-tick table: staged in shared memory (s = its 32-bit shared address) or read from
+// global memory (g). A compile-time choice, so the gather is an LDS rather than a generic load.
 struct TabRef {
-    const double2* g;
+    const uint32_t* g;
     uint32_t s;
 };
 
 template <bool SMEM>
-__device__ __forceinline__ double2 tab_ld(const TabRef& t, uint32_t i) {
+__device__ __forceinline__ uint32_t xt_ld(const TabRef& t, uint32_t i) {
     if constexpr (SMEM) {
-        double2 v;
-        asm("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(t.s + i * 16u));
+        uint32_t v;
+        asm("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(t.s + i * 4u));
         return v;
     } else {
         return __ldg(t.g + i);
     }
 }
 
-__device__ __forceinline__ double warp_sum(double v) {
-#pragma unroll
-    for (int d = 16; d; d >>= 1) v += __shfl_xor_sync(FULL, v, d);
-    return v;
-}
-
-// order-preserving map float -> u32 (for REDUX max)
-__device__ __forceinline__ uint32_t f2key(float f) {
-    const uint32_t b = __float_as_uint(f);
-    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-}
-__device__ __forceinline__ float key2f(uint32_t k) {
-    return __uint_as_float((k & 0x80000000u) ? (k & 0x7fffffffu) : ~k);
-}
-
 // segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
-// (and at the unit start) and are at most mb long, so log2(mb) shuffle steps suffice. The
-// segment start comes from the bitmask, so only the value is shuffled.
-__device__ __forceinline__ double seg_max(double e, uint32_t w, int lane, int mb) {
-    double m = dmax(e, 0.0);  // makespans start at 0 (reference P:src/priority_mapper.cpp:266)
+// (and at the unit start) and are at most mb long, so log2(mb) shuffle steps suffice
+__device__ __forceinline__ uint32_t seg_max(uint32_t x, uint32_t w, int lane, int mb) {
+    uint32_t m = x;
     const uint32_t below = w & ((1u << lane) - 1u);
     const int span = lane - (below ? 32 - __clz(below) : 0);  // positions before lane in its segment
     for (int d = 1; d < mb; d <<= 1) {
-        const double mu = __shfl_up_sync(FULL, m, d);
-        if (d <= span) m = dmax(m, mu);
+        const uint32_t mu = __shfl_up_sync(FULL, m, d);
+        if (d <= span) m = max(m, mu);
     }
     return m;
 }
 
-// cooperative summary of unit u (all 32 lanes; every lane receives the result)
+// Cooperative count of the met finite-deadline SLOs of unit u, whose first batch started at
+// elapsed E with makespan F. Rare (live units whose inputs changed): kept out of line.
 template <bool SMEM>
-__device__ __forceinline__ UnitSum unit_summary(const uint16_t* ent, const uint32_t* bits, const TabRef& tab, int n,
-                                                int mb, int u, int lane) {
-    UnitSum s;
-    const int q0 = u << 5;
-    const int cnt = min(32, n - q0);
+__device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
+                                      int n, int mb, int u, int lane, long long E, uint32_t F) {
+    const int q = (u << 5) + lane;
     const uint32_t w = bits[u];
-    double e = 0.0, D = kNegInf;
-    if (lane < cnt) {
-        const double2 v = tab_ld<SMEM>(tab, ent[q0 + lane]);
-        e = v.x, D = v.y;
+    uint32_t x = 0;
+    long long D = -1;
+    if (q < n) {
+        const uint32_t e = ent[q];
+        const uint32_t v = xt_ld<SMEM>(tab, e);
+        x = v & kTickMask;
+        if (!(v & kAlways)) D = __ldg(dt + e);  // +inf deadlines are counted in A, not here
     }
-    const double m = seg_max(e, w, lane, mb);
-    const int f = w ? __ffs(w) - 1 : -1;
-    const int la = w ? 31 - __clz(w) : -1;
-    const double m_last = __shfl_sync(FULL, m, cnt - 1);
-    const double m_first = __shfl_sync(FULL, m, f < 0 ? cnt - 1 : f);
-    const bool inner_end = ((w >> lane) & 1u) && lane != f;
-    const double mk = inner_end ? m : 0.0;
-    double inner = mk, bs = e + mk * (double)(cnt - 1 - lane);
+    const uint32_t m = seg_max(x, w, lane, mb);
+    const int f = w ? __ffs(w) - 1 : 32;
+    const uint32_t v = ((w >> lane) & 1u) ? (lane == f ? F : m) : 0u;
+    uint32_t s = v;  // closed makespans of the unit: < 32 * 2^27, no overflow
 #pragma unroll
-    for (int d = 16; d; d >>= 1) {  // two interleaved butterfly reductions
-        inner += __shfl_xor_sync(FULL, inner, d);
-        bs += __shfl_xor_sync(FULL, bs, d);
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t up = __shfl_up_sync(FULL, s, d);
+        if (lane >= d) s += up;
     }
-    s.fe = w != 0;
-    s.cnt = cnt;
-    s.A = w ? cnt - 1 - f : 0;
-    s.hm = m_first;
-    s.tm = (w == 0 || la < cnt - 1) ? m_last : 0.0;
-    s.inner = inner;
-    s.bs = bs;
-    const bool inf = D == INFINITY;  // host marks deadlines no schedule can miss as +inf
-    s.always = __popc(__ballot_sync(FULL, inf));
-    s.dmax = key2f(__reduce_max_sync(FULL, f2key(__double2float_ru(inf ? kNegInf : D))));
-    return s;
-}
-
-// cooperative SLO count of unit u whose first position starts at elapsed E, the batch open at
-// the unit start having makespan fmk. Rare (live units whose inputs changed): kept out of line.
-template <bool SMEM>
-__device__ __noinline__ int unit_met(const uint16_t* ent, const uint32_t* bits, TabRef tab, int n, int mb, int u,
-                                     int lane, double E, double fmk) {
-    const int q0 = u << 5;
-    const int cnt = min(32, n - q0);
-    const uint32_t w = bits[u];
-    double e = 0.0, D = kNegInf;
-    if (lane < cnt) {
-        const double2 v = tab_ld<SMEM>(tab, ent[q0 + lane]);
-        e = v.x, D = v.y;
-    }
-    const double m = seg_max(e, w, lane, mb);
-    const int f = w ? __ffs(w) - 1 : -1;
-    double v = ((w >> lane) & 1u) ? (lane == f ? fmk : m) : 0.0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // inclusive prefix of closed makespans
-        const double up = __shfl_up_sync(FULL, v, d);
-        if (lane >= d) v += up;
-    }
-    double off = __shfl_up_sync(FULL, v, 1);
-    if (lane == 0) off = 0.0;
-    const bool met = lane < cnt && E + off <= D;
+    const bool met = q < n && E + (long long)(s - v) <= D;
     return __popc(__ballot_sync(FULL, met));
 }
 
@@ -198,9 +149,8 @@ struct Move {
 // bitmask representation: batch sizes come from the entries, batch starts from one bit search.
 // Attempts < kPreAttempts read the lane-parallel Philox block; later retries draw directly.
 // Counter = (proposal, chain, attempt, tag): results do not depend on the launch geometry.
-__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint32_t nn,
-                                          uint64_t magic, uint32_t prop, uint32_t cid, uint32_t k0, uint32_t k1,
-                                          const uint32_t* rw) {
+__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint64_t magic,
+                                          uint32_t prop, uint32_t cid, uint32_t k0, uint32_t k1, const uint32_t* rw) {
     auto size_at = [&](int q) { return (int)(((uint64_t)ent[q] * magic) >> 32) + 1; };
     Move mv;
     mv.kind = 0;
@@ -262,95 +212,15 @@ __device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* b
     return mv;
 }
 
-// Warp-wide scan over unit summaries: E[k] (start elapsed) and fmk[k] for this lane's units.
-// Batches hold at most 16 positions, so every non-empty unit of 32 contains a batch end (the
-// last, partial unit ends at position n-1): the batch open at a unit's start is exactly the
-// previous unit's tail, and only the elapsed times need a scan.
-template <int UPL>
-__device__ __forceinline__ void combine_units(const ChainState<UPL>& cs, int lane, double (&E)[UPL],
-                                              double (&fmk)[UPL]) {
-    double rest = cs.s[0].inner;
-#pragma unroll
-    for (int k = 1; k < UPL; ++k) rest = rest + dmax(cs.s[k - 1].tm, cs.s[k].hm), rest = rest + cs.s[k].inner;
-    double carry = __shfl_up_sync(FULL, cs.s[UPL - 1].tm, 1);
-    if (lane == 0) carry = 0.0;
-    double S = cs.s[0].fe ? dmax(carry, cs.s[0].hm) + rest : 0.0;
-#pragma unroll
-    for (int d = 1; d < 32; d <<= 1) {  // sum scan of the makespans closed in each lane
-        const double v = __shfl_up_sync(FULL, S, d);
-        if (lane >= d) S += v;
-    }
-    double el = __shfl_up_sync(FULL, S, 1);
-    if (lane == 0) el = 0.0;
-    double cm = carry;
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) {
-        const UnitSum& s = cs.s[k];
-        E[k] = el;
-        fmk[k] = dmax(cm, s.hm);
-        el = el + fmk[k], el = el + s.inner, cm = s.tm;
-    }
-}
-
 // objective G = n / t (reference :278); the reciprocal form is used identically everywhere
 __device__ __forceinline__ double objective(int nm, double tot) {
     return tot > 0.0 ? (double)nm * __drcp_rn(tot) : 0.0;
 }
 
-// Objective of the current state. full: re-summarise every unit and re-walk every live unit;
-// otherwise only units du0/du1 (-1 = none). Outputs the total latency, the SLO count and the
-// per-unit (E, fmk, walk result) to commit when the state is accepted.
-template <int UPL, bool SMEM>
-__device__ __forceinline__ void evaluate_chain(ChainState<UPL>& cs, const uint16_t* ent, const uint32_t* bits,
-                                               const TabRef& tab, int n, int mb, int lane, bool full, int du0,
-                                               int du1, double& tot_out, int& nm_out, double (&E)[UPL],
-                                               double (&fmk)[UPL], int (&nN)[UPL], unsigned long long& sc1,
-                                               unsigned long long& sc2) {
-    const int U = (n + 31) >> 5;
-    const int todo = full ? 32 * UPL : (du0 < 0 ? 0 : (du1 >= 0 && du1 != du0 ? 2 : 1));
-    for (int i = 0; i < todo; ++i) {  // one inlined copy of the unit summary
-        const int u = full ? i : (i == 0 ? du0 : du1);
-        UnitSum v{0.0, 0.0, 0.0, 0.0, -INFINITY, 0, 0, 0, 0};
-        if (u < U) v = unit_summary<SMEM>(ent, bits, tab, n, mb, u, lane), sc1 += lane == 0 ? 32 : 0;
-        if (lane == u / UPL) {
-#pragma unroll
-            for (int k = 0; k < UPL; ++k)
-                if (k == u % UPL) cs.s[k] = v;
-        }
-    }
-    combine_units<UPL>(cs, lane, E, fmk);
-    double tot = 0.0;
-    int nm = 0;
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) {
-        const UnitSum& s = cs.s[k];
-        const int u = lane * UPL + k;
-        // summed latency of the unit's positions, closed form
-        tot += (double)s.cnt * E[k] + (s.fe ? fmk[k] * (double)s.A : 0.0) + s.bs;
-        const bool live = E[k] <= (double)s.dmax;
-        const bool dirty = full || u == du0 || u == du1;
-        const bool need = live && (dirty || E[k] != cs.wE[k] || fmk[k] != cs.wF[k]);
-        nN[k] = live ? cs.wN[k] : s.always;
-        unsigned mask = __ballot_sync(FULL, need);
-        while (mask) {  // cooperative SLO walks of the units that need one
-            const int ln = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const double Eu = __shfl_sync(FULL, E[k], ln);
-            const double Fu = __shfl_sync(FULL, fmk[k], ln);
-            const int cntm = unit_met<SMEM>(ent, bits, tab, n, mb, ln * UPL + k, lane, Eu, Fu);
-            if (lane == ln) nN[k] = cntm;
-            sc2 += lane == 0 ? 32 : 0;
-        }
-        nm += nN[k];
-    }
-    tot_out = warp_sum(tot);
-    nm_out = __reduce_add_sync(FULL, nm);
-}
-
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
-    // entries + bitmask + two parked unit summaries + Philox block (32 proposals)
-    return 1024 * UPL * 2 + 32 * UPL * 4 + 2 * (int)sizeof(UnitSum) + 32 * kRndWords * 4;
+    // entries + bitmask + Philox block (32 proposals)
+    return 1024 * UPL * 2 + 32 * UPL * 4 + 32 * kRndWords * 4;
 }
 
 template <int UPL>
@@ -361,32 +231,114 @@ __device__ __forceinline__ void copy_state(uint16_t* de, uint32_t* db, const uin
     for (int i = lane; i < kBits; i += 32) db[i] = sb[i];
 }
 
-// Prologue: one warp evaluates the start schedule shared by every chain and publishes its
-// unit summaries, so the chains start without a full evaluation each.
+// Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts.
+template <int UPL, bool SMEM>
+__device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UPL>& ls, const uint16_t* ent,
+                                           const uint32_t* bits, const TabRef& tab, const long long* dt, int n,
+                                           int mb, int lane, unsigned long long& sc2) {
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) {
+        unsigned mask = __ballot_sync(FULL, need[k]);
+        while (mask) {
+            const int ln = __ffs(mask) - 1;
+            mask &= mask - 1;
+            const long long Eu = __shfl_sync(FULL, ls.E[k], ln);
+            const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
+            const int cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, ln * UPL + k, lane, Eu, Fu);
+            if (lane == ln) ls.W[k] = cnt;
+            sc2 += lane == 0 ? 32 : 0;
+        }
+    }
+}
+
+template <int UPL>
+__device__ __forceinline__ int live_met(const LaneState<UPL>& ls, long long dg) {
+    int s = 0;
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) s += ls.E[k] <= dg ? ls.W[k] : 0;
+    return (int)__reduce_add_sync(FULL, (unsigned)s);
+}
+
+// Prologue: one warp evaluates the start schedule shared by every chain and publishes its unit
+// anchors, so the chains start without a full evaluation each.
 template <int UPL>
 __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kU = 32 * UPL;
     const int lane = threadIdx.x;
-    uint16_t* ent = reinterpret_cast<uint16_t*>(smem);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + 1024 * UPL * 2);
+    const int n = p.n;
+    long long* Es = reinterpret_cast<long long*>(smem);
+    uint32_t* Fs = reinterpret_cast<uint32_t*>(smem + kU * 8);
+    uint16_t* ent = reinterpret_cast<uint16_t*>(smem + kU * 12);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + kU * 12 + 1024 * UPL * 2);
     copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
+    for (int u = lane; u < kU; u += 32) Es[u] = kPadE, Fs[u] = 0;
     __syncwarp();
-    ChainState<UPL> cs;
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) cs.wE[k] = 0.0, cs.wF[k] = 0.0, cs.wN[k] = 0;
-    double tot, E[UPL], fmk[UPL];
-    int nm, nN[UPL];
-    unsigned long long sc1 = 0, sc2 = 0;
-    const TabRef tab{p.tab, 0u};
-    evaluate_chain<UPL, false>(cs, ent, bits, tab, p.n, p.mb, lane, true, -1, -1, tot, nm, E, fmk, nN, sc1, sc2);
-#pragma unroll
-    for (int k = 0; k < UPL; ++k) cs.wE[k] = E[k], cs.wF[k] = fmk[k], cs.wN[k] = nN[k];
-    reinterpret_cast<ChainState<UPL>*>(const_cast<void*>(p.start_sum))[lane] = cs;
-    if (lane == 0) {
-        double* o = const_cast<double*>(p.start_obj);
-        o[0] = objective(nm, tot), o[1] = tot, o[2] = (double)nm;
+    // each lane owns positions [q0, q1) (its UPL units); every non-empty range holds a batch end
+    // (ranges are >= 32 long, batches <= 16), so the batch open at a range start is closed in it
+    const int q0 = lane * 32 * UPL, q1 = min(n, q0 + 32 * UPL);
+    uint32_t hm = 0, tm = 0;  // max exec through the first end; after the last end
+    long long inner = 0;      // makespans of the batches that start after the first end
+    bool seen = false;
+    for (int q = q0; q < q1; ++q) {
+        const uint32_t x = __ldg(p.xt + ent[q]) & kTickMask;
+        if (!seen) hm = max(hm, x);
+        else tm = max(tm, x);
+        if ((bits[q >> 5] >> (q & 31)) & 1u) {
+            if (seen) inner += tm;
+            seen = true, tm = 0;
+        }
     }
+    uint32_t tprev = __shfl_up_sync(FULL, tm, 1);
+    if (lane == 0) tprev = 0;
+    const long long S = q0 < q1 ? (long long)max(tprev, hm) + inner : 0ll;
+    long long E = S;  // exclusive scan: elapsed at the start of the batch open at q0
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const long long up = __shfl_up_sync(FULL, E, d);
+        if (lane >= d) E += up;
+    }
+    E -= S;
+    long long tot = 0;
+    int A = 0, pend = -1;
+    uint32_t mk = tprev;
+    for (int q = q0; q < q1; ++q) {
+        if ((q & 31) == 0) Es[q >> 5] = E, pend = q >> 5;
+        const uint32_t v = __ldg(p.xt + ent[q]);
+        const uint32_t x = v & kTickMask;
+        A += v >> 31;
+        tot += E + x;
+        mk = max(mk, x);
+        if ((bits[q >> 5] >> (q & 31)) & 1u) {
+            if (pend >= 0) Fs[pend] = mk, pend = -1;
+            E += mk, mk = 0;
+        }
+    }
+#pragma unroll
+    for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(FULL, tot, d);
+    A = (int)__reduce_add_sync(FULL, (unsigned)A);
+    if (lane == 0) p.start_obj[0] = tot, p.start_obj[1] = A;
+    __syncwarp();
+    LaneState<UPL> ls;
+    bool need[UPL];
+#pragma unroll
+    for (int k = 0; k < UPL; ++k) {
+        ls.E[k] = Es[lane * UPL + k], ls.F[k] = Fs[lane * UPL + k], ls.W[k] = 0;
+        need[k] = ls.E[k] <= p.dg;
+    }
+    unsigned long long sc2 = 0;
+    const TabRef tab{p.xt, 0u};
+    walk_units<UPL, false>(need, ls, ent, bits, tab, p.dt, n, p.mb, lane, sc2);
+    const int nm = live_met<UPL>(ls, p.dg);
+    reinterpret_cast<LaneState<UPL>*>(p.start_lane)[lane] = ls;
+    if (lane == 0) p.start_obj[2] = p.start_obj[1] + nm;
 }
+
+// one proposal's effect on the objective, computed by the warp from the rebuilt batches
+struct Delta {
+    long long dtot;  // change of the total latency (ticks)
+    int dA;          // change of the +inf-deadline count
+};
 
 template <int UPL, bool SMEM>
 __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chains(const ChainParams p) {
@@ -394,22 +346,23 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = p.n, mb = p.mb;
 
-    TabRef tab{p.tab, 0u};
+    TabRef tab{p.xt, 0u};
     size_t off = 0;
-    if constexpr (SMEM) {  // stage the (exec, deadline) table once per block: coalesced 16 B loads
-        double2* st = reinterpret_cast<double2*>(smem);
+    if constexpr (SMEM) {  // stage the exec-tick table once per block: coalesced 16 B loads
         const int total = mb * n;
-        for (int i = threadIdx.x; i < total; i += blockDim.x) st[i] = p.tab[i];
+        uint32_t* st = reinterpret_cast<uint32_t*>(smem);
+        const int v4 = total >> 2;
+        for (int i = threadIdx.x; i < v4; i += blockDim.x) reinterpret_cast<uint4*>(st)[i] = reinterpret_cast<const uint4*>(p.xt)[i];
+        for (int i = (v4 << 2) + threadIdx.x; i < total; i += blockDim.x) st[i] = p.xt[i];
         __syncthreads();
         tab.s = (uint32_t)__cvta_generic_to_shared(st);
-        off = ((size_t)total * sizeof(double2) + 15) & ~(size_t)15;
+        off = ((size_t)total * sizeof(uint32_t) + 15) & ~(size_t)15;
     }
     constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
     unsigned char* slot = smem + off + (size_t)wid * slot_bytes<UPL>();
     uint16_t* ent = reinterpret_cast<uint16_t*>(slot);
     uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2);
-    UnitSum* saved = reinterpret_cast<UnitSum*>(slot + kEnt * 2 + kBits * 4);
-    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + kBits * 4 + 2 * sizeof(UnitSum));
+    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + kBits * 4);
 
     const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
     if (gw >= p.chain_count) return;
@@ -418,13 +371,16 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
     uint64_t deadline = ~0ull;
     if (p.budget_ns > 0) deadline = __shfl_sync(FULL, gtimer(), 0) + (uint64_t)p.budget_ns;
 
-    ChainState<UPL> cs;
+    LaneState<UPL> cur;  // committed anchors
+    long long tot = 0;   // committed total (ticks)
+    int A = 0, nm_cur = 0;
     double f = 0.0, best_f = 0.0;
     unsigned long long props = 0, accs = 0;
     int stop = 0;
     const uint32_t nn = (uint32_t)n;
     const uint64_t magic = p.magic;
-    auto* parked = reinterpret_cast<ChainState<UPL>*>(p.st_sum);
+    const long long dg = p.dg;
+    auto* parked = reinterpret_cast<LaneState<UPL>*>(p.st_lane);
 
     double t = p.t0;
     for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
@@ -440,14 +396,16 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
             unsigned long long sc1 = 0, sc2 = 0;
             if (lev == 0) {  // every chain starts from the shared start state
                 copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
-                cs = reinterpret_cast<const ChainState<UPL>*>(p.start_sum)[lane];
-                f = best_f = p.start_obj[0], props = 0, accs = 0;
+                cur = reinterpret_cast<const LaneState<UPL>*>(p.start_lane)[lane];
+                tot = p.start_obj[0], A = (int)p.start_obj[1], nm_cur = (int)p.start_obj[2];
+                f = best_f = objective(nm_cur, (double)tot * p.tick), props = 0, accs = 0;
                 __syncwarp();
                 copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits, lane);
-                if (lane == 0) rc->g = f, rc->t = p.start_obj[1], rc->n_met = (int)p.start_obj[2];
+                if (lane == 0) rc->g = f, rc->t = (double)tot * p.tick, rc->n_met = nm_cur;
             } else if (n_my > 1) {  // resume a parked chain
                 copy_state<UPL>(ent, bits, p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, lane);
-                cs = parked[(size_t)c * 32 + lane];
+                cur = parked[(size_t)c * 32 + lane];
+                tot = rc->cur_tot, A = rc->cur_A, nm_cur = rc->cur_n;
                 f = rc->cur_f, best_f = rc->g, props = rc->proposals, accs = rc->accepted;
                 __syncwarp();
             }
@@ -480,14 +438,20 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     __syncwarp();
                 }
                 const uint32_t* rw = rnd + kRndWords * (it & 31);
-                const Move mv = draw_move(ent, bits, n, mb, nn, magic, prop, cid, p.key0, p.key1, rw);
+                const Move mv = draw_move(ent, bits, n, mb, magic, prop, cid, p.key0, p.key1, rw);
 
-                // ---- apply in place (undo on reject)
+                // ---- apply in place (undo on reject) and score from the rebuilt batches
+                LaneState<UPL> nx = cur;
+                bool need[UPL];
+                long long dtot = 0;
+                int dA = 0;
                 int q = 0;
                 uint16_t old_q = 0;
                 uint32_t ow0 = 0, ow1 = 0;
-                int w0 = 0, w1 = 0, du0 = -1, du1 = -1;
+                int w0 = 0, w1 = 0;
                 if (mv.kind == 1) {
+                    // squeeze / delay: [lo, hi] held old batches [lo, osp], (osp, hi] and holds
+                    // new batches [lo, nsp], (nsp, hi] (either part may be empty)
                     q = mv.lo + lane;
                     const bool act = q <= mv.hi;
                     uint16_t nw = 0;
@@ -510,29 +474,98 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                         if (mv.clr >= 0) bits[mv.clr >> 5] &= ~(1u << (mv.clr & 31));
                         if (mv.set >= 0) bits[mv.set >> 5] |= 1u << (mv.set & 31);
                     }
-                    __syncwarp();
-                    du0 = mv.lo >> 5, du1 = mv.hi >> 5;
-                } else if (mv.kind == 2) {
-                    const uint32_t ea = ent[mv.a], eb = ent[mv.b];
-                    ow0 = ea, ow1 = eb;
-                    const uint32_t ba = (uint32_t)(((uint64_t)ea * magic) >> 32) * nn;
-                    const uint32_t bb = (uint32_t)(((uint64_t)eb * magic) >> 32) * nn;
-                    __syncwarp();
-                    if (lane == 0) ent[mv.a] = (uint16_t)(ba + (eb - bb)), ent[mv.b] = (uint16_t)(bb + (ea - ba));
-                    __syncwarp();
-                    du0 = mv.a >> 5, du1 = mv.b >> 5;
-                }
-                // owners park the summaries of the dirty units (restored on reject)
+                    const int lo = mv.lo, hi = mv.hi;
+                    const int osp = mv.clr >= 0 ? mv.clr : hi, nsp = mv.split;
+                    const uint32_t vo = act ? xt_ld<SMEM>(tab, old_q) : 0u;
+                    const uint32_t vn = act ? xt_ld<SMEM>(tab, nw) : 0u;
+                    const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
+                    const uint32_t mO0 = __reduce_max_sync(FULL, q <= osp ? xo : 0u);
+                    const uint32_t mO1 = __reduce_max_sync(FULL, q > osp ? xo : 0u);
+                    const uint32_t mN0 = __reduce_max_sync(FULL, q <= nsp ? xn : 0u);
+                    const uint32_t mN1 = __reduce_max_sync(FULL, q > nsp ? xn : 0u);
+                    const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
+                    dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
+                    const long long after_hi = n - 1 - hi;
+                    long long oc, nc, omk, nmk;
+                    if (osp < hi) oc = (long long)mO0 * (n - 1 - osp) + (long long)mO1 * after_hi, omk = (long long)mO0 + mO1;
+                    else oc = (long long)mO0 * after_hi, omk = mO0;
+                    if (nsp < lo) nc = (long long)mN1 * after_hi, nmk = mN1;
+                    else if (nsp < hi) nc = (long long)mN0 * (n - 1 - nsp) + (long long)mN1 * after_hi, nmk = (long long)mN0 + mN1;
+                    else nc = (long long)mN0 * after_hi, nmk = mN0;
+                    dtot = sN - sO + nc - oc;
+                    const long long delta = nmk - omk;
 #pragma unroll
-                for (int kk = 0; kk < UPL; ++kk) {
-                    if (du0 >= 0 && lane == du0 / UPL && kk == du0 % UPL) saved[0] = cs.s[kk];
-                    if (du1 >= 0 && du1 != du0 && lane == du1 / UPL && kk == du1 % UPL) saved[1] = cs.s[kk];
+                    for (int kk = 0; kk < UPL; ++kk) {
+                        const int pu = (lane * UPL + kk) << 5;
+                        if (pu > hi) {
+                            nx.E[kk] += delta;
+                        } else if (pu >= lo) {
+                            const long long Eb = nx.E[kk] - ((osp < hi && pu > osp) ? (long long)mO0 : 0ll);
+                            nx.E[kk] = Eb + ((nsp >= lo && pu > nsp) ? (long long)mN0 : 0ll);
+                            nx.F[kk] = pu > nsp ? mN1 : mN0;
+                        }
+                        need[kk] = pu + 31 >= lo && (pu <= hi || delta != 0) && nx.E[kk] <= dg;
+                    }
+                    sc1 += lane == 0 ? (unsigned long long)(hi - lo + 1) : 0ull;
+                    __syncwarp();
+                } else if (mv.kind == 2) {
+                    // swap: batches [sa, ea] and [sb, eb] (sa < sb, or the same batch) keep their
+                    // sizes; lanes 0-15 cover the first, 16-31 the second
+                    const int pa = min(mv.a, mv.b), pb = max(mv.a, mv.b);
+                    const uint32_t ea_ = ent[pa], eb_ = ent[pb];
+                    ow0 = ea_, ow1 = eb_;
+                    const uint32_t za = (uint32_t)(((uint64_t)ea_ * magic) >> 32);  // batch size - 1
+                    const uint32_t zb = (uint32_t)(((uint64_t)eb_ * magic) >> 32);
+                    const uint32_t ba = za * nn, bb = zb * nn;
+                    const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
+                    const int sa = prev_end(bits, pa) + 1, sb = prev_end(bits, pb) + 1;
+                    const int ea = sa + (int)za, eb = sb + (int)zb;
+                    const bool first = lane < 16;
+                    q = first ? sa + lane : sb + lane - 16;
+                    const bool act = q <= (first ? ea : eb);
+                    uint32_t eo = 0, en = 0;
+                    if (act) {
+                        eo = ent[q];
+                        en = q == pa ? na : (q == pb ? nb : eo);
+                    }
+                    __syncwarp();
+                    if (lane == 0) ent[pa] = (uint16_t)na, ent[pb] = (uint16_t)nb;
+                    const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
+                    const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
+                    const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
+                    const uint32_t mO0 = __reduce_max_sync(FULL, first ? xo : 0u);
+                    const uint32_t mO1 = __reduce_max_sync(FULL, first ? 0u : xo);
+                    const uint32_t mN0 = __reduce_max_sync(FULL, first ? xn : 0u);
+                    const uint32_t mN1 = __reduce_max_sync(FULL, first ? 0u : xn);
+                    const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
+                    dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
+                    const long long da = (long long)mN0 - mO0, db = (long long)mN1 - mO1;
+                    dtot = sN - sO + da * (n - 1 - ea) + db * (n - 1 - eb);
+                    if (sa == sb) dtot = 0, dA = 0;  // one batch: order inside a batch changes nothing
+#pragma unroll
+                    for (int kk = 0; kk < UPL; ++kk) {
+                        const int pu = (lane * UPL + kk) << 5;
+                        if (pu > eb) nx.E[kk] += da + db;
+                        else if (pu >= sb) nx.E[kk] += da, nx.F[kk] = mN1;
+                        else if (pu > ea) nx.E[kk] += da;
+                        else if (pu >= sa) nx.F[kk] = mN0;
+                        // contents (the units of pa, pb) or anchors (F of a rebuilt batch, E after it) changed
+                        const int u = lane * UPL + kk;
+                        const bool chg = u == (pa >> 5) || u == (pb >> 5) || (pu >= sa && da != 0) || (pu >= sb && db != 0);
+                        need[kk] = chg && nx.E[kk] <= dg;
+                    }
+                    sc1 += lane == 0 ? (unsigned long long)(ea - sa + eb - sb + 2) : 0ull;
+                    __syncwarp();
+                } else {
+#pragma unroll
+                    for (int kk = 0; kk < UPL; ++kk) need[kk] = false;
                 }
-                double tot, E[UPL], fmk[UPL];
-                int nm, nN[UPL];
-                evaluate_chain<UPL, SMEM>(cs, ent, bits, tab, n, mb, lane, false, du0, du1, tot, nm, E, fmk, nN, sc1,
-                                          sc2);
-                const double f_new = objective(nm, tot);
+                walk_units<UPL, SMEM>(need, nx, ent, bits, tab, p.dt, n, mb, lane, sc2);
+                const long long tot_new = tot + dtot;
+                const int A_new = A + dA;
+                const int nm = A_new + live_met<UPL>(nx, dg);
+                const double t_new = (double)tot_new * p.tick;
+                const double f_new = objective(nm, t_new);
                 ++props;
                 bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
                 if (!accept) {
@@ -545,37 +578,32 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 }
                 if (accept) {
                     ++accs;
-#pragma unroll
-                    for (int kk = 0; kk < UPL; ++kk) cs.wE[kk] = E[kk], cs.wF[kk] = fmk[kk], cs.wN[kk] = nN[kk];
+                    cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
                     if (f > best_f) {
                         best_f = f;
                         copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,
                                         lane);
-                        if (lane == 0) rc->g = f, rc->t = tot, rc->n_met = nm;
+                        if (lane == 0) rc->g = f, rc->t = t_new, rc->n_met = nm;
                     }
                 } else {
                     if (mv.kind == 1) {
                         if (q <= mv.hi) ent[q] = old_q;
                         if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
                     } else if (mv.kind == 2) {
-                        if (lane == 0) ent[mv.a] = (uint16_t)ow0, ent[mv.b] = (uint16_t)ow1;
-                    }
-#pragma unroll
-                    for (int kk = 0; kk < UPL; ++kk) {
-                        if (du0 >= 0 && lane == du0 / UPL && kk == du0 % UPL) cs.s[kk] = saved[0];
-                        if (du1 >= 0 && du1 != du0 && lane == du1 / UPL && kk == du1 % UPL) cs.s[kk] = saved[1];
+                        if (lane == 0) ent[min(mv.a, mv.b)] = (uint16_t)ow0, ent[max(mv.a, mv.b)] = (uint16_t)ow1;
                     }
                     __syncwarp();
                 }
             }
-            if (n_my > 1) {  // park the chain (state + summaries) until the next level
+            if (n_my > 1) {  // park the chain (state + anchors) until the next level
                 copy_state<UPL>(p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, ent, bits, lane);
-                parked[(size_t)c * 32 + lane] = cs;
+                parked[(size_t)c * 32 + lane] = cur;
                 __syncwarp();
             }
             if (lane == 0) {
                 rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
+                rc->cur_tot = tot, rc->cur_A = A, rc->cur_n = nm_cur;
                 rc->scan1 += sc1, rc->scan2 += sc2;
             }
             if (stop) break;

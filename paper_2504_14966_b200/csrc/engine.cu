@@ -42,6 +42,8 @@ struct ChainRec {
     double g;      // best score of the chain (-1 = never started)
     double t;      // summed latency of the best
     double cur_f;  // current score (multi-chain-per-warp state save)
+    long long cur_tot;  // current total latency in ticks (K3 state save)
+    int cur_A, cur_n;   // current +inf-deadline count and SLO count (K3 state save)
     int n_met;
     int levels;
     unsigned long long proposals;
@@ -213,10 +215,18 @@ __global__ void __launch_bounds__(1024) k_smem_probe(int iters, uint4* sink) {
     if ((acc.x ^ acc.y ^ acc.z ^ acc.w) == 0x9e3779b9u) sink[threadIdx.x] = acc;
 }
 
-// interleave the SoA tables into {exec, deadline} pairs
-__global__ void k_interleave(int total, const double* exec, const double* dl, double2* tab) {
+// interleave the SoA tables into {exec, deadline} pairs (K1, K2, exhaustive) and build the
+// tick tables of K3: exec rounded to the 2^-k ms grid (| kAlways where the deadline is +inf) and
+// deadline ticks floor(D * 2^k) (-1 where no elapsed time >= 0 meets it)
+__global__ void k_tables(int total, const double* exec, const double* dl, double scale, double2* tab, uint32_t* xt,
+                         long long* dt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < total) tab[i] = make_double2(exec[i], dl[i]);
+    if (i >= total) return;
+    const double e = exec[i], d = dl[i];
+    tab[i] = make_double2(e, d);
+    const bool always = d == INFINITY;
+    xt[i] = (uint32_t)__double2ull_rn(e * scale) | (always ? kAlways : 0u);
+    dt[i] = always || !(d >= 0.0) ? -1ll : (long long)fmin(floor(d * scale), 0x1.0p62);
 }
 
 // ------------------------------------------------------------------ host side
@@ -268,7 +278,10 @@ struct slo_ctx {
     int sm_count = 0;
     size_t smem_optin = 0;
     int n = 0, mb = 0;
-    DevBuf tab, exec_soa, dl_soa;
+    DevBuf tab, exec_soa, dl_soa, xt, dt;
+    double tick = 1.0;   // K3 grid: 2^-k ms
+    long long dg = -1;   // K3: largest finite deadline in ticks
+    bool exec_nonneg = true;
     // chains
     DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
         result, win_ent, win_bits;
@@ -349,10 +362,31 @@ int slo_problem_set(slo_ctx* c, int32_t n, int32_t mb, const double* exec, const
     CK(c->tab.reserve(total * sizeof(double2)));
     CK(c->exec_soa.reserve(total * sizeof(double)));
     CK(c->dl_soa.reserve(total * sizeof(double)));
+    CK(c->xt.reserve(total * sizeof(uint32_t)));
+    CK(c->dt.reserve(total * sizeof(long long)));
+    // K3 tick grid: the largest power of two 2^k with max exec * 2^k <= kTickMask
+    double emax = 0.0, dmax_fin = -1.0;
+    bool nonneg = true;
+    for (size_t i = 0; i < total; ++i) {
+        if (!(exec[i] >= 0.0) || !std::isfinite(exec[i])) nonneg = false;
+        else emax = std::max(emax, exec[i]);
+        if (std::isfinite(deadline[i]) && deadline[i] >= 0.0) dmax_fin = std::max(dmax_fin, deadline[i]);
+    }
+    int k = 40;
+    if (emax > 0.0) {
+        k = 0;
+        while (k < 60 && std::ldexp(emax, k + 1) <= (double)kTickMask) ++k;
+        while (k > -60 && std::ldexp(emax, k) > (double)kTickMask) --k;
+    }
+    c->tick = std::ldexp(1.0, -k);
+    c->dg = dmax_fin >= 0.0 ? (long long)std::fmin(std::floor(std::ldexp(dmax_fin, k)), 0x1.0p62) : -1;
+    c->exec_nonneg = nonneg;
     CK(cudaMemcpyAsync(c->exec_soa.p, exec, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->dl_soa.p, deadline, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    k_interleave<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>((int)total, c->exec_soa.as<double>(),
-                                                                           c->dl_soa.as<double>(), c->tab.as<double2>());
+    k_tables<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>((int)total, c->exec_soa.as<double>(),
+                                                                       c->dl_soa.as<double>(), std::ldexp(1.0, k),
+                                                                       c->tab.as<double2>(), c->xt.as<uint32_t>(),
+                                                                       c->dt.as<long long>());
     CK(cudaGetLastError());
     CK(cudaStreamSynchronize(c->stream));
     c->n = n;
@@ -360,6 +394,8 @@ int slo_problem_set(slo_ctx* c, int32_t n, int32_t mb, const double* exec, const
     c->prepared = false;
     return SLO_OK;
 }
+
+double slo_problem_tick_ms(slo_ctx* c) { return c && c->n > 0 ? c->tick : 0.0; }
 
 int slo_evaluate_batch(slo_ctx* c, int32_t count, const uint16_t* perms, const uint32_t* bits, int32_t* n_met,
                        double* t, double* g) {
@@ -442,7 +478,7 @@ int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
 
 template <int UPL>
 int configure_chains(slo_ctx* c) {
-    const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(double2);
+    const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(uint32_t);
     const size_t slot = slot_bytes<UPL>();
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
     const int max_w = UPL == 1 ? SLO_CHAIN_THREADS / 32 : 16;
@@ -453,7 +489,7 @@ int configure_chains(slo_ctx* c) {
 
 template <int UPL>
 void launch_t(slo_ctx* c) {
-    const size_t ss = 1024 * (size_t)UPL * 2 + 32 * (size_t)UPL * 4;
+    const size_t ss = 32 * (size_t)UPL * 12 + 1024 * (size_t)UPL * 2 + 32 * (size_t)UPL * 4;
     k_start<UPL><<<1, 32, ss, c->stream>>>(c->kp);
     if (c->smem_tab) k_chains<UPL, true><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
     else k_chains<UPL, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
@@ -472,7 +508,7 @@ int launch_chains_U(slo_ctx* c) {
 }
 
 size_t chain_state_bytes(int upl) {
-    return upl == 1 ? sizeof(ChainState<1>) : (upl == 2 ? sizeof(ChainState<2>) : sizeof(ChainState<4>));
+    return upl == 1 ? sizeof(LaneState<1>) : (upl == 2 ? sizeof(LaneState<2>) : sizeof(LaneState<4>));
 }
 
 int configure_U(slo_ctx* c) {
@@ -565,6 +601,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
         return SLO_OK;
     }
     if (prm->rng_mode != SLO_RNG_PHILOX) return fail(SLO_ERR_ARG, "slo_chains_prepare: unknown rng_mode");
+    if (!c->exec_nonneg) return fail(SLO_ERR_DATA, "slo_chains_prepare: the chain kernel needs finite, non-negative exec times");
 
     const int UPL = pick_upl(n);
     c->UPL = UPL;
@@ -611,7 +648,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     CK(cudaStreamSynchronize(c->stream));  // host staging vectors go out of scope
 
     ChainParams& kp = c->kp;
-    kp.n = n, kp.mb = c->mb, kp.tab = c->tab.as<double2>(), kp.smem_tab = c->smem_tab ? 1 : 0;
+    kp.n = n, kp.mb = c->mb, kp.smem_tab = c->smem_tab ? 1 : 0;
+    kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.dg = c->dg, kp.tick = c->tick;
     kp.magic = (1ull << 32) / (uint64_t)n + 1;
     kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;
     kp.iter = prm->iter, kp.levels = c->levels;
@@ -621,8 +659,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     kp.budget_ns = prm->budget_ns;
     kp.start_ent = c->start_ent.as<uint16_t>(), kp.start_bits = c->start_bits.as<uint32_t>();
     kp.st_ent = multi ? c->st_ent.as<uint16_t>() : nullptr, kp.st_bits = multi ? c->st_bits.as<uint32_t>() : nullptr;
-    kp.st_sum = multi ? c->st_sum.p : nullptr;
-    kp.start_sum = c->start_sum.p, kp.start_obj = c->start_obj.as<double>();
+    kp.st_lane = multi ? c->st_sum.p : nullptr;
+    kp.start_lane = c->start_sum.p, kp.start_obj = c->start_obj.as<long long>();
     kp.best_ent = c->best_ent.as<uint16_t>(), kp.best_bits = c->best_bits.as<uint32_t>();
     kp.rec = c->rec.as<ChainRec>();
     c->prepared = true;

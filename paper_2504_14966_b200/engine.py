@@ -79,6 +79,11 @@ class Engine:
         _check_engine(lib().slo_problem_set(self._ctx, n, mb, _p(ex, c_double), _p(dl, c_double)))
         self.n, self.mb = n, mb
 
+    @property
+    def tick_ms(self) -> float:
+        """Grid (ms) of the chain kernel's integer objective for the current problem."""
+        return float(lib().slo_problem_tick_ms(self._ctx))
+
     def evaluate_batch(self, perms: np.ndarray, bits: np.ndarray):
         """K1: bit-exact n_met / t / g of `count` candidates (dense-index perms [count, n])."""
         perms = np.ascontiguousarray(perms, dtype=np.uint16)

@@ -19,7 +19,10 @@ LADDERS = {
     "1e2..1e6": (1e2, 1e3, 1e4, 1e5, 1e6),
     "1e3..1e7": (1e3, 1e4, 1e5, 1e6, 1e7),
     "1e4..1e8": (1e4, 1e5, 1e6, 1e7, 1e8),
+    "1e5..1e9": (1e5, 1e6, 1e7, 1e8, 1e9),
 }
+SCHEDULES = [(500.0, 0.7, 60), (500.0, 0.7, 100), (500.0, 0.7, 160), (500.0, 0.5, 200), (500.0, 0.85, 60),
+             (2000.0, 0.7, 100), (100.0, 0.8, 100)]
 
 
 def main():
@@ -28,13 +31,13 @@ def main():
     ap.add_argument("--chains", type=int, default=16384)
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--seeds", type=int, default=2)
+    ap.add_argument("--ladders", default="1e3..1e7,1e4..1e8,1e5..1e9")
     args = ap.parse_args()
     c = S.table_coefficients()
     w = S.generate_mixed(args.n, 0)
     ids = w.ids()
     rows = []
-    grid = itertools.product(LADDERS.items(), [(500.0, 0.7, 60), (500.0, 0.5, 100), (500.0, 0.85, 30),
-                                               (2000.0, 0.7, 60), (100.0, 0.7, 60)])
+    grid = itertools.product([(k, LADDERS[k]) for k in args.ladders.split(",")], SCHEDULES)
     for (lname, ladder), (t0, tau, it) in grid:
         for chains in (args.chains, args.chains // 4):
             ns, gs = [], []
