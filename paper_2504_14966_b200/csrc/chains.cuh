@@ -30,9 +30,10 @@
 #ifndef SLO_CHAIN_THREADS
 #define SLO_CHAIN_THREADS 768  // k_chains<1> block size (24 warps)
 #endif
-constexpr int kPreAttempts = 6;                      // move attempts drawn ahead (3 words each)
-constexpr int kRndWords = 3 * kPreAttempts + 2;      // + the acceptance uniform (2 words)
-static_assert(kRndWords % 4 == 0, "Philox block rows are stored as uint4");
+constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
+constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
+constexpr int kRndWords = 32;                        // words per proposal: 8 Philox blocks of 4
+static_assert(kAccWord + 2 <= kRndWords, "Philox row too small");
 constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
 constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
 constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
@@ -89,6 +90,26 @@ __device__ __forceinline__ uint32_t xt_ld(const TabRef& t, uint32_t i) {
     }
 }
 
+// Batch-end searches for batches of <= 16 positions: the answer lies within the 64-bit window of
+// the word holding q and its neighbour, so no loop is needed.
+// last set bit strictly before q, or -1
+__device__ __forceinline__ int prev_end16(const uint32_t* bits, int q) {
+    const int w = q >> 5;
+    const uint32_t lo = w > 0 ? bits[w - 1] : 0u;
+    const uint32_t hi = bits[w] & ((1u << (q & 31)) - 1u);
+    const unsigned long long x = ((unsigned long long)hi << 32) | lo;
+    return x ? (w << 5) + 31 - __clzll(x) : -1;
+}
+// first set bit at or after q (bit n-1 is always set; the word after the last one is never the
+// answer, so reading past it is harmless)
+__device__ __forceinline__ int next_end16(const uint32_t* bits, int q) {
+    const int w = q >> 5;
+    const unsigned long long x = (((unsigned long long)bits[w + 1] << 32) | bits[w]) >> (q & 31);
+    return q + __ffsll(x) - 1;
+}
+
+__device__ __forceinline__ unsigned long long mulw(uint32_t a, uint32_t b) { return (unsigned long long)a * b; }
+
 // segmented inclusive max over the 32 positions of a unit; segments restart after an end bit
 // (and at the unit start) and are at most mb long, so log2(mb) shuffle steps suffice
 __device__ __forceinline__ uint32_t seg_max(uint32_t x, uint32_t w, int lane, int mb) {
@@ -130,13 +151,6 @@ __device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits,
     return __popc(__ballot_sync(FULL, met));
 }
 
-// Philox words of (proposal, chain, attempt) -- out of line: only retries >= kPreAttempts need it
-__device__ __noinline__ uint4 philox_draw(uint32_t prop, uint32_t cid, uint32_t attempt, uint32_t k0, uint32_t k1) {
-    uint32_t r[4] = {prop, cid, attempt, kTagMove};
-    philox10(r, k0, k1);
-    return make_uint4(r[0], r[1], r[2], r[3]);
-}
-
 struct Move {
     int kind;        // 0 none, 1 range (squeeze/delay), 2 swap
     int lo, hi, split, sz1, sz2;
@@ -146,69 +160,79 @@ struct Move {
 };
 
 // The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the entry /
-// bitmask representation: batch sizes come from the entries, batch starts from one bit search.
-// Attempts < kPreAttempts read the lane-parallel Philox block; later retries draw directly.
-// Counter = (proposal, chain, attempt, tag): results do not depend on the launch geometry.
+// bitmask representation: up to 8 attempts of op = U[0,3) (squeeze / delay / swap), the first
+// that applies wins, else a forced swap. Lane j < 9 evaluates attempt j from its three Philox
+// words (attempt 8 is the forced swap) and the warp takes the first valid one -- the same move
+// the sequential loop would pick, at the cost of one attempt instead of ~3. Batch sizes come
+// from the entries, batch bounds from one 64-bit bit search.
 __device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint64_t magic,
-                                          uint32_t prop, uint32_t cid, uint32_t k0, uint32_t k1, const uint32_t* rw) {
+                                          const uint32_t* rw, int lane) {
     auto size_at = [&](int q) { return (int)(((uint64_t)ent[q] * magic) >> 32) + 1; };
-    Move mv;
-    mv.kind = 0;
-    if (n == 0) return mv;
-    for (int attempt = 0; attempt <= 8; ++attempt) {
-        uint32_t r0, r1, r2;
-        if (attempt < kPreAttempts) {
-            r0 = rw[3 * attempt], r1 = rw[3 * attempt + 1], r2 = rw[3 * attempt + 2];
-        } else {
-            const uint4 r = philox_draw(prop, cid, (uint32_t)attempt, k0, k1);
-            r0 = r.x, r1 = r.y, r2 = r.z;
-        }
-        const uint32_t op = attempt < 8 ? lemire32(r0, 3) : 2u;  // forced swap after 8 misses
+    // packed move: p0 = lo | hi << 16 (swap: a | b << 16), p1 = (split + 1) | ra << 16,
+    // p2 = rb | (clr + 1) << 16, p3 = (set + 1) | kind << 16 | (dir > 0) << 20
+    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+    bool ok = false;
+    if (lane < kAttempts && n > 0) {
+        const uint32_t r0 = rw[3 * lane], r1 = rw[3 * lane + 1], r2 = rw[3 * lane + 2];
+        const uint32_t op = lane < kAttempts - 1 ? lemire32(r0, 3) : 2u;
         if (op == 0) {  // squeeze (:141-153)
             const int first = size_at(0);
-            if (first >= n) continue;
-            const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
-            const int sk = prev_end(bits, pos) + 1;
-            const int prev_size = size_at(sk - 1);
-            if (prev_size >= mb) continue;
-            const int ek = sk + size_at(sk) - 1;
-            mv.kind = 1;
-            mv.lo = sk - prev_size, mv.hi = ek, mv.split = sk;
-            mv.sz1 = prev_size + 1, mv.sz2 = ek - sk;
-            mv.ra = sk, mv.rb = pos, mv.dir = 1;
-            mv.clr = sk - 1, mv.set = sk;
-            return mv;
+            if (first < n) {
+                const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
+                const int sk = prev_end16(bits, pos) + 1;
+                const int prev_size = size_at(sk - 1);
+                if (prev_size < mb) {
+                    const int ek = sk + size_at(sk) - 1;
+                    ok = true;
+                    p0 = (uint32_t)(sk - prev_size) | (uint32_t)ek << 16;
+                    p1 = (uint32_t)(sk + 1) | (uint32_t)sk << 16;
+                    p2 = (uint32_t)pos | (uint32_t)sk << 16;
+                    p3 = (uint32_t)(sk + 1) | 1u << 16 | 1u << 20;
+                }
+            }
         } else if (op == 1) {  // delay (:155-170)
             const int pos = (int)lemire32(r1, (uint32_t)n);
-            const int sk = prev_end(bits, pos) + 1;
-            const int ek = sk + size_at(pos) - 1;
+            const int ek = next_end16(bits, pos);
+            const int sk = ek - size_at(pos) + 1;
             if (ek < n - 1) {
                 const int next_size = size_at(ek + 1);
-                if (next_size >= mb) continue;
-                const int ek1 = ek + next_size;
-                mv.kind = 1;
-                mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
-                mv.sz1 = ek - sk, mv.sz2 = next_size + 1;
-                mv.ra = pos, mv.rb = ek1, mv.dir = -1;
-                mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
+                if (next_size < mb) {
+                    ok = true;
+                    p0 = (uint32_t)sk | (uint32_t)(ek + next_size) << 16;
+                    p1 = (uint32_t)ek | (uint32_t)pos << 16;
+                    p2 = (uint32_t)(ek + next_size) | (uint32_t)(ek + 1) << 16;
+                    p3 = (uint32_t)(ek >= 1 ? ek : 0) | 1u << 16;
+                }
             } else {
-                mv.kind = 1;
-                mv.lo = sk, mv.hi = n - 1, mv.split = n - 2;
-                mv.sz1 = n - 1 - sk, mv.sz2 = 1;
-                mv.ra = pos, mv.rb = n - 1, mv.dir = -1;
-                mv.clr = -1, mv.set = n >= 2 ? n - 2 : -1;
+                ok = true;
+                p0 = (uint32_t)sk | (uint32_t)(n - 1) << 16;
+                p1 = (uint32_t)(n - 1) | (uint32_t)pos << 16;
+                p2 = (uint32_t)(n - 1);
+                p3 = (uint32_t)(n >= 2 ? n - 1 : 0) | 1u << 16;
             }
-            return mv;
-        } else {  // swap (:172-180)
-            if (n < 2) continue;
+        } else if (n >= 2) {  // swap (:172-180)
             const int a = (int)lemire32(r1, (uint32_t)n);
             int b = (int)lemire32(r2, (uint32_t)(n - 1));
             if (b >= a) ++b;
-            mv.kind = 2;
-            mv.a = a, mv.b = b;
-            return mv;
+            ok = true;
+            p0 = (uint32_t)a | (uint32_t)b << 16;
+            p3 = 2u << 16;
         }
     }
+    const unsigned vm = __ballot_sync(FULL, ok);
+    Move mv;
+    mv.kind = 0;
+    if (!vm) return mv;
+    const int src = __ffs(vm) - 1;
+    p0 = __shfl_sync(FULL, p0, src), p1 = __shfl_sync(FULL, p1, src);
+    p2 = __shfl_sync(FULL, p2, src), p3 = __shfl_sync(FULL, p3, src);
+    mv.kind = (int)((p3 >> 16) & 15u);
+    mv.lo = (int)(p0 & 0xffffu), mv.hi = (int)(p0 >> 16);
+    mv.a = mv.lo, mv.b = mv.hi;
+    mv.split = (int)(p1 & 0xffffu) - 1, mv.ra = (int)(p1 >> 16);
+    mv.rb = (int)(p2 & 0xffffu), mv.clr = (int)(p2 >> 16) - 1;
+    mv.set = (int)(p3 & 0xffffu) - 1, mv.dir = (p3 >> 20) & 1u ? 1 : -1;
+    mv.sz1 = mv.split - mv.lo + 1, mv.sz2 = mv.hi - mv.split;
     return mv;
 }
 
@@ -412,33 +436,29 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
 
             for (int it = 0; it < p.iter; ++it) {
-                // the device budget is checked every 8 proposals (warp-uniform), so a launch
-                // overruns it by at most ~8 proposal latencies; the chain is parked as usual
-                if (p.budget_ns > 0 && (it & 7) == 7 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
-                    stop = 1;
-                    break;
+                if ((it & 7) == 0 && it > 0) {
+                    // the device budget is checked every 8 proposals (warp-uniform), so a launch
+                    // overruns it by at most ~8 proposal latencies; the chain is parked as usual
+                    if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
+                        stop = 1;
+                        break;
+                    }
                 }
                 const uint32_t prop = (uint32_t)(lev * p.iter + it);
                 if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..5 and acceptance
                     __syncwarp();      // every lane is done reading the previous block
+                    // row of proposal prop + lane: Philox block b = counter (proposal, chain, b, tag)
                     uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
-                    uint32_t w[kRndWords];
 #pragma unroll
-                    for (int a = 0; a < kPreAttempts; ++a) {
-                        uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)a, kTagMove};
+                    for (int b = 0; b < kRndWords / 4; ++b) {
+                        uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
                         philox10(r, p.key0, p.key1);
-                        w[3 * a] = r[0], w[3 * a + 1] = r[1], w[3 * a + 2] = r[2];
+                        dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
                     }
-                    uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)kAcceptAttempt, kTagMove};
-                    philox10(r, p.key0, p.key1);
-                    w[3 * kPreAttempts] = r[0], w[3 * kPreAttempts + 1] = r[1];
-#pragma unroll
-                    for (int v = 0; v < kRndWords / 4; ++v)
-                        dst[v] = make_uint4(w[4 * v], w[4 * v + 1], w[4 * v + 2], w[4 * v + 3]);
                     __syncwarp();
                 }
                 const uint32_t* rw = rnd + kRndWords * (it & 31);
-                const Move mv = draw_move(ent, bits, n, mb, magic, prop, cid, p.key0, p.key1, rw);
+                const Move mv = draw_move(ent, bits, n, mb, magic, rw, lane);
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
@@ -485,15 +505,17 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     const uint32_t mN1 = __reduce_max_sync(FULL, q > nsp ? xn : 0u);
                     const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
                     dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
-                    const long long after_hi = n - 1 - hi;
-                    long long oc, nc, omk, nmk;
-                    if (osp < hi) oc = (long long)mO0 * (n - 1 - osp) + (long long)mO1 * after_hi, omk = (long long)mO0 + mO1;
-                    else oc = (long long)mO0 * after_hi, omk = mO0;
-                    if (nsp < lo) nc = (long long)mN1 * after_hi, nmk = mN1;
-                    else if (nsp < hi) nc = (long long)mN0 * (n - 1 - nsp) + (long long)mN1 * after_hi, nmk = (long long)mN0 + mN1;
-                    else nc = (long long)mN0 * after_hi, nmk = mN0;
-                    dtot = sN - sO + nc - oc;
-                    const long long delta = nmk - omk;
+                    // makespan * positions-after products: 27 x 12 bits, one widening multiply each
+                    const uint32_t after_hi = (uint32_t)(n - 1 - hi);
+                    unsigned long long oc, nc;
+                    int omk, nmk;
+                    if (osp < hi) oc = mulw(mO0, (uint32_t)(n - 1 - osp)) + mulw(mO1, after_hi), omk = (int)(mO0 + mO1);
+                    else oc = mulw(mO0, after_hi), omk = (int)mO0;
+                    if (nsp < lo) nc = mulw(mN1, after_hi), nmk = (int)mN1;
+                    else if (nsp < hi) nc = mulw(mN0, (uint32_t)(n - 1 - nsp)) + mulw(mN1, after_hi), nmk = (int)(mN0 + mN1);
+                    else nc = mulw(mN0, after_hi), nmk = (int)mN0;
+                    dtot = sN - sO + (long long)(nc - oc);
+                    const int delta = nmk - omk;
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) {
                         const int pu = (lane * UPL + kk) << 5;
@@ -518,7 +540,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     const uint32_t zb = (uint32_t)(((uint64_t)eb_ * magic) >> 32);
                     const uint32_t ba = za * nn, bb = zb * nn;
                     const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
-                    const int sa = prev_end(bits, pa) + 1, sb = prev_end(bits, pb) + 1;
+                    const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
                     const int ea = sa + (int)za, eb = sb + (int)zb;
                     const bool first = lane < 16;
                     q = first ? sa + lane : sb + lane - 16;
@@ -539,8 +561,8 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     const uint32_t mN1 = __reduce_max_sync(FULL, first ? 0u : xn);
                     const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
                     dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
-                    const long long da = (long long)mN0 - mO0, db = (long long)mN1 - mO1;
-                    dtot = sN - sO + da * (n - 1 - ea) + db * (n - 1 - eb);
+                    const int da = (int)mN0 - (int)mO0, db = (int)mN1 - (int)mO1;
+                    dtot = sN - sO + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
                     if (sa == sb) dtot = 0, dA = 0;  // one batch: order inside a batch changes nothing
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) {
@@ -572,7 +594,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     // x = (f - f_new) * scale / t; the test u < exp(-x) runs on the SFU in fp32
                     // (relative error ~1e-7 on the acceptance probability)
                     const double x = (f - f_new) * scale * inv_t;
-                    const uint32_t* ru = rw + 3 * kPreAttempts;
+                    const uint32_t* ru = rw + kAccWord;
                     const double u = (double)((((uint64_t)ru[0] << 32) | ru[1]) >> 11) * 0x1.0p-53;
                     accept = x < 38.0 ? (float)u < __expf(-(float)x) : u == 0.0;
                 }

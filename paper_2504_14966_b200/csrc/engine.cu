@@ -36,7 +36,6 @@ thread_local std::string g_err;
 
 constexpr unsigned FULL = 0xffffffffu;
 constexpr uint32_t kTagMove = 0x5105c4edu;   // Philox counter word 3 for move draws
-constexpr int kAcceptAttempt = 15;           // Philox counter word 2 for the Metropolis draw
 
 struct ChainRec {
     double g;      // best score of the chain (-1 = never started)
