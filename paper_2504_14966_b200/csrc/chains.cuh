@@ -93,12 +93,12 @@ __device__ __forceinline__ uint32_t xt_ld(const TabRef& t, uint32_t i) {
 // Batch-end searches for batches of <= 16 positions: the answer lies within the 64-bit window of
 // the word holding q and its neighbour, so no loop is needed.
 // last set bit strictly before q, or -1
+// (bits[-1] is a zero word in the chain slot)
 __device__ __forceinline__ int prev_end16(const uint32_t* bits, int q) {
     const int w = q >> 5;
-    const uint32_t lo = w > 0 ? bits[w - 1] : 0u;
+    const uint32_t lo = bits[w - 1];
     const uint32_t hi = bits[w] & ((1u << (q & 31)) - 1u);
-    const unsigned long long x = ((unsigned long long)hi << 32) | lo;
-    return x ? (w << 5) + 31 - __clzll(x) : -1;
+    return hi ? (w << 5) + 31 - __clz(hi) : max((w << 5) - 1 - __clz(lo), -1);  // lo = 0 only when w = 0
 }
 // first set bit at or after q (bit n-1 is always set; the word after the last one is never the
 // answer, so reading past it is harmless)
@@ -241,10 +241,14 @@ __device__ __forceinline__ double objective(int nm, double tot) {
     return tot > 0.0 ? (double)nm * __drcp_rn(tot) : 0.0;
 }
 
+// Philox rows drawn per refill (one per lane): 32 proposals, 16 where shared memory is tight
+template <int UPL>
+__host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : 16; }
+
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
-    // entries + bitmask + Philox block (32 proposals)
-    return 1024 * UPL * 2 + 32 * UPL * 4 + 32 * kRndWords * 4;
+    // entries + a zero word (bits[-1]) and padding + bitmask + Philox rows
+    return 1024 * UPL * 2 + 16 + 32 * UPL * 4 + rnd_rows<UPL>() * kRndWords * 4;
 }
 
 template <int UPL>
@@ -385,8 +389,10 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
     constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
     unsigned char* slot = smem + off + (size_t)wid * slot_bytes<UPL>();
     uint16_t* ent = reinterpret_cast<uint16_t*>(slot);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2);
-    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + kBits * 4);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16);
+    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16 + kBits * 4);
+    constexpr int kRows = rnd_rows<UPL>();
+    if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
 
     const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
     if (gw >= p.chain_count) return;
@@ -445,19 +451,21 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     }
                 }
                 const uint32_t prop = (uint32_t)(lev * p.iter + it);
-                if ((it & 31) == 0) {  // lane j draws proposal prop + j: attempts 0..5 and acceptance
-                    __syncwarp();      // every lane is done reading the previous block
-                    // row of proposal prop + lane: Philox block b = counter (proposal, chain, b, tag)
-                    uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
+                if ((it & (kRows - 1)) == 0) {  // lane j draws the row of proposal prop + j
+                    __syncwarp();                // every lane is done reading the previous rows
+                    if (lane < kRows) {
+                        // Philox block b of a row = counter (proposal, chain, b, tag)
+                        uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
 #pragma unroll
-                    for (int b = 0; b < kRndWords / 4; ++b) {
-                        uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
-                        philox10(r, p.key0, p.key1);
-                        dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
+                        for (int b = 0; b < kRndWords / 4; ++b) {
+                            uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
+                            philox10(r, p.key0, p.key1);
+                            dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
+                        }
                     }
                     __syncwarp();
                 }
-                const uint32_t* rw = rnd + kRndWords * (it & 31);
+                const uint32_t* rw = rnd + kRndWords * (it & (kRows - 1));
                 const Move mv = draw_move(ent, bits, n, mb, magic, rw, lane);
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
