@@ -348,9 +348,10 @@ def run_ours(args):
             dist.destroy_process_group()
         return
 
-    # ---- roofline of the dominant kernel (k_chains). It is instruction-issue bound (ncu: ~76%
-    # issue slots busy, DRAM ~1%, L1 ~52%), so the roofline is warp-instruction issue:
-    # achieved = (ncu-measured instructions per proposal, profiles/r1) x proposals this run
+    # ---- roofline of the dominant kernel (k_chains). It is instruction-issue bound (ncu: ~75%
+    # issue slots busy, DRAM < 1%, L1 ~20%), so the roofline is warp-instruction issue:
+    # achieved = (ncu-measured instructions per proposal of the same configuration,
+    # profiles/r1/k_chains_summary.json from tools/prof_chains.py --bench) x proposals this run
     # evaluated / the kernel's CUDA-event time; peak = 4 issue slots x SMs x the SM clock sampled
     # during the timed region. The shared-memory view (bytes the evaluator gathers) is kept beside.
     prof = load_profile_summary()
@@ -360,12 +361,14 @@ def run_ours(args):
     peak_ginst = 4 * n_sms * sm_mhz * 1e6 / 1e9
     ipp = prof.get("instr_per_proposal") if prof else None
     achieved_ginst = (ipp * props / (kern_ms / 1e3) / 1e9) if ipp else None
-    smem_bytes = 18.0 * (pos1 + pos2)  # 2 B entry + 16 B (exec, deadline) per gathered position
+    # rebuilt-batch positions: 2 B entry + old and new 4 B exec ticks; walked positions: 2 B entry +
+    # 4 B exec ticks + 8 B deadline ticks
+    smem_bytes = 10.0 * pos1 + 14.0 * pos2
     roof = {"bound": "issue", "achieved": achieved_ginst, "peak": peak_ginst, "unit": "Gwarp-inst/s",
             "frac": (achieved_ginst / peak_ginst) if achieved_ginst else None,
             "traffic": (prof["dram_bytes_per_proposal"] * props / args.steps) if prof else None,
             "kernel": "k_chains", "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
-            "instr_per_proposal": ipp, "instr_source": "profiles/r1/k_chains_summary.json (ncu --set full)",
+            "instr_per_proposal": ipp, "instr_source": "profiles/r1/k_chains_summary.json (ncu --set full, tools/prof_chains.py --bench)",
             "peak_source": f"4 warp-inst/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz (sampled under load)",
             "smem_view": {"achieved_gbs": smem_bytes / (kern_ms / 1e3) / 1e9, "peak_gbs": smem_peak_gbs,
                           "peak_source": "slo_probe_smem_bandwidth (conflict-free LDS.128, all SMs, measured here)",
@@ -383,7 +386,7 @@ def run_ours(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f64", "data": "synthetic",
+        "dtype": "i64", "data": "synthetic",
         "config": {"workload": f"configs[2]: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
                                f"predictions, {args.chains} chains/GPU, {args.budget_ms} ms budget",
                    "n_requests": n, "max_batch": mb, "chains_per_gpu": args.chains, "chains_total": chains_total,

@@ -617,6 +617,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                         if (lane == 0) rc->g = f, rc->t = t_new, rc->n_met = nm;
                     }
                 } else {
+                    __syncwarp();  // every lane is done reading the state (SLO walks) before the undo
                     if (mv.kind == 1) {
                         if (q <= mv.hi) ent[q] = old_q;
                         if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;

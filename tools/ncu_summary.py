@@ -85,6 +85,9 @@ def functions(rep):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
+    ap.add_argument("--desc", default="k_chains<1> (N=1024, mb=4, 16384 chains, bench configuration via "
+                    "tools/prof_chains.py --bench: best of three starts, t0=500 tau=0.7 iter=100, 7 levels, "
+                    "scale ladder 1e4..1e8, no budget)")
     ap.add_argument("--proposals", type=float, required=True)
     ap.add_argument("--tag", required=True)
     ap.add_argument("--launches", default=None)
@@ -102,7 +105,7 @@ def main():
             "Block Size", "Grid Size"]
     summary = {
         "report": os.path.basename(args.rep),
-        "kernel": "k_chains<1> (N=1024, mb=4, 16384 chains, t0=500 tau=0.5 iter=32, no budget)",
+        "kernel": args.desc,
         "metrics": {k: {"value": d[k][0], "unit": d[k][1]} for k in keys if k in d},
         "proposals": args.proposals,
         "instr_per_proposal": instr / args.proposals if instr else None,

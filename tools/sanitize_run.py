@@ -13,7 +13,7 @@ import paper_2504_14966_b200 as S  # noqa: E402
 from paper_2504_14966_b200 import engine as E  # noqa: E402
 
 c = S.table_coefficients()
-for n, mb, chains in [(5, 2, 8), (70, 4, 64), (300, 8, 100), (1500, 4, 40)]:
+for n, mb, chains in [(5, 2, 8), (70, 4, 64), (300, 8, 100), (200, 16, 50), (1500, 4, 40), (3000, 4, 20)]:
     w = S.generate_mixed(n, n)
     r = S.anneal(w, w.ids(), c, S.AnnealConfig(seed=1, chains=chains, t0=60.0, iter=40,
                                                scale_ladder=(1.0, 100.0)), mb)
