@@ -47,7 +47,8 @@ struct __align__(16) LaneState {  // this lane's unit anchors
 
 struct ChainParams {
     int n, mb;
-    uint64_t magic;      // floor(2^32 / n) + 1: (e * magic) >> 32 == e / n exactly for e < 65536
+    uint32_t magic;      // floor(2^32 / n) + 1 (0 for n = 1, whose only entry is 0):
+                         // umulhi(e, magic) == e / n exactly for e < 65536, 2 <= n <= 4096
     const uint32_t* xt;  // global [mb][n] exec ticks | kAlways
     const long long* dt; // global [mb][n] deadline ticks (-1: never met; unused where kAlways)
     long long dg;        // largest finite deadline (ticks): units with E > dg are dead
@@ -165,9 +166,9 @@ struct Move {
 // words (attempt 8 is the forced swap) and the warp takes the first valid one -- the same move
 // the sequential loop would pick, at the cost of one attempt instead of ~3. Batch sizes come
 // from the entries, batch bounds from one 64-bit bit search.
-__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint64_t magic,
+__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint32_t magic,
                                           const uint32_t* rw, int lane) {
-    auto size_at = [&](int q) { return (int)(((uint64_t)ent[q] * magic) >> 32) + 1; };
+    auto size_at = [&](int q) { return (int)__umulhi(ent[q], magic) + 1; };
     // packed move: p0 = lo | hi << 16 (swap: a | b << 16), p1 = (split + 1) | ra << 16,
     // p2 = rb | (clr + 1) << 16, p3 = (set + 1) | kind << 16 | (dir > 0) << 20
     uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
@@ -408,13 +409,14 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
     unsigned long long props = 0, accs = 0;
     int stop = 0;
     const uint32_t nn = (uint32_t)n;
-    const uint64_t magic = p.magic;
+    const uint32_t magic = p.magic;
     const long long dg = p.dg;
     auto* parked = reinterpret_cast<LaneState<UPL>*>(p.st_lane);
 
     double t = p.t0;
     for (int lev = 0; lev < p.levels && !stop; ++lev, t *= p.tau) {
         const double inv_t = 1.0 / t;
+        double sinv = 0.0;  // objective scale / t of the current chain
         for (int k = 0; k < n_my; ++k) {
             if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
                 stop = 1;
@@ -440,6 +442,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 __syncwarp();
             }
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
+            sinv = scale * inv_t;
 
             for (int it = 0; it < p.iter; ++it) {
                 if ((it & 7) == 0 && it > 0) {
@@ -489,7 +492,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                         else s = q == mv.rb ? mv.ra : (q >= mv.ra && q < mv.rb ? q + 1 : q);
                         old_q = ent[q];
                         const uint32_t se = ent[s];
-                        const uint32_t idx = se - (uint32_t)(((uint64_t)se * magic) >> 32) * nn;
+                        const uint32_t idx = se - __umulhi(se, magic) * nn;
                         const int sz = q <= mv.split ? mv.sz1 : mv.sz2;
                         nw = (uint16_t)(idx + (uint32_t)(sz - 1) * nn);
                     }
@@ -544,8 +547,8 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     const int pa = min(mv.a, mv.b), pb = max(mv.a, mv.b);
                     const uint32_t ea_ = ent[pa], eb_ = ent[pb];
                     ow0 = ea_, ow1 = eb_;
-                    const uint32_t za = (uint32_t)(((uint64_t)ea_ * magic) >> 32);  // batch size - 1
-                    const uint32_t zb = (uint32_t)(((uint64_t)eb_ * magic) >> 32);
+                    const uint32_t za = __umulhi(ea_, magic);  // batch size - 1
+                    const uint32_t zb = __umulhi(eb_, magic);
                     const uint32_t ba = za * nn, bb = zb * nn;
                     const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
                     const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
@@ -600,11 +603,10 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
                 if (!accept) {
                     // x = (f - f_new) * scale / t; the test u < exp(-x) runs on the SFU in fp32
-                    // (relative error ~1e-7 on the acceptance probability)
-                    const double x = (f - f_new) * scale * inv_t;
-                    const uint32_t* ru = rw + kAccWord;
-                    const double u = (double)((((uint64_t)ru[0] << 32) | ru[1]) >> 11) * 0x1.0p-53;
-                    accept = x < 38.0 ? (float)u < __expf(-(float)x) : u == 0.0;
+                    // with a 24-bit uniform (acceptance probabilities within ~1e-7 of exact)
+                    const float x = (float)((f - f_new) * sinv);
+                    const float u = (float)(rw[kAccWord] >> 8) * 0x1.0p-24f;
+                    accept = u < __expf(-x);
                 }
                 if (accept) {
                     ++accs;

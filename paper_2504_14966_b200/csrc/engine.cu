@@ -649,7 +649,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     ChainParams& kp = c->kp;
     kp.n = n, kp.mb = c->mb, kp.smem_tab = c->smem_tab ? 1 : 0;
     kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.dg = c->dg, kp.tick = c->tick;
-    kp.magic = (1ull << 32) / (uint64_t)n + 1;
+    kp.magic = n >= 2 ? (uint32_t)((1ull << 32) / (uint64_t)n + 1) : 0u;
     kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;
     kp.iter = prm->iter, kp.levels = c->levels;
     kp.scale_mult = c->scale_mult.as<double>(), kp.n_mult = prm->n_scale_mult;
