@@ -62,11 +62,11 @@ struct ChainParams {
     int chain_begin, chain_count;
     long long budget_ns;
     const uint16_t* start_ent;   // [1024*UPL]
-    const uint32_t* start_bits;  // [32*UPL]
+    uint32_t* start_bits;        // [3][32*UPL]: batch ends (host), move flags sqb, dlb (k_start)
     void* start_lane;            // LaneState<UPL>[32]: the start state's anchors (k_start)
     long long* start_obj;        // {total ticks, A, n_met} of the start state (k_start)
     uint16_t* st_ent;            // [chain_count][1024*UPL]  parked chains (several chains per warp)
-    uint32_t* st_bits;           // [chain_count][32*UPL]
+    uint32_t* st_bits;           // [chain_count][3][32*UPL]
     void* st_lane;               // [chain_count][32] LaneState<UPL>
     uint16_t* best_ent;          // [chain_count][1024*UPL]
     uint32_t* best_bits;         // [chain_count][32*UPL]
@@ -162,78 +162,76 @@ struct Move {
 
 // The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the entry /
 // bitmask representation: up to 8 attempts of op = U[0,3) (squeeze / delay / swap), the first
-// that applies wins, else a forced swap. Lane j < 9 evaluates attempt j from its three Philox
-// words (attempt 8 is the forced swap) and the warp takes the first valid one -- the same move
-// the sequential loop would pick, at the cost of one attempt instead of ~3. Batch sizes come
-// from the entries, batch bounds from one 64-bit bit search.
-__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, int n, int mb, uint32_t magic,
-                                          const uint32_t* rw, int lane) {
+// that applies wins, else a forced swap. Lane j < 9 tests attempt j from its three Philox words
+// (attempt 8 is the forced swap) with one move-flag bit, the warp takes the first valid one --
+// the same move the sequential loop would pick -- and only that move's batch bounds are computed
+// (batch sizes from the entries, bounds from one 64-bit bit search).
+__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, const uint32_t* sqb,
+                                          const uint32_t* dlb, int n, int mb, uint32_t magic, const uint32_t* rw,
+                                          int lane) {
     auto size_at = [&](int q) { return (int)__umulhi(ent[q], magic) + 1; };
-    // packed move: p0 = lo | hi << 16 (swap: a | b << 16), p1 = (split + 1) | ra << 16,
-    // p2 = rb | (clr + 1) << 16, p3 = (set + 1) | kind << 16 | (dir > 0) << 20
-    uint32_t p0 = 0, p1 = 0, p2 = 0, p3 = 0;
+    uint32_t pk = 0;  // op << 30 | a | b << 13  (squeeze / delay: a = pos)
     bool ok = false;
     if (lane < kAttempts && n > 0) {
         const uint32_t r0 = rw[3 * lane], r1 = rw[3 * lane + 1], r2 = rw[3 * lane + 2];
         const uint32_t op = lane < kAttempts - 1 ? lemire32(r0, 3) : 2u;
-        if (op == 0) {  // squeeze (:141-153)
+        if (op == 0) {  // squeeze (:141-153): fails if the batch before pos's batch is full
             const int first = size_at(0);
             if (first < n) {
                 const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
-                const int sk = prev_end16(bits, pos) + 1;
-                const int prev_size = size_at(sk - 1);
-                if (prev_size < mb) {
-                    const int ek = sk + size_at(sk) - 1;
-                    ok = true;
-                    p0 = (uint32_t)(sk - prev_size) | (uint32_t)ek << 16;
-                    p1 = (uint32_t)(sk + 1) | (uint32_t)sk << 16;
-                    p2 = (uint32_t)pos | (uint32_t)sk << 16;
-                    p3 = (uint32_t)(sk + 1) | 1u << 16 | 1u << 20;
-                }
+                ok = !((sqb[pos >> 5] >> (pos & 31)) & 1u);
+                pk = (uint32_t)pos;
             }
-        } else if (op == 1) {  // delay (:155-170)
+        } else if (op == 1) {  // delay (:155-170): fails if the next batch exists and is full
             const int pos = (int)lemire32(r1, (uint32_t)n);
-            const int ek = next_end16(bits, pos);
-            const int sk = ek - size_at(pos) + 1;
-            if (ek < n - 1) {
-                const int next_size = size_at(ek + 1);
-                if (next_size < mb) {
-                    ok = true;
-                    p0 = (uint32_t)sk | (uint32_t)(ek + next_size) << 16;
-                    p1 = (uint32_t)ek | (uint32_t)pos << 16;
-                    p2 = (uint32_t)(ek + next_size) | (uint32_t)(ek + 1) << 16;
-                    p3 = (uint32_t)(ek >= 1 ? ek : 0) | 1u << 16;
-                }
-            } else {
-                ok = true;
-                p0 = (uint32_t)sk | (uint32_t)(n - 1) << 16;
-                p1 = (uint32_t)(n - 1) | (uint32_t)pos << 16;
-                p2 = (uint32_t)(n - 1);
-                p3 = (uint32_t)(n >= 2 ? n - 1 : 0) | 1u << 16;
-            }
+            ok = !((dlb[pos >> 5] >> (pos & 31)) & 1u);
+            pk = 1u << 30 | (uint32_t)pos;
         } else if (n >= 2) {  // swap (:172-180)
             const int a = (int)lemire32(r1, (uint32_t)n);
             int b = (int)lemire32(r2, (uint32_t)(n - 1));
             if (b >= a) ++b;
             ok = true;
-            p0 = (uint32_t)a | (uint32_t)b << 16;
-            p3 = 2u << 16;
+            pk = 2u << 30 | (uint32_t)a | (uint32_t)b << 13;
         }
     }
     const unsigned vm = __ballot_sync(FULL, ok);
     Move mv;
     mv.kind = 0;
     if (!vm) return mv;
-    const int src = __ffs(vm) - 1;
-    p0 = __shfl_sync(FULL, p0, src), p1 = __shfl_sync(FULL, p1, src);
-    p2 = __shfl_sync(FULL, p2, src), p3 = __shfl_sync(FULL, p3, src);
-    mv.kind = (int)((p3 >> 16) & 15u);
-    mv.lo = (int)(p0 & 0xffffu), mv.hi = (int)(p0 >> 16);
-    mv.a = mv.lo, mv.b = mv.hi;
-    mv.split = (int)(p1 & 0xffffu) - 1, mv.ra = (int)(p1 >> 16);
-    mv.rb = (int)(p2 & 0xffffu), mv.clr = (int)(p2 >> 16) - 1;
-    mv.set = (int)(p3 & 0xffffu) - 1, mv.dir = (p3 >> 20) & 1u ? 1 : -1;
-    mv.sz1 = mv.split - mv.lo + 1, mv.sz2 = mv.hi - mv.split;
+    pk = __shfl_sync(FULL, pk, __ffs(vm) - 1);
+    const uint32_t op = pk >> 30;
+    const int pos = (int)(pk & 0x1fffu);
+    if (op == 2) {
+        mv.kind = 2;
+        mv.a = pos, mv.b = (int)((pk >> 13) & 0x1fffu);
+    } else if (op == 0) {
+        const int sk = prev_end16(bits, pos) + 1;
+        const int prev_size = size_at(sk - 1);
+        const int ek = sk + size_at(sk) - 1;
+        mv.kind = 1;
+        mv.lo = sk - prev_size, mv.hi = ek, mv.split = sk;
+        mv.sz1 = prev_size + 1, mv.sz2 = ek - sk;
+        mv.ra = sk, mv.rb = pos, mv.dir = 1;
+        mv.clr = sk - 1, mv.set = sk;
+    } else {
+        const int ek = next_end16(bits, pos);
+        const int sk = ek - size_at(pos) + 1;
+        mv.kind = 1;
+        mv.ra = pos, mv.dir = -1;
+        if (ek < n - 1) {
+            const int next_size = size_at(ek + 1);
+            const int ek1 = ek + next_size;
+            mv.lo = sk, mv.hi = ek1, mv.split = ek - 1;
+            mv.sz1 = ek - sk, mv.sz2 = next_size + 1;
+            mv.rb = ek1;
+            mv.clr = ek, mv.set = ek >= 1 ? ek - 1 : -1;
+        } else {
+            mv.lo = sk, mv.hi = n - 1, mv.split = n - 2;
+            mv.sz1 = n - 1 - sk, mv.sz2 = 1;
+            mv.rb = n - 1;
+            mv.clr = -1, mv.set = n >= 2 ? n - 2 : -1;
+        }
+    }
     return mv;
 }
 
@@ -248,16 +246,37 @@ __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : 16; }
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
-    // entries + a zero word (bits[-1]) and padding + bitmask + Philox rows
-    return 1024 * UPL * 2 + 16 + 32 * UPL * 4 + rnd_rows<UPL>() * kRndWords * 4;
+    // entries + a zero word (bits[-1]) and padding + batch-end bitmask + two move-flag bitmasks +
+    // Philox rows (next_end16 may read one word past the bitmask: the first flag word)
+    return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * kRndWords * 4;
 }
 
-template <int UPL>
+// entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
+template <int UPL, int BW = 32 * UPL>
 __device__ __forceinline__ void copy_state(uint16_t* de, uint32_t* db, const uint16_t* se, const uint32_t* sb,
                                            int lane) {
-    constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
+    constexpr int kEnt = 1024 * UPL;
     for (int i = lane; i < kEnt / 8; i += 32) reinterpret_cast<uint4*>(de)[i] = reinterpret_cast<const uint4*>(se)[i];
-    for (int i = lane; i < kBits; i += 32) db[i] = sb[i];
+    for (int i = lane; i < BW; i += 32) db[i] = sb[i];
+}
+
+// Move flags, words [w0, w1] (all lanes): bit q of sqb set iff a squeeze of position q fails (the
+// batch before q's batch is full), of dlb iff a delay of q fails (q's batch is not the last and
+// the next one is full). They change only when an accepted squeeze/delay rebuilds batches, so the
+// draw tests an attempt with one bit instead of a batch-bound search.
+__device__ __forceinline__ void rebuild_flags(const uint16_t* ent, const uint32_t* bits, uint32_t* sqb, uint32_t* dlb,
+                                              int n, int mb, uint32_t magic, int w0, int w1, int lane) {
+    for (int w = w0; w <= w1; ++w) {
+        const int q = (w << 5) + lane;
+        bool sb = false, db = false;
+        if (q < n) {
+            const int s = prev_end16(bits, q) + 1, e = next_end16(bits, q);
+            sb = s > 0 && (int)__umulhi(ent[s - 1], magic) + 1 >= mb;
+            db = e < n - 1 && (int)__umulhi(ent[e + 1], magic) + 1 >= mb;
+        }
+        const unsigned a = __ballot_sync(FULL, sb), b = __ballot_sync(FULL, db);
+        if (lane == 0) sqb[w] = a, dlb[w] = b;
+    }
 }
 
 // Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts.
@@ -299,10 +318,12 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     long long* Es = reinterpret_cast<long long*>(smem);
     uint32_t* Fs = reinterpret_cast<uint32_t*>(smem + kU * 8);
     uint16_t* ent = reinterpret_cast<uint16_t*>(smem + kU * 12);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + kU * 12 + 1024 * UPL * 2);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + kU * 12 + 1024 * UPL * 2 + 16);  // bits[-1] = 0
     copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
     for (int u = lane; u < kU; u += 32) Es[u] = kPadE, Fs[u] = 0;
+    if (lane == 0) bits[-1] = 0u, bits[kU] = 0u;
     __syncwarp();
+    rebuild_flags(ent, bits, p.start_bits + kU, p.start_bits + 2 * kU, n, p.mb, p.magic, 0, kU - 1, lane);
     // each lane owns positions [q0, q1) (its UPL units); every non-empty range holds a batch end
     // (ranges are >= 32 long, batches <= 16), so the batch open at a range start is closed in it
     const int q0 = lane * 32 * UPL, q1 = min(n, q0 + 32 * UPL);
@@ -391,7 +412,9 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
     unsigned char* slot = smem + off + (size_t)wid * slot_bytes<UPL>();
     uint16_t* ent = reinterpret_cast<uint16_t*>(slot);
     uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16);
-    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16 + kBits * 4);
+    uint32_t* sqb = bits + kBits;  // move flags (state: copied and parked with the bitmask)
+    uint32_t* dlb = bits + 2 * kBits;
+    uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16 + 3 * kBits * 4);
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
 
@@ -427,7 +450,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
             ChainRec* rc = p.rec + c;
             unsigned long long sc1 = 0, sc2 = 0;
             if (lev == 0) {  // every chain starts from the shared start state
-                copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
+                copy_state<UPL, 3 * kBits>(ent, bits, p.start_ent, p.start_bits, lane);
                 cur = reinterpret_cast<const LaneState<UPL>*>(p.start_lane)[lane];
                 tot = p.start_obj[0], A = (int)p.start_obj[1], nm_cur = (int)p.start_obj[2];
                 f = best_f = objective(nm_cur, (double)tot * p.tick), props = 0, accs = 0;
@@ -435,7 +458,8 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits, lane);
                 if (lane == 0) rc->g = f, rc->t = (double)tot * p.tick, rc->n_met = nm_cur;
             } else if (n_my > 1) {  // resume a parked chain
-                copy_state<UPL>(ent, bits, p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, lane);
+                copy_state<UPL, 3 * kBits>(ent, bits, p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * 3 * kBits,
+                                           lane);
                 cur = parked[(size_t)c * 32 + lane];
                 tot = rc->cur_tot, A = rc->cur_A, nm_cur = rc->cur_n;
                 f = rc->cur_f, best_f = rc->g, props = rc->proposals, accs = rc->accepted;
@@ -469,7 +493,7 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                     __syncwarp();
                 }
                 const uint32_t* rw = rnd + kRndWords * (it & (kRows - 1));
-                const Move mv = draw_move(ent, bits, n, mb, magic, rw, lane);
+                const Move mv = draw_move(ent, bits, sqb, dlb, n, mb, magic, rw, lane);
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
@@ -610,6 +634,11 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 }
                 if (accept) {
                     ++accs;
+                    if (mv.kind == 1) {  // rebuilt batches: refresh the move flags around them
+                        rebuild_flags(ent, bits, sqb, dlb, n, mb, magic, max(mv.lo - mb, 0) >> 5,
+                                      min(mv.hi + mb, n - 1) >> 5, lane);
+                        __syncwarp();
+                    }
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
                     if (f > best_f) {
@@ -630,7 +659,8 @@ __global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chain
                 }
             }
             if (n_my > 1) {  // park the chain (state + anchors) until the next level
-                copy_state<UPL>(p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * kBits, ent, bits, lane);
+                copy_state<UPL, 3 * kBits>(p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * 3 * kBits, ent, bits,
+                                           lane);
                 parked[(size_t)c * 32 + lane] = cur;
                 __syncwarp();
             }

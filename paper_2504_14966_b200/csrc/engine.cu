@@ -488,7 +488,7 @@ int configure_chains(slo_ctx* c) {
 
 template <int UPL>
 void launch_t(slo_ctx* c) {
-    const size_t ss = 32 * (size_t)UPL * 12 + 1024 * (size_t)UPL * 2 + 32 * (size_t)UPL * 4;
+    const size_t ss = 32 * (size_t)UPL * 12 + 1024 * (size_t)UPL * 2 + 16 + 32 * (size_t)UPL * 4 + 16;
     k_start<UPL><<<1, 32, ss, c->stream>>>(c->kp);
     if (c->smem_tab) k_chains<UPL, true><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
     else k_chains<UPL, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
@@ -618,7 +618,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     }
     const size_t cc = c->chain_count;
     CK(c->start_ent.reserve(ent_words * sizeof(uint16_t)));
-    CK(c->start_bits.reserve(bit_words * sizeof(uint32_t)));
+    CK(c->start_bits.reserve(3 * bit_words * sizeof(uint32_t)));  // + move flags (k_start)
     CK(c->best_ent.reserve(cc * ent_words * sizeof(uint16_t)));
     CK(c->best_bits.reserve(cc * bit_words * sizeof(uint32_t)));
     CK(c->rec.reserve(cc * sizeof(ChainRec)));
@@ -634,7 +634,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     CK(c->start_obj.reserve(4 * sizeof(double)));
     if (multi) {
         CK(c->st_ent.reserve(cc * ent_words * sizeof(uint16_t)));
-        CK(c->st_bits.reserve(cc * bit_words * sizeof(uint32_t)));
+        CK(c->st_bits.reserve(cc * 3 * bit_words * sizeof(uint32_t)));
         CK(c->st_sum.reserve(cc * 32 * csb));
     }
     // summaries are stored field-wise and copied as whole 16-byte vectors: define the padding

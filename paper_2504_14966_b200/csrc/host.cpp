@@ -527,7 +527,7 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
     // most the sum of its members'). A deadline at or beyond that bound is met in every schedule:
     // store +inf, which leaves every exact compare unchanged and lets the chain kernel count such
     // requests without walking them (loose classes such as "offline" would otherwise keep every
-    // unit live). The margin covers the engine's reassociated sums.
+    // unit live). The margin covers the chain kernel's tick rounding (<= n half-ticks of elapsed).
     double horizon = 0.0;
     for (int i = 0; i < n; ++i) {
         double m = 0.0;
