@@ -28,7 +28,7 @@
 // anchors or contents changed are re-walked (at N=1024 the first one or two units).
 
 #ifndef SLO_CHAIN_THREADS
-#define SLO_CHAIN_THREADS 768  // k_chains<1> block size (24 warps)
+#define SLO_CHAIN_THREADS 896  // k_chains<1> block size (28 warps, 72 registers; 768 and 1024 measured slower)
 #endif
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
 constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
