@@ -30,6 +30,10 @@
 #ifndef SLO_CHAIN_THREADS
 #define SLO_CHAIN_THREADS 896  // k_chains<1> block size (28 warps, 72 registers; 768 and 1024 measured slower)
 #endif
+// block-size bound per units-per-lane (N <= 1024 / 2048 / 4096): more resident warps hide the
+// dependent-latency stalls until registers spill (measured: UPL 2 768 > 640 > 512, UPL 4 512 > 640)
+template <int UPL>
+__host__ __device__ constexpr int chain_threads() { return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? 768 : 512); }
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
 constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
 constexpr int kRndWords = 32;                        // words per proposal: 8 Philox blocks of 4
@@ -391,7 +395,7 @@ struct Delta {
 };
 
 template <int UPL, bool SMEM>
-__global__ void __launch_bounds__(UPL == 1 ? SLO_CHAIN_THREADS : 512, 1) k_chains(const ChainParams p) {
+__global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
     const int n = p.n, mb = p.mb;

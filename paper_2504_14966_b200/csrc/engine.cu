@@ -480,7 +480,7 @@ int configure_chains(slo_ctx* c) {
     const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(uint32_t);
     const size_t slot = slot_bytes<UPL>();
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
-    const int max_w = UPL == 1 ? SLO_CHAIN_THREADS / 32 : 16;
+    const int max_w = chain_threads<UPL>() / 32;
     c->smem_tab = tab_smem + slot <= c->smem_optin;
     return c->smem_tab ? configure_chains_t<UPL, true>(c, tab_smem, slot, max_w)
                        : configure_chains_t<UPL, false>(c, 0, slot, max_w);
