@@ -449,28 +449,29 @@ int count_levels(double t0, double t_thres, double tau) {
 // The max-dynamic-smem attribute is per function and device (process-wide). Raise it to the
 // device maximum once: concurrent contexts then never race on it, and no call blocks behind a
 // running instance of the kernel (setting it while the kernel runs serialises the callers).
-template <int UPL, bool SMEM>
+template <void (*K)(ChainParams)>
 cudaError_t ensure_smem_attr(int device, int bytes) {
     static std::mutex mu;
     static bool done[64] = {};
     std::lock_guard<std::mutex> g(mu);
     if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(k_chains<UPL, SMEM>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    const cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
     return e;
 }
 
-template <int UPL, bool SMEM>
-int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
-    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / slot);
-    W = std::max(1, std::min(W, c->chain_count));
-    c->smem = base + (size_t)W * slot;
-    CK((ensure_smem_attr<UPL, SMEM>(c->device, (int)c->smem_optin)));
+// W warps per block (bounded by max_w and shared memory), cpw chains per warp
+template <void (*K)(ChainParams)>
+int configure_kernel(slo_ctx* c, size_t base, size_t warp_bytes, int max_w, int cpw) {
+    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / warp_bytes);
+    W = std::max(1, std::min(W, (c->chain_count + cpw - 1) / cpw));
+    c->smem = base + (size_t)W * warp_bytes;
+    CK(ensure_smem_attr<K>(c->device, (int)c->smem_optin));
     int occ = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_chains<UPL, SMEM>, W * 32, c->smem));
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, W * 32, c->smem));
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
     c->block = W * 32;
-    c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
+    c->grid = std::min((c->chain_count + W * cpw - 1) / (W * cpw), c->sm_count * occ);
     if (c->prm.max_blocks > 0) c->grid = std::min(c->grid, c->prm.max_blocks);
     return SLO_OK;
 }
@@ -478,12 +479,12 @@ int configure_chains_t(slo_ctx* c, size_t base, size_t slot, int max_w) {
 template <int UPL>
 int configure_chains(slo_ctx* c) {
     const size_t tab_bytes = (size_t)c->n * c->mb * sizeof(uint32_t);
-    const size_t slot = slot_bytes<UPL>();
     const size_t tab_smem = (tab_bytes + 15) & ~(size_t)15;
+    const size_t slot = slot_bytes<UPL>();
     const int max_w = chain_threads<UPL>() / 32;
     c->smem_tab = tab_smem + slot <= c->smem_optin;
-    return c->smem_tab ? configure_chains_t<UPL, true>(c, tab_smem, slot, max_w)
-                       : configure_chains_t<UPL, false>(c, 0, slot, max_w);
+    return c->smem_tab ? configure_kernel<k_chains<UPL, true>>(c, tab_smem, slot, max_w, 1)
+                       : configure_kernel<k_chains<UPL, false>>(c, 0, slot, max_w, 1);
 }
 
 template <int UPL>
