@@ -298,7 +298,7 @@ __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UP
             const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
             const int cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, ln * UPL + k, lane, Eu, Fu);
             if (lane == ln) ls.W[k] = cnt;
-            sc2 += lane == 0 ? 32 : 0;
+            sc2 += 32;  // only lane 0's count is stored
         }
     }
 }
@@ -508,6 +508,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 uint16_t old_q = 0;
                 uint32_t ow0 = 0, ow1 = 0;
                 int w0 = 0, w1 = 0;
+                uint32_t sw_na = 0, sw_nb = 0;
+                int sw_pa = 0, sw_pb = 0;
+                bool sw_applied = false;  // swap written to shared memory
                 if (mv.kind == 1) {
                     // squeeze / delay: [lo, hi] held old batches [lo, osp], (osp, hi] and holds
                     // new batches [lo, nsp], (nsp, hi] (either part may be empty)
@@ -567,7 +570,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         }
                         need[kk] = pu + 31 >= lo && (pu <= hi || delta != 0) && nx.E[kk] <= dg;
                     }
-                    sc1 += lane == 0 ? (unsigned long long)(hi - lo + 1) : 0ull;
+                    sc1 += (unsigned)(hi - lo + 1);
                     __syncwarp();
                 } else if (mv.kind == 2) {
                     // swap: batches [sa, ea] and [sb, eb] (sa < sb, or the same batch) keep their
@@ -589,8 +592,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         eo = ent[q];
                         en = q == pa ? na : (q == pb ? nb : eo);
                     }
-                    __syncwarp();
-                    if (lane == 0) ent[pa] = (uint16_t)na, ent[pb] = (uint16_t)nb;
+                    // the swap is written to shared memory only when an SLO walk or an accept needs
+                    // it (the common rejected swap never touches the state)
+                    sw_na = na, sw_nb = nb, sw_pa = pa, sw_pb = pb;
                     const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
                     const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
                     const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
@@ -615,8 +619,16 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const bool chg = u == (pa >> 5) || u == (pb >> 5) || (pu >= sa && da != 0) || (pu >= sb && db != 0);
                         need[kk] = chg && nx.E[kk] <= dg;
                     }
-                    sc1 += lane == 0 ? (unsigned long long)(ea - sa + eb - sb + 2) : 0ull;
-                    __syncwarp();
+                    sc1 += (unsigned)(ea - sa + eb - sb + 2);
+                    bool any = false;
+#pragma unroll
+                    for (int kk = 0; kk < UPL; ++kk) any |= need[kk];
+                    if (__any_sync(FULL, any)) {  // the walks read the proposed state
+                        __syncwarp();
+                        if (lane == 0) ent[pa] = (uint16_t)na, ent[pb] = (uint16_t)nb;
+                        __syncwarp();
+                        sw_applied = true;
+                    }
                 } else {
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) need[kk] = false;
@@ -638,6 +650,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 }
                 if (accept) {
                     ++accs;
+                    if (mv.kind == 2 && !sw_applied) {
+                        __syncwarp();
+                        if (lane == 0) ent[sw_pa] = (uint16_t)sw_na, ent[sw_pb] = (uint16_t)sw_nb;
+                        __syncwarp();
+                    }
                     if (mv.kind == 1) {  // rebuilt batches: refresh the move flags around them
                         rebuild_flags(ent, bits, sqb, dlb, n, mb, magic, max(mv.lo - mb, 0) >> 5,
                                       min(mv.hi + mb, n - 1) >> 5, lane);
@@ -651,13 +668,13 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                         lane);
                         if (lane == 0) rc->g = f, rc->t = t_new, rc->n_met = nm;
                     }
-                } else {
+                } else if (mv.kind == 1 || sw_applied) {
                     __syncwarp();  // every lane is done reading the state (SLO walks) before the undo
                     if (mv.kind == 1) {
                         if (q <= mv.hi) ent[q] = old_q;
                         if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
-                    } else if (mv.kind == 2) {
-                        if (lane == 0) ent[min(mv.a, mv.b)] = (uint16_t)ow0, ent[max(mv.a, mv.b)] = (uint16_t)ow1;
+                    } else {
+                        if (lane == 0) ent[sw_pa] = (uint16_t)ow0, ent[sw_pb] = (uint16_t)ow1;
                     }
                     __syncwarp();
                 }
