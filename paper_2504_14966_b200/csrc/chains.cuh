@@ -239,9 +239,23 @@ __device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* b
     return mv;
 }
 
-// objective G = n / t (reference :278); the reciprocal form is used identically everywhere
+// objective G = n / t (reference :278); the reciprocal form is used identically everywhere a
+// score is recorded (the winner's g is compared bit-for-bit in the tests)
 __device__ __forceinline__ double objective(int nm, double tot) {
     return tot > 0.0 ? (double)nm * __drcp_rn(tot) : 0.0;
+}
+
+// the chain's working score: the same quotient from a hardware reciprocal estimate and two Newton
+// steps (relative error ~1e-16), a pure function of (nm, tot) like the exact one; only the
+// Metropolis comparisons use it, recorded scores use objective()
+__device__ __forceinline__ double objective_fast(int nm, double tot) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(tot));
+    double e = fma(-tot, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-tot, r, 1.0);
+    r = fma(r, e, r);
+    return tot > 0.0 ? (double)nm * r : 0.0;
 }
 
 // Philox rows drawn per refill (one per lane): 32 proposals, 16 where shared memory is tight
@@ -457,16 +471,16 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 copy_state<UPL, 3 * kBits>(ent, bits, p.start_ent, p.start_bits, lane);
                 cur = reinterpret_cast<const LaneState<UPL>*>(p.start_lane)[lane];
                 tot = p.start_obj[0], A = (int)p.start_obj[1], nm_cur = (int)p.start_obj[2];
-                f = best_f = objective(nm_cur, (double)tot * p.tick), props = 0, accs = 0;
+                f = best_f = objective_fast(nm_cur, (double)tot * p.tick), props = 0, accs = 0;
                 __syncwarp();
                 copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits, lane);
-                if (lane == 0) rc->g = f, rc->t = (double)tot * p.tick, rc->n_met = nm_cur;
+                if (lane == 0) rc->g = objective(nm_cur, (double)tot * p.tick), rc->t = (double)tot * p.tick, rc->n_met = nm_cur;
             } else if (n_my > 1) {  // resume a parked chain
                 copy_state<UPL, 3 * kBits>(ent, bits, p.st_ent + (size_t)c * kEnt, p.st_bits + (size_t)c * 3 * kBits,
                                            lane);
                 cur = parked[(size_t)c * 32 + lane];
                 tot = rc->cur_tot, A = rc->cur_A, nm_cur = rc->cur_n;
-                f = rc->cur_f, best_f = rc->g, props = rc->proposals, accs = rc->accepted;
+                f = rc->cur_f, best_f = rc->best_f, props = rc->proposals, accs = rc->accepted;
                 __syncwarp();
             }
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
@@ -638,7 +652,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 const int A_new = A + dA;
                 const int nm = A_new + live_met<UPL>(nx, dg);
                 const double t_new = (double)tot_new * p.tick;
-                const double f_new = objective(nm, t_new);
+                const double f_new = objective_fast(nm, t_new);
                 ++props;
                 bool accept = f_new > f;  // Metropolis (P:src/priority_mapper.cpp:385-391)
                 if (!accept) {
@@ -666,7 +680,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         best_f = f;
                         copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,
                                         lane);
-                        if (lane == 0) rc->g = f, rc->t = t_new, rc->n_met = nm;
+                        if (lane == 0) rc->g = objective(nm, t_new), rc->t = t_new, rc->n_met = nm;
                     }
                 } else if (mv.kind == 1 || sw_applied) {
                     __syncwarp();  // every lane is done reading the state (SLO walks) before the undo
@@ -686,7 +700,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 __syncwarp();
             }
             if (lane == 0) {
-                rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f;
+                rc->proposals = props, rc->accepted = accs, rc->levels = lev + 1, rc->cur_f = f, rc->best_f = best_f;
                 rc->cur_tot = tot, rc->cur_A = A, rc->cur_n = nm_cur;
                 rc->scan1 += sc1, rc->scan2 += sc2;
             }

@@ -40,7 +40,8 @@ constexpr uint32_t kTagMove = 0x5105c4edu;   // Philox counter word 3 for move d
 struct ChainRec {
     double g;      // best score of the chain (-1 = never started)
     double t;      // summed latency of the best
-    double cur_f;  // current score (multi-chain-per-warp state save)
+    double cur_f;  // current working score (multi-chain-per-warp state save)
+    double best_f; // best working score (K3 state save; g is its exact counterpart)
     long long cur_tot;  // current total latency in ticks (K3 state save)
     int cur_A, cur_n;   // current +inf-deadline count and SLO count (K3 state save)
     int n_met;
