@@ -217,11 +217,20 @@ def run_ours(args):
     from paper_2504_14966_b200 import engine as E
 
     world, rank, local = dist_env()
+    # SLO_BENCH_BACKEND=gloo runs the N > 1 path with host-side exchanges, ranks sharing GPUs
+    # round-robin (a functional check of the multi-rank code on a one-GPU box; not a measurement)
+    backend = os.environ.get("SLO_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
+    xdev = f"cuda:{local}" if backend == "nccl" else None  # exchange tensors
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
 
     w = synthetic_workload(args.n)
     c = S.table_coefficients()
@@ -270,11 +279,14 @@ def run_ours(args):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         eng.launch()
-        e1.record(stream)
-        bp, bs, res = eng.fetch()
-        if world > 1:  # best-of-GPUs: all-gather (g, t, chain), broadcast the winner's schedule
+        if world == 1:
+            e1.record(stream)
+            bp, bs, res = eng.fetch()
+        else:  # best-of-GPUs inside the step: all-gather (g, t, chain), broadcast the winner
+            bp, bs, res = eng.fetch()
             exchange_best(LocalBest(res.g, res.t, res.chain, np.asarray(ids, dtype=np.int32)[bp], bs), n,
-                          device=f"cuda:{local}")
+                          device=xdev)
+            e1.record(torch.cuda.current_stream())  # after the exchange completed
         return e0, e1, res
 
     for _ in range(args.warmup):
@@ -303,7 +315,7 @@ def run_ours(args):
     pos1 = float(sum(r[2] for r in results))
     pos2 = float(sum(r[3] for r in results))
     if dist:
-        t = torch.tensor([dev_ms, props, kern_ms, pos1, pos2], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([dev_ms, props, kern_ms, pos1, pos2], dtype=torch.float64, device=xdev or "cpu")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
@@ -325,13 +337,13 @@ def run_ours(args):
         seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids, c, cfg, mb)
         if dist:
             _, seq, sizes, (g, n_met) = exchange_best(
-                LocalBest(st.engine_g, st.engine_t, st.best_chain, seq, sizes, g, n_met), n, device=f"cuda:{local}",
+                LocalBest(st.engine_g, st.engine_t, st.best_chain, seq, sizes, g, n_met), n, device=xdev,
                 return_record=True)
         e2e_s += time.perf_counter() - t0
         e2e_props += st.proposals
         final = (n_met, g, st)
     if dist:
-        t = torch.tensor([e2e_s, e2e_props], dtype=torch.float64, device=f"cuda:{local}")
+        t = torch.tensor([e2e_s, e2e_props], dtype=torch.float64, device=xdev or "cpu")
         mx = t.clone()
         dist.all_reduce(mx, op=dist.ReduceOp.MAX)
         dist.all_reduce(t, op=dist.ReduceOp.SUM)
