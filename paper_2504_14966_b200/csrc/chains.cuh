@@ -167,52 +167,45 @@ struct Move {
 // The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the entry /
 // bitmask representation: up to 8 attempts of op = U[0,3) (squeeze / delay / swap), the first
 // that applies wins, else a forced swap. Lane j < 9 tests attempt j from its three Philox words
-// (attempt 8 is the forced swap) with one move-flag bit, the warp takes the first valid one --
-// the same move the sequential loop would pick -- and only that move's batch bounds are computed
-// (batch sizes from the entries, bounds from one 64-bit bit search).
-__device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* bits, const uint32_t* sqb,
-                                          const uint32_t* dlb, int n, int mb, uint32_t magic, const uint32_t* rw,
-                                          int lane) {
-    auto size_at = [&](int q) { return (int)__umulhi(ent[q], magic) + 1; };
-    uint32_t pk = 0;  // op << 30 | a | b << 13  (squeeze / delay: a = pos)
+// (attempt 8 is the forced swap) with one move-flag bit -- branch-free, all attempts at once --
+// and the warp takes the first valid one: the same move the sequential loop would pick.
+// Returns op << 30 | pos | b << 13 (squeeze / delay: pos; swap: a = pos, b), or kNoMove.
+constexpr uint32_t kNoMove = 0xffffffffu;
+__device__ __forceinline__ uint32_t draw_move(const uint16_t* ent, const uint32_t* sqb, const uint32_t* dlb, int n,
+                                              uint32_t magic, const uint32_t* rw, int lane) {
+    const uint32_t nn = (uint32_t)n;
+    const uint32_t first = __umulhi(ent[0], magic) + 1u;  // size of the first batch
     bool ok = false;
+    uint32_t pk = 0;
     if (lane < kAttempts && n > 0) {
         const uint32_t r0 = rw[3 * lane], r1 = rw[3 * lane + 1], r2 = rw[3 * lane + 2];
         const uint32_t op = lane < kAttempts - 1 ? lemire32(r0, 3) : 2u;
-        if (op == 0) {  // squeeze (:141-153): fails if the batch before pos's batch is full
-            const int first = size_at(0);
-            if (first < n) {
-                const int pos = first + (int)lemire32(r1, (uint32_t)(n - first));
-                ok = !((sqb[pos >> 5] >> (pos & 31)) & 1u);
-                pk = (uint32_t)pos;
-            }
-        } else if (op == 1) {  // delay (:155-170): fails if the next batch exists and is full
-            const int pos = (int)lemire32(r1, (uint32_t)n);
-            ok = !((dlb[pos >> 5] >> (pos & 31)) & 1u);
-            pk = 1u << 30 | (uint32_t)pos;
-        } else if (n >= 2) {  // swap (:172-180)
-            const int a = (int)lemire32(r1, (uint32_t)n);
-            int b = (int)lemire32(r2, (uint32_t)(n - 1));
-            if (b >= a) ++b;
-            ok = true;
-            pk = 2u << 30 | (uint32_t)a | (uint32_t)b << 13;
-        }
+        const uint32_t a = lemire32(r1, nn);                   // delay position / first swap position
+        const uint32_t ps = first + lemire32(r1, nn - first);  // squeeze position (:141-153)
+        uint32_t b = lemire32(r2, nn - 1);                     // swap (:172-180)
+        b += b >= a ? 1u : 0u;
+        const uint32_t pos = op == 0 ? ps : a;
+        const uint32_t qf = min(pos, nn - 1);
+        // squeeze fails if the batch before pos's batch is full; delay if the next one is full
+        const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
+        ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
+        pk = op << 30 | pos | (op == 2 ? b << 13 : 0u);
     }
     const unsigned vm = __ballot_sync(FULL, ok);
+    return vm ? __shfl_sync(FULL, pk, __ffs(vm) - 1) : kNoMove;
+}
+
+// the batch rebuild of a squeeze (op 0) or delay (op 1) of position pos: batch bounds from one
+// bit search, sizes from the entries
+__device__ __forceinline__ Move range_move(const uint16_t* ent, const uint32_t* bits, int n, uint32_t magic,
+                                           uint32_t op, int pos) {
+    auto size_at = [&](int q) { return (int)__umulhi(ent[q], magic) + 1; };
     Move mv;
-    mv.kind = 0;
-    if (!vm) return mv;
-    pk = __shfl_sync(FULL, pk, __ffs(vm) - 1);
-    const uint32_t op = pk >> 30;
-    const int pos = (int)(pk & 0x1fffu);
-    if (op == 2) {
-        mv.kind = 2;
-        mv.a = pos, mv.b = (int)((pk >> 13) & 0x1fffu);
-    } else if (op == 0) {
+    mv.kind = 1;
+    if (op == 0) {
         const int sk = prev_end16(bits, pos) + 1;
         const int prev_size = size_at(sk - 1);
         const int ek = sk + size_at(sk) - 1;
-        mv.kind = 1;
         mv.lo = sk - prev_size, mv.hi = ek, mv.split = sk;
         mv.sz1 = prev_size + 1, mv.sz2 = ek - sk;
         mv.ra = sk, mv.rb = pos, mv.dir = 1;
@@ -220,7 +213,6 @@ __device__ __forceinline__ Move draw_move(const uint16_t* ent, const uint32_t* b
     } else {
         const int ek = next_end16(bits, pos);
         const int sk = ek - size_at(pos) + 1;
-        mv.kind = 1;
         mv.ra = pos, mv.dir = -1;
         if (ek < n - 1) {
             const int next_size = size_at(ek + 1);
@@ -511,7 +503,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     __syncwarp();
                 }
                 const uint32_t* rw = rnd + kRndWords * (it & (kRows - 1));
-                const Move mv = draw_move(ent, bits, sqb, dlb, n, mb, magic, rw, lane);
+                const uint32_t pk = draw_move(ent, sqb, dlb, n, magic, rw, lane);
+                const uint32_t op = pk >> 30;
+                const int kind = op == 3u ? 0 : (op == 2u ? 2 : 1);
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
@@ -525,7 +519,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 uint32_t sw_na = 0, sw_nb = 0;
                 int sw_pa = 0, sw_pb = 0;
                 bool sw_applied = false;  // swap written to shared memory
-                if (mv.kind == 1) {
+                int r_lo = 0, r_hi = -1;   // squeeze / delay: the rebuilt range
+                if (kind == 1) {
+                    const Move mv = range_move(ent, bits, n, magic, op, (int)(pk & 0x1fffu));
+                    r_lo = mv.lo, r_hi = mv.hi;
                     // squeeze / delay: [lo, hi] held old batches [lo, osp], (osp, hi] and holds
                     // new batches [lo, nsp], (nsp, hi] (either part may be empty)
                     q = mv.lo + lane;
@@ -586,10 +583,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                     sc1 += (unsigned)(hi - lo + 1);
                     __syncwarp();
-                } else if (mv.kind == 2) {
+                } else if (kind == 2) {
                     // swap: batches [sa, ea] and [sb, eb] (sa < sb, or the same batch) keep their
                     // sizes; lanes 0-15 cover the first, 16-31 the second
-                    const int pa = min(mv.a, mv.b), pb = max(mv.a, mv.b);
+                    const int sa0 = (int)(pk & 0x1fffu), sb0 = (int)((pk >> 13) & 0x1fffu);
+                    const int pa = min(sa0, sb0), pb = max(sa0, sb0);
                     const uint32_t ea_ = ent[pa], eb_ = ent[pb];
                     ow0 = ea_, ow1 = eb_;
                     const uint32_t za = __umulhi(ea_, magic);  // batch size - 1
@@ -664,14 +662,14 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 }
                 if (accept) {
                     ++accs;
-                    if (mv.kind == 2 && !sw_applied) {
+                    if (kind == 2 && !sw_applied) {
                         __syncwarp();
                         if (lane == 0) ent[sw_pa] = (uint16_t)sw_na, ent[sw_pb] = (uint16_t)sw_nb;
                         __syncwarp();
                     }
-                    if (mv.kind == 1) {  // rebuilt batches: refresh the move flags around them
-                        rebuild_flags(ent, bits, sqb, dlb, n, mb, magic, max(mv.lo - mb, 0) >> 5,
-                                      min(mv.hi + mb, n - 1) >> 5, lane);
+                    if (kind == 1) {  // rebuilt batches: refresh the move flags around them
+                        rebuild_flags(ent, bits, sqb, dlb, n, mb, magic, max(r_lo - mb, 0) >> 5,
+                                      min(r_hi + mb, n - 1) >> 5, lane);
                         __syncwarp();
                     }
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
@@ -682,10 +680,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                         lane);
                         if (lane == 0) rc->g = objective(nm, t_new), rc->t = t_new, rc->n_met = nm;
                     }
-                } else if (mv.kind == 1 || sw_applied) {
+                } else if (kind == 1 || sw_applied) {
                     __syncwarp();  // every lane is done reading the state (SLO walks) before the undo
-                    if (mv.kind == 1) {
-                        if (q <= mv.hi) ent[q] = old_q;
+                    if (kind == 1) {
+                        if (q <= r_hi) ent[q] = old_q;
                         if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
                     } else {
                         if (lane == 0) ent[sw_pa] = (uint16_t)ow0, ent[sw_pb] = (uint16_t)ow1;
