@@ -293,7 +293,7 @@ __device__ __forceinline__ void rebuild_flags(const uint16_t* ent, const uint32_
 template <int UPL, bool SMEM>
 __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UPL>& ls, const uint16_t* ent,
                                            const uint32_t* bits, const TabRef& tab, const long long* dt, int n,
-                                           int mb, int lane, unsigned long long& sc2) {
+                                           int mb, int lane, unsigned& sc2) {
 #pragma unroll
     for (int k = 0; k < UPL; ++k) {
         unsigned mask = __ballot_sync(FULL, need[k]);
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
         ls.E[k] = Es[lane * UPL + k], ls.F[k] = Fs[lane * UPL + k], ls.W[k] = 0;
         need[k] = ls.E[k] <= p.dg;
     }
-    unsigned long long sc2 = 0;
+    unsigned sc2 = 0;
     const TabRef tab{p.xt, 0u};
     walk_units<UPL, false>(need, ls, ent, bits, tab, p.dt, n, p.mb, lane, sc2);
     const int nm = live_met<UPL>(ls, p.dg);
@@ -439,7 +439,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     long long tot = 0;   // committed total (ticks)
     int A = 0, nm_cur = 0;
     double f = 0.0, best_f = 0.0;
-    unsigned long long props = 0, accs = 0;
+    unsigned props = 0, accs = 0;  // per chain and launch (< 2^32: levels * iter)
     int stop = 0;
     const uint32_t nn = (uint32_t)n;
     const uint32_t magic = p.magic;
@@ -458,7 +458,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
             const int c = gw + k * TW;
             const uint32_t cid = (uint32_t)(p.chain_begin + c);
             ChainRec* rc = p.rec + c;
-            unsigned long long sc1 = 0, sc2 = 0;
+            unsigned sc1 = 0, sc2 = 0;
             if (lev == 0) {  // every chain starts from the shared start state
                 copy_state<UPL, 3 * kBits>(ent, bits, p.start_ent, p.start_bits, lane);
                 cur = reinterpret_cast<const LaneState<UPL>*>(p.start_lane)[lane];
@@ -472,7 +472,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                            lane);
                 cur = parked[(size_t)c * 32 + lane];
                 tot = rc->cur_tot, A = rc->cur_A, nm_cur = rc->cur_n;
-                f = rc->cur_f, best_f = rc->best_f, props = rc->proposals, accs = rc->accepted;
+                f = rc->cur_f, best_f = rc->best_f, props = (unsigned)rc->proposals, accs = (unsigned)rc->accepted;
                 __syncwarp();
             }
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
