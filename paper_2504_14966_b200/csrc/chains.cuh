@@ -156,7 +156,7 @@ __device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits,
     return __popc(__ballot_sync(FULL, met));
 }
 
-struct Move {
+struct Move {         // also the move record of K2 (replay.cuh)
     int kind;        // 0 none, 1 range (squeeze/delay), 2 swap
     int lo, hi, split, sz1, sz2;
     int ra, rb, dir; // rotation on [ra, rb]; dir +1 right, -1 left
@@ -393,12 +393,6 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     reinterpret_cast<LaneState<UPL>*>(p.start_lane)[lane] = ls;
     if (lane == 0) p.start_obj[2] = p.start_obj[1] + nm;
 }
-
-// one proposal's effect on the objective, computed by the warp from the rebuilt batches
-struct Delta {
-    long long dtot;  // change of the total latency (ticks)
-    int dA;          // change of the +inf-deadline count
-};
 
 template <int UPL, bool SMEM>
 __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainParams p) {
