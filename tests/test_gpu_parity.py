@@ -464,3 +464,58 @@ def test_budget_stops_early():
     assert r.stats.kernel_ms < 2.0 + 0.1  # the budget is checked every 8 proposals
     assert r.best.schedule.is_partition_of(w.ids(), 4)
     assert r.best.g >= max(r.stats.g_sorted_start, r.stats.g_input_start)
+
+
+def _start_schedule(n, mb, kind, seed):
+    rs = np.random.default_rng(seed)
+    perm = [int(x) for x in rs.permutation(n)]
+    if kind == "full":
+        sizes = [mb] * (n // mb) + ([n % mb] if n % mb else [])
+    else:  # mixed sizes: squeezes and delays apply often
+        sizes, left, k = [], n, 0
+        while left:
+            s = min(1 + (k % mb), left)
+            sizes.append(s)
+            left -= s
+            k += 1
+    return perm, sizes
+
+
+@pytest.mark.parametrize("n,mb,three,kind,chains", [(64, 4, True, "full", 1), (64, 4, False, "mixed", 1),
+                                                     (200, 8, True, "mixed", 1), (150, 4, False, "full", 3),
+                                                     (40, 16, True, "mixed", 2), (37, 2, False, "mixed", 1),
+                                                     (1500, 4, True, "mixed", 1), (3000, 4, False, "full", 1)])
+def test_chain_trajectory_matches_model(eng, n, mb, three, kind, chains):
+    """K3 chains follow exactly the trajectory of a plain-Python model of their specification
+    (tests/k3_model.py: the reference's proposal discipline on Philox words, the tick-grid
+    objective evaluated from scratch, fp32 Metropolis): same winner schedule, (n_met, t, g),
+    proposals and accepted counts. This pins the kernel's incremental scoring (rebuilt-batch
+    deltas, anchor shifts, SLO walks), its move flags and its lazy swap writes."""
+    import k3_model as K
+    w = _three_class(n, 70 + n) if three else S.generate_mixed(n, 70 + n)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    perm, sizes = _start_schedule(n, mb, kind, n)
+    start, q = [], 0
+    for s in sizes:
+        start.append(perm[q:q + s])
+        q += s
+    f0 = prob.score(start)[2]
+    seed, t0, t_thres, tau, it = 12345 + n, 100.0, 20.0, 0.8, 40
+    scale = t0 / f0 if f0 > 0 else t0
+    bp, bs, r = eng.anneal_chains(perm, sizes, chains=chains, t0=t0, t_thres=t_thres, tau=tau, iter=it, seed=seed,
+                                  objective_scale=scale)
+    runs = [K.run_chain(prob, start, cid, seed, t0, t_thres, tau, it, scale) for cid in range(chains)]
+    win = min(range(chains), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    assert r.chain == win
+    assert r.proposals == sum(x["proposals"] for x in runs)
+    assert r.accepted == sum(x["accepted"] for x in runs)
+    assert (r.n_met, r.t, r.g) == runs[win]["best"]
+    got, q = [], 0
+    for s in bs:
+        got.append([int(x) for x in bp[q:q + s]])
+        q += s
+    assert got == runs[win]["best_batches"]

@@ -171,3 +171,42 @@ def test_deadline_first_candidate():
     ev_dl = S.evaluate(S.deadline_first_candidate(w, w.ids(), c, 4), c, w)
     ev_sorted = S.evaluate(s_sorted, c, w)
     assert ev_dl.n >= 74 and ev_dl.n > ev_sorted.n and ev_dl.g > ev_sorted.g
+
+
+def test_k3_model_philox_and_tick_objective():
+    """The K3 model used by the GPU trajectory tests (tests/k3_model.py): its Philox matches the
+    Random123 known answers, and its tick-grid objective is within the grid's rounding of the
+    exact objective (CostModel::score) on random schedules."""
+    import k3_model as K
+    f = 0xFFFFFFFF
+    assert K.philox4x32_10([0, 0, 0, 0], [0, 0]) == [0x6627E8D5, 0xE169C58D, 0xBC57AC4C, 0x9B00DBD8]
+    assert K.philox4x32_10([f, f, f, f], [f, f]) == [0x408F276D, 0x41C83B0E, 0xA20BC7C6, 0x6D5451FD]
+    assert K.philox4x32_10([0x243F6A88, 0x85A308D3, 0x13198A2E, 0x03707344], [0xA4093822, 0x299F31D0]) == \
+        [0xD16CFE09, 0x94FDCCEB, 0x5001E420, 0x24126EA1]
+    import numpy as np
+    from oracle import TABLE_COEFFS
+    from oracle import port
+    w = S.generate_mixed(48, 3)
+    a = w.arrays
+    from oracle import FlatWorkload
+    fw = FlatWorkload(**{k: a[k] for k in ("id", "cls", "in_len", "true_out", "pred_out", "arrival", "class_id",
+                                           "kind", "e2e", "ttft", "tpot")})
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, S.table_coefficients(), 4)
+    tick = 2.0 ** -int(np.floor(np.log2((2 ** 27 - 1) / ex.max())))
+    prob = K.TickProblem(ex, dl, tick)
+    rs = np.random.default_rng(5)
+    for _ in range(20):
+        perm = rs.permutation(48)
+        sizes, left = [], 48
+        while left:
+            k = int(rs.integers(1, min(4, left) + 1))
+            sizes.append(k)
+            left -= k
+        batches, q = [], 0
+        for s in sizes:
+            batches.append([int(x) for x in perm[q:q + s]])
+            q += s
+        nm, t, g = prob.score(batches)
+        o_n, o_t, o_g = port.score_batch(fw, TABLE_COEFFS, ids, 4, perm[None, :].astype(np.int32), [sizes])
+        assert abs(t - o_t[0]) <= 48 * 48 * tick and abs(nm - o_n[0]) <= 1
