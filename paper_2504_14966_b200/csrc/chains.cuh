@@ -36,8 +36,9 @@ template <int UPL>
 __host__ __device__ constexpr int chain_threads() { return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? 768 : 512); }
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
 constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
-constexpr int kRndWords = 32;                        // words per proposal: 8 Philox blocks of 4
-static_assert(kAccWord + 2 <= kRndWords, "Philox row too small");
+constexpr int kRndWords = 32;                        // row stride (words) per proposal
+constexpr int kRndBlocks = (kAccWord + 1 + 3) / 4;   // Philox blocks a row needs (7: words 0..27)
+static_assert(4 * kRndBlocks <= kRndWords, "Philox row too small");
 constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
 constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
 constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
@@ -488,7 +489,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         // Philox block b of a row = counter (proposal, chain, b, tag)
                         uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
 #pragma unroll
-                        for (int b = 0; b < kRndWords / 4; ++b) {
+                        for (int b = 0; b < kRndBlocks; ++b) {
                             uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
                             philox10(r, p.key0, p.key1);
                             dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
