@@ -1,10 +1,29 @@
+# One GPU verification + measurement pass (run on a B200 box from the repo root, e.g.
+#   gpurun --timeout 3000 -- 'bash tools/gpu_round.sh'
+# ); outputs land in gpurun_out/. The summaries committed under profiles/<round>/ come from these
+# files: python tools/ncu_summary.py gpurun_out/k_chains.ncu-rep --proposals <printed> --tag <round>
+#   --launches gpurun_out/launches.csv
 set -x
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
 timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1
+# fixed-work capture of the chain kernel in the bench configuration (prints the proposal count)
+timeout 300 python tools/prof_chains.py --bench --reps 3 > gpurun_out/prof_chains.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 \
+    -o gpurun_out/k_chains python tools/prof_chains.py --bench > gpurun_out/ncu_full.log 2>&1
+# the bench's roofline reads profiles/r1/k_chains_summary.json: refresh it from this capture
+# (prof_chains.py --bench evaluates 16384 chains x 7 levels x 100 proposals = 11468800)
+python tools/ncu_summary.py gpurun_out/k_chains.ncu-rep --proposals 11468800 --tag r1 > /dev/null 2>&1 && \
+    cp profiles/r1/k_chains_summary.json gpurun_out/k_chains_summary.json
+# launch list of the bench command (times are cold-cache and serialised: use the shares)
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
+    --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 2 \
+    > gpurun_out/b_ncu.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/b_ncu.log 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 -o gpurun_out/k_chains_full python tools/prof_chains.py 1024 16384 1 > gpurun_out/ncu_full.log 2>&1
+for t in memcheck racecheck synccheck initcheck; do
+  timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > gpurun_out/san_$t.log 2>&1
+done
 tail -3 gpurun_out/pytest_gpu.log
-cat gpurun_out/bench.json
+cat gpurun_out/prof_chains.log gpurun_out/bench.json
