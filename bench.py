@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--t0", type=float, default=500.0)
     ap.add_argument("--t-thres", type=float, default=20.0)
     ap.add_argument("--tau", type=float, default=0.7)
-    ap.add_argument("--iter", type=int, default=100)
+    ap.add_argument("--iter", type=int, default=150)  # the device budget, not the ladder, ends a decision
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
@@ -266,9 +266,10 @@ def run_ours(args):
     except Exception:
         pass
     # the whole decision fits the budget: host preparation (candidates, tables, deadline-first start
-    # on two threads, ~0.5 ms), launch/argmax/copies (~0.1 ms), the exact final evaluation and the
-    # Python call (~0.3 ms) take the last 1.1 ms; the kernel stops within 8 proposals of its budget
-    kernel_budget_ms = max(0.0, args.budget_ms - 1.1)
+    # on two threads, ~0.75 ms), launch/argmax/copies (~0.1 ms), the exact final evaluation and the
+    # Python call (~0.2 ms) take ~1.05 ms, 1.3 ms is reserved; the kernel stops within 8 proposals
+    # of its budget
+    kernel_budget_ms = max(0.0, args.budget_ms - 1.3)
     eng.prepare(start_perm, start_sizes, t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                 objective_scale=scale, chains=chains_total, chain_begin=cb, chain_end=ce,
                 budget_ms=kernel_budget_ms, scale_ladder=SCALE_LADDER)
