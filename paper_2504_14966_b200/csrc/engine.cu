@@ -1,20 +1,20 @@
 // B200 annealing engine: hand-written sm_100a kernels behind include/slosched_gpu.h.
 //
-// Data layout (see DESIGN.md):
+// Data layout (see DESIGN.md section 3):
 //   * Tables: HBM structure-of-arrays exec[mb][n], deadline[mb][n] (uploaded by
-//     slo_problem_set) interleaved once on device into tab[mb][n] = {exec, deadline}
-//     (16 B), then staged into shared memory by every CTA of the chain kernel with
-//     coalesced 16-byte loads (once per block).
-//   * Chain state (one chain per warp): 16-bit position entries
-//     ent = dense_index | (batch_size-1) << 12 stored "lane-major" -- position
-//     q = lane*P + j lives at ent[j*32 + lane] so every lane reads its own
-//     contiguous run of P positions with conflict-free shared loads -- plus a linear
-//     batch-end bitmask (bit q set iff q ends its batch).
+//     slo_problem_set). One device pass (k_tables) derives the exact pair table
+//     tab[mb][n] = {exec, deadline} (16 B, for K1, K2 and the exhaustive oracle) and the chain
+//     kernel's tick tables: xt[mb][n] (u32 exec ticks | +inf-deadline flag, staged into shared
+//     memory by every CTA of K3 with coalesced 16-byte loads) and dt[mb][n] (int64 deadline ticks).
+//   * Chain state (one chain per warp, shared memory): 16-bit position entries
+//     ent[q] = (batch_size-1) * n + dense_index (the table index itself), a linear batch-end
+//     bitmask (bit q set iff q ends its batch) and two move-flag bitmasks (K3).
 //
 // Kernels:
 //   k_eval_exact   K1: one candidate per thread, sequential reference arithmetic.
 //   k_replay       K2: one chain per warp, xoshiro256++ and FlatSchedule moves, exact.
-//   k_chains<P>    K3: one chain per warp, Philox4x32-10 moves, incremental objective.
+//   k_start<U>     K3 prologue: the shared start state's unit anchors and move flags.
+//   k_chains<U>    K3: one chain per warp, Philox4x32-10 moves, tick-exact delta objective.
 //   k_argmax       K4: best-of-chains (g desc, t asc, chain asc) + winner copy.
 // P: = /root/reference/proj/.
 #include <cuda_runtime.h>
