@@ -98,8 +98,8 @@ typedef struct {
 } slo_chain_params;
 
 typedef struct {
-    double g;            /* best score found (engine evaluator) */
-    double t;            /* its summed latency */
+    double g;            /* best score found (chain kernel: exact on the 2^-k ms tick grid) */
+    double t;            /* its summed latency (ticks x tick) */
     int32_t n_met;
     int32_t chain;       /* winning chain id (ties: lower t, then lower id) */
     uint64_t proposals;  /* summed over the chains run */
@@ -107,8 +107,8 @@ typedef struct {
     int32_t chains_run;  /* chains that started */
     int32_t levels_run;  /* temperature levels completed by the slowest chain */
     float kernel_ms;     /* device time of the annealing launches (CUDA events) */
-    uint64_t positions_pass1; /* positions walked by the incremental evaluator (pass 1: */
-    uint64_t positions_pass2; /*   batch makespans, pass 2: elapsed/met/latency sums) */
+    uint64_t positions_pass1; /* Philox mode: positions of the rebuilt batches scored */
+    uint64_t positions_pass2; /*   and positions re-walked for SLO counts (replay: 0) */
 } slo_chain_result;
 
 /* Run chains from the start schedule (dense indices in position order + batch sizes) and
