@@ -15,8 +15,9 @@
  *   slo_anneal_chains   the annealing loop of anneal(), P:src/priority_mapper.cpp:368-402:
  *                       SLO_RNG_XOSHIRO_REPLAY reproduces the reference walk bit-for-bit
  *                       (FlatSchedule moves :104-199, Rng P:include/slosched/rng.hpp:14-100);
- *                       SLO_RNG_PHILOX runs thousands of independent chains (one per warp)
- *                       plus a grid-wide best-of-chains argmax.
+ *                       SLO_RNG_PHILOX runs thousands of independent chains (one per warp),
+ *                       each move scored from the batches it rebuilds on an integer tick
+ *                       grid (slo_problem_tick_ms), plus a grid-wide best-of-chains argmax.
  *
  * Conventions: every function returns an slo_status; on failure slo_last_error()
  * (thread-local) holds the message. No exceptions cross the ABI. Output buffers are
