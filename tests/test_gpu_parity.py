@@ -519,3 +519,43 @@ def test_chain_trajectory_matches_model(eng, n, mb, three, kind, chains):
         got.append([int(x) for x in bp[q:q + s]])
         q += s
     assert got == runs[win]["best_batches"]
+
+
+@pytest.mark.parametrize("scale", [1e-3, 1e4])
+def test_chain_trajectory_matches_model_at_other_time_scales(eng, scale):
+    """The tick grid follows the problem's scale (largest exec < 2^27 ticks): the same queue with
+    every exec time and deadline multiplied by `scale` still matches the model exactly."""
+    import k3_model as K
+    n, mb = 96, 4
+    w = _three_class(n, 5)
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, S.table_coefficients(), mb)
+    ex, dl = ex * scale, dl * scale
+    eng.set_problem(ex, dl)
+    tick = eng.tick_ms
+    assert np.rint(ex / tick).max() < 2 ** 27 and np.rint(ex / tick).max() >= 2 ** 26
+    prob = K.TickProblem(ex, dl, tick)
+    perm, sizes = _start_schedule(n, mb, "mixed", 3)
+    start, q = [], 0
+    for s in sizes:
+        start.append(perm[q:q + s])
+        q += s
+    f0 = prob.score(start)[2]
+    seed, t0, t_thres, tau, it = 99, 100.0, 20.0, 0.8, 40
+    bp, bs, r = eng.anneal_chains(perm, sizes, chains=1, t0=t0, t_thres=t_thres, tau=tau, iter=it, seed=seed,
+                                  objective_scale=t0 / f0)
+    model = K.run_chain(prob, start, 0, seed, t0, t_thres, tau, it, t0 / f0)
+    assert (r.n_met, r.t, r.g) == model["best"] and r.accepted == model["accepted"]
+
+
+def test_chains_reject_negative_exec_times(eng):
+    """The chain kernel's integer grid needs finite, non-negative exec times: anything else is a
+    DataError from the engine, never a silent result."""
+    n, mb = 16, 2
+    ex = np.full((mb, n), 10.0)
+    dl = np.full((mb, n), 100.0)
+    ex[1, 3] = -1.0
+    eng.set_problem(ex, dl)
+    with pytest.raises(Exception) as e:
+        eng.anneal_chains(list(range(n)), [2] * (n // 2), chains=4, t0=50.0, iter=5)
+    assert "non-negative" in str(e.value)
