@@ -36,7 +36,7 @@ template <int UPL>
 __host__ __device__ constexpr int chain_threads() { return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? 768 : 512); }
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
 constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
-constexpr int kRndWords = 32;                        // row stride (words) per proposal
+constexpr int kRndWords = 32;                        // words of a proposal's row (stride: rnd_stride)
 constexpr int kRndBlocks = (kAccWord + 1 + 3) / 4;   // Philox blocks a row needs (7: words 0..27)
 static_assert(4 * kRndBlocks <= kRndWords, "Philox row too small");
 constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
@@ -255,11 +255,17 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
 template <int UPL>
 __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : 16; }
 
+// row stride (words): 36 = 9 x 16 B puts the 32 lanes' row stores on distinct bank groups
+// (conflict-free uint4 stores); where shared memory bounds the resident warps (2-4 units per
+// lane) the dense stride keeps one more warp per SM
+template <int UPL>
+__host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : kRndWords; }
+
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
     // entries + a zero word (bits[-1]) and padding + batch-end bitmask + two move-flag bitmasks +
     // Philox rows (next_end16 may read one word past the bitmask: the first flag word)
-    return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * kRndWords * 4;
+    return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4;
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -487,7 +493,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     __syncwarp();                // every lane is done reading the previous rows
                     if (lane < kRows) {
                         // Philox block b of a row = counter (proposal, chain, b, tag)
-                        uint4* dst = reinterpret_cast<uint4*>(rnd + kRndWords * lane);
+                        uint4* dst = reinterpret_cast<uint4*>(rnd + rnd_stride<UPL>() * lane);
 #pragma unroll
                         for (int b = 0; b < kRndBlocks; ++b) {
                             uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
@@ -497,7 +503,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                     __syncwarp();
                 }
-                const uint32_t* rw = rnd + kRndWords * (it & (kRows - 1));
+                const uint32_t* rw = rnd + rnd_stride<UPL>() * (it & (kRows - 1));
                 const uint32_t pk = draw_move(ent, sqb, dlb, n, magic, rw, lane);
                 const uint32_t op = pk >> 30;
                 const int kind = op == 3u ? 0 : (op == 2u ? 2 : 1);
