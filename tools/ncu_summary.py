@@ -112,6 +112,17 @@ def main():
         "dram_bytes": dram,
         "dram_bytes_per_proposal": dram / args.proposals,
         "stall_samples_top": [[k, int(v)] for v, k in stalls],
+        # the counters SURVEY section 8(d) names: shared-memory wavefronts and bank conflicts, issue
+        # and pipe utilisation, resident warps (per proposal where it is a count)
+        "shared_memory": {
+            "wavefronts_per_proposal": (num(rw.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum")) or 0) / args.proposals,
+            "bank_conflicts_per_proposal": (num(rw.get("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum")) or 0) / args.proposals,
+            "wavefronts_pct_of_peak": num(rw.get("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed")),
+        },
+        "pipes_pct_of_peak_active": {k: num(rw.get(f"sm__inst_executed_pipe_{k}.avg.pct_of_peak_sustained_active"))
+                                     for k in ("alu", "fma", "fp64", "lsu", "xu", "adu", "cbu", "uniform")},
+        "issue_active_pct": num(rw.get("smsp__issue_active.avg.pct_of_peak_sustained_active")),
+        "warps_active_per_sm": num(rw.get("sm__warps_active.avg.per_cycle_active")),
         "instructions_by_function": functions(args.rep),
     }
     if args.launches:
