@@ -559,3 +559,45 @@ def test_chains_reject_negative_exec_times(eng):
     with pytest.raises(Exception) as e:
         eng.anneal_chains(list(range(n)), [2] * (n // 2), chains=4, t0=50.0, iter=5)
     assert "non-negative" in str(e.value)
+
+
+def test_chain_trajectory_random_shapes(eng):
+    """Randomised shapes (N 2..300, mb 1..16, random start batchings, scales, ladders, 1-2 chains):
+    K3 and the Python model agree exactly on every case."""
+    import random
+    import k3_model as K
+    rs = random.Random(2024)
+    for case in range(24):
+        n = rs.choice([2, 3, 5, 9, 17, 33, 64, 100, 150, 257, 300])
+        mb = rs.choice([1, 2, 3, 4, 5, 8, 16])
+        w = _three_class(n, case) if rs.random() < 0.5 else S.generate_mixed(n, case)
+        ids = sorted(w.ids())
+        ex, dl = E.build_tables(w, ids, S.table_coefficients(), mb)
+        eng.set_problem(ex, dl)
+        prob = K.TickProblem(ex, dl, eng.tick_ms)
+        perm = list(range(n))
+        rs.shuffle(perm)
+        sizes, left = [], n
+        while left:
+            s = rs.randint(1, min(mb, left))
+            sizes.append(s)
+            left -= s
+        start, q = [], 0
+        for s in sizes:
+            start.append(perm[q:q + s])
+            q += s
+        f0 = prob.score(start)[2]
+        t0, tau, it = rs.choice([30.0, 100.0, 500.0]), rs.choice([0.5, 0.8]), rs.choice([7, 20, 33])
+        scale = (t0 / f0 if f0 > 0 else t0) * rs.choice([1.0, 1e3, 1e-2])
+        seed, chains = rs.randrange(1 << 40), rs.choice([1, 2])
+        bp, bs, r = eng.anneal_chains(perm, sizes, chains=chains, t0=t0, t_thres=20.0, tau=tau, iter=it, seed=seed,
+                                      objective_scale=scale)
+        runs = [K.run_chain(prob, start, cid, seed, t0, 20.0, tau, it, scale) for cid in range(chains)]
+        win = min(range(chains), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+        got, q = [], 0
+        for s in bs:
+            got.append([int(x) for x in bp[q:q + s]])
+            q += s
+        assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                       sum(x["accepted"] for x in runs)), case
+        assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"], case
