@@ -585,10 +585,14 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
         c->smem = (size_t)(c->block / 32) * slot;
         c->grid = (chains + c->block / 32 - 1) / (c->block / 32);
         CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)c->smem_optin));
-        // carve out only the shared memory the slot needs: the rest of the SM's 256 KB stays L1,
-        // which holds the (exec, deadline) table for the per-proposal gathers
+        // carve out only the shared memory the resident chains need (one warp each, as many per SM
+        // as there are chains per SM, up to what fits): the rest of the SM's 256 KB stays L1, which
+        // holds the (exec, deadline) table for the per-proposal gathers. A single chain is
+        // latency-bound (one warp), so co-resident chains multiply throughput.
+        const size_t per_sm = std::max<size_t>(1, std::min<size_t>((chains + c->sm_count - 1) / c->sm_count,
+                                                                   c->smem_optin / c->smem));
         CK(cudaFuncSetAttribute(k_replay, cudaFuncAttributePreferredSharedMemoryCarveout,
-                                (int)std::min<size_t>(100, (c->smem * 100 + c->smem_optin - 1) / c->smem_optin + 1)));
+                                (int)std::min<size_t>(100, (per_sm * c->smem * 100 + c->smem_optin - 1) / c->smem_optin + 1)));
         c->UPL = npad / 32;  // words of the state, for fetch
         ReplayParams& rp = c->rp;
         rp.n = n, rp.mb = c->mb, rp.chains = chains, rp.magic = (1ull << 32) / (uint64_t)n + 1;
