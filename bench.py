@@ -400,11 +400,12 @@ def run_ours(args):
                          f"proposals each) on the same N={n} mb={mb} workload; {cw / 1e3:.1f} s wall; "
                          f"host {lscpu_model()}",
                "attainment": cn / n, "g_req_per_ms": cg}
+    cfg_name = {1024: "configs[2]", 4096: "configs[3] (one GPU's shard)"}.get(n, f"N={n}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "i64", "data": "synthetic",
-        "config": {"workload": f"configs[2]: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
+        "config": {"workload": f"{cfg_name}: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
                                f"predictions, {args.chains} chains/GPU, {args.budget_ms} ms budget",
                    "n_requests": n, "max_batch": mb, "chains_per_gpu": args.chains, "chains_total": chains_total,
                    "budget_ms": args.budget_ms, "kernel_budget_ms": kernel_budget_ms,
