@@ -643,9 +643,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
         CK(c->st_bits.reserve(cc * 3 * bit_words * sizeof(uint32_t)));
         CK(c->st_sum.reserve(cc * 32 * csb));
     }
-    // summaries are stored field-wise and copied as whole 16-byte vectors: define the padding
-    CK(cudaMemsetAsync(c->start_sum.p, 0, 32 * csb, c->stream));
-    if (multi) CK(cudaMemsetAsync(c->st_sum.p, 0, cc * 32 * csb, c->stream));
+    // (LaneState has no padding and parked anchors are written before they are read: no memset)
     CK(cudaMemcpyAsync(c->start_ent.p, ent.data(), ent_words * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->start_bits.p, bits.data(), bit_words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
     if (prm->n_scale_mult > 0)

@@ -505,24 +505,32 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
     const int n = static_cast<int>(sorted_ids.size());
     exec.assign((std::size_t)n * max_batch, 0.0);
     deadline.assign((std::size_t)n * max_batch, 0.0);
-    for (int i = 0; i < n; ++i) {
-        const Request& r = require_predicted(w, sorted_ids[i], "anneal");
-        const SloSpec& slo = w.class_of(r).slo;
-        const int lo = *r.predicted_output_len;
-        for (int b = 1; b <= max_batch; ++b) {
-            const double e = predict_exec(c, b, r.input_len, lo);
-            double d;
-            if (slo.kind == SloKind::E2E) {
-                d = latest_start(*slo.e2e_ms, e);
-            } else {
-                const double tp = predict_tpot(c, b, r.input_len, lo);
-                d = tp <= *slo.tpot_ms ? latest_start(*slo.ttft_ms, predict_prefill(c, b, r.input_len))
-                                       : -std::numeric_limits<double>::infinity();
+    auto fill = [&](int i0, int i1) {
+        for (int i = i0; i < i1; ++i) {
+            const Request& r = require_predicted(w, sorted_ids[i], "anneal");
+            const SloSpec& slo = w.class_of(r).slo;
+            const int lo = *r.predicted_output_len;
+            for (int b = 1; b <= max_batch; ++b) {
+                const double e = predict_exec(c, b, r.input_len, lo);
+                double d;
+                if (slo.kind == SloKind::E2E) {
+                    d = latest_start(*slo.e2e_ms, e);
+                } else {
+                    const double tp = predict_tpot(c, b, r.input_len, lo);
+                    d = tp <= *slo.tpot_ms ? latest_start(*slo.ttft_ms, predict_prefill(c, b, r.input_len))
+                                           : -std::numeric_limits<double>::infinity();
+                }
+                exec[(std::size_t)(b - 1) * n + i] = e;
+                deadline[(std::size_t)(b - 1) * n + i] = d;
             }
-            exec[(std::size_t)(b - 1) * n + i] = e;
-            deadline[(std::size_t)(b - 1) * n + i] = d;
         }
-    }
+    };
+    // large queues: the rows are independent, fill them on up to 4 threads
+    const int parts = static_cast<int>(std::min<std::size_t>(4, (std::size_t)n * max_batch / 2048 + 1));
+    std::vector<std::future<void>> rest;
+    for (int k = 1; k < parts; ++k) rest.push_back(std::async(std::launch::async, fill, n * k / parts, n * (k + 1) / parts));
+    fill(0, n / parts);
+    for (auto& f : rest) f.get();
     // No batch can start later than the sum of every request's largest exec (a makespan is at
     // most the sum of its members'). A deadline at or beyond that bound is met in every schedule:
     // store +inf, which leaves every exact compare unchanged and lets the chain kernel count such
@@ -711,16 +719,20 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     } pool_return{ctx, device, ctx_ok};
     auto tables = std::async(std::launch::async, [&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
-        if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB) {
-            ctx = CtxPool::get().acquire(device);
-            engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
-            ctx_ok = true;
-        }
+        // the upload (context, tables, device-side tick tables) overlaps the deadline-first start
+        auto upload = std::async(std::launch::async, [&] {
+            if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB) {
+                ctx = CtxPool::get().acquire(device);
+                engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
+                ctx_ok = true;
+            }
+        });
         if (want_dl) {
             EvaluatedSchedule ev;
             best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, dl_perm, dl_sizes, ev);
             ev_dl = std::move(ev);
         }
+        upload.get();
     });
     auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
     EvaluatedSchedule ev_sorted = evaluate(sorted_s, c, w);
