@@ -106,21 +106,37 @@ __device__ __forceinline__ int prev_end(const uint32_t* bits, int q) {
 
 // ================================================================ K1: exact evaluate
 // Sequential CostModel::score (P:src/priority_mapper.cpp:259-279) per candidate.
-__global__ void k_eval_exact(int count, int n, int words, const uint16_t* __restrict__ perms,
+// Candidates are validated here, not on the host: bit n-1 must end a batch, batches hold at most
+// mb positions, indices are below n (error bits 1 / 2 / 4 in *err; the candidate is not scored).
+__global__ void k_eval_exact(int count, int n, int mb, int words, const uint16_t* __restrict__ perms,
                              const uint32_t* __restrict__ bits, const double2* __restrict__ tab,
-                             int* __restrict__ n_met, double* __restrict__ t_out, double* __restrict__ g_out) {
+                             int* __restrict__ n_met, double* __restrict__ t_out, double* __restrict__ g_out,
+                             int* __restrict__ err) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= count) return;
     const uint16_t* pr = perms + (size_t)c * n;
     const uint32_t* br = bits + (size_t)c * words;
+    if (!((br[(n - 1) >> 5] >> ((n - 1) & 31)) & 1u)) {
+        atomicOr(err, 1);
+        return;
+    }
     double elapsed = 0.0, total = 0.0;
     int met = 0, s = 0;
     while (s < n) {
         const int e = next_end(br, s);
         const int bidx = e - s;
+        if (bidx >= mb) {
+            atomicOr(err, 2);
+            return;
+        }
         double makespan = 0.0;
         for (int q = s; q <= e; ++q) {
-            const double2 v = __ldg(&tab[bidx * n + pr[q]]);
+            const int i = pr[q];
+            if (i >= n) {
+                atomicOr(err, 4);
+                return;
+            }
+            const double2 v = __ldg(&tab[bidx * n + i]);
             const double e2e = elapsed + v.x;
             total += e2e;
             met += elapsed <= v.y;
@@ -286,7 +302,7 @@ struct slo_ctx {
     DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
         result, win_ent, win_bits;
     // K1
-    DevBuf e_perms, e_bits, e_n, e_t, e_g;
+    DevBuf e_perms, e_bits, e_n, e_t, e_g, e_err;
     bool prepared = false;
     slo_chain_params prm{};
     int UPL = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
@@ -403,37 +419,30 @@ int slo_evaluate_batch(slo_ctx* c, int32_t count, const uint16_t* perms, const u
     if (c->n == 0) return fail(SLO_ERR_STATE, "slo_evaluate_batch: no problem set");
     if (count <= 0) return SLO_OK;
     const int n = c->n, words = (n + 31) / 32;
-    // validate on the host: every batch non-empty and <= mb, last bit set, indices in range
-    for (int k = 0; k < count; ++k) {
-        const uint16_t* pr = perms + (size_t)k * n;
-        const uint32_t* br = bits + (size_t)k * words;
-        if (!((br[(n - 1) >> 5] >> ((n - 1) & 31)) & 1u)) return fail(SLO_ERR_DATA, "slo_evaluate_batch: last position must end a batch");
-        int run = 0;
-        for (int q = 0; q < n; ++q) {
-            if (pr[q] >= n) return fail(SLO_ERR_DATA, "slo_evaluate_batch: dense index out of range");
-            ++run;
-            if ((br[q >> 5] >> (q & 31)) & 1u) {
-                if (run > c->mb) return fail(SLO_ERR_DATA, "slo_evaluate_batch: batch larger than max_batch");
-                run = 0;
-            }
-        }
-    }
     CK(cudaSetDevice(c->device));
     CK(c->e_perms.reserve((size_t)count * n * sizeof(uint16_t)));
     CK(c->e_bits.reserve((size_t)count * words * sizeof(uint32_t)));
     CK(c->e_n.reserve((size_t)count * sizeof(int)));
     CK(c->e_t.reserve((size_t)count * sizeof(double)));
     CK(c->e_g.reserve((size_t)count * sizeof(double)));
+    CK(c->e_err.reserve(sizeof(int)));
+    CK(cudaMemsetAsync(c->e_err.p, 0, sizeof(int), c->stream));
     CK(cudaMemcpyAsync(c->e_perms.p, perms, (size_t)count * n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->e_bits.p, bits, (size_t)count * words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
-    k_eval_exact<<<(count + 127) / 128, 128, 0, c->stream>>>(count, n, words, c->e_perms.as<uint16_t>(),
+    k_eval_exact<<<(count + 127) / 128, 128, 0, c->stream>>>(count, n, c->mb, words, c->e_perms.as<uint16_t>(),
                                                                c->e_bits.as<uint32_t>(), c->tab.as<double2>(),
-                                                               c->e_n.as<int>(), c->e_t.as<double>(), c->e_g.as<double>());
+                                                               c->e_n.as<int>(), c->e_t.as<double>(), c->e_g.as<double>(),
+                                                               c->e_err.as<int>());
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(n_met, c->e_n.p, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(t, c->e_t.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(g, c->e_g.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    int err = 0;
+    CK(cudaMemcpyAsync(&err, c->e_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
+    if (err & 1) return fail(SLO_ERR_DATA, "slo_evaluate_batch: last position must end a batch");
+    if (err & 2) return fail(SLO_ERR_DATA, "slo_evaluate_batch: batch larger than max_batch");
+    if (err & 4) return fail(SLO_ERR_DATA, "slo_evaluate_batch: dense index out of range");
     return SLO_OK;
 }
 

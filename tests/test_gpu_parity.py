@@ -102,6 +102,17 @@ def test_evaluate_batch_rejects_bad_input(eng):
         eng.evaluate_batch(perm, E.end_bits([[3, 3, 2, 2]], 10))
     with pytest.raises(S.DataError):  # last position not a batch end
         eng.evaluate_batch(perm, np.zeros((1, 1), dtype=np.uint32))
+    bad = perm.copy()
+    bad[0, 4] = 10
+    with pytest.raises(S.DataError):  # dense index out of range
+        eng.evaluate_batch(bad, E.end_bits([[2] * 5], 10))
+    # validation runs on the device, per candidate: one bad row among good ones still fails the call
+    rows = np.repeat(perm, 64, axis=0)
+    rows[37, 2] = 11
+    with pytest.raises(S.DataError):
+        eng.evaluate_batch(rows, E.end_bits([[2] * 5] * 64, 10))
+    nm, t, g = eng.evaluate_batch(np.repeat(perm, 64, axis=0), E.end_bits([[2] * 5] * 64, 10))
+    assert (nm == nm[0]).all() and (t == t[0]).all()
 
 
 # ---------------------------------------------------------------- K2 replay
