@@ -210,3 +210,22 @@ def test_k3_model_philox_and_tick_objective():
         nm, t, g = prob.score(batches)
         o_n, o_t, o_g = port.score_batch(fw, TABLE_COEFFS, ids, 4, perm[None, :].astype(np.int32), [sizes])
         assert abs(t - o_t[0]) <= 48 * 48 * tick and abs(nm - o_n[0]) <= 1
+
+
+def test_bench_reference_arm_line():
+    """`bench.py --impl reference` (the driver's reference arm) runs the unmodified reference on the
+    host cores and prints one JSON line with the contract's keys."""
+    import json
+    import subprocess
+    import sys
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--impl", "reference", "--steps", "1",
+                          "--warmup", "1", "--n", "256"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["impl"] == "reference" and line["unit"] == "evals/s" and line["value"] > 0
+    assert line["higher_is_better"] is True and line["n_gpus"] == 1
+    assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] == line["value"]
+    assert line["e2e"] == {"value": line["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
