@@ -384,7 +384,7 @@ def run_ours(args):
     # profiles/r1/k_chains_summary.json from tools/prof_chains.py --bench) x proposals this run
     # evaluated / the kernel's CUDA-event time; peak = 4 issue slots x SMs x the SM clock sampled
     # during the timed region. The shared-memory view (bytes the evaluator gathers) is kept beside.
-    prof = load_profile_summary()
+    prof, prof_file = load_profile_summary(n, mb)
     clk = clocks.summary()
     sm_mhz = clk.get("sm_mhz") or measured_peaks().get("sm_max_mhz") or 1965.0
     n_sms = eng.sm_count
@@ -398,7 +398,8 @@ def run_ours(args):
             "frac": (achieved_ginst / peak_ginst) if achieved_ginst else None,
             "traffic": (prof["dram_bytes_per_proposal"] * props / args.steps) if prof else None,
             "kernel": "k_chains", "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
-            "instr_per_proposal": ipp, "instr_source": "profiles/r1/k_chains_summary.json (ncu --set full, tools/prof_chains.py --bench)",
+            "instr_per_proposal": ipp, "instr_source": (f"profiles/r1/{prof_file} (ncu --set full, tools/prof_chains.py --bench --n {n})"
+                             if prof else f"none: no ncu capture of N={n} mb={mb} under profiles/r1"),
             "peak_source": f"4 warp-inst/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz (sampled under load)",
             "smem_view": {"achieved_gbs": smem_bytes / (kern_ms / 1e3) / 1e9, "peak_gbs": smem_peak_gbs,
                           "peak_source": "slo_probe_smem_bandwidth (conflict-free LDS.128, all SMs, measured here)",
@@ -442,13 +443,16 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def load_profile_summary():
-    path = os.path.join(ROOT, "profiles", "r1", "k_chains_summary.json")
+def load_profile_summary(n, mb):
+    """The ncu summary of k_chains captured at this (n, mb) (instructions per proposal depend on
+    the units per lane and the live units), or None: a capture of another shape is not used."""
+    name = "k_chains_summary.json" if (n, mb) == (1024, 4) else f"k_chains_summary_n{n}_mb{mb}.json"
     try:
-        with open(path) as f:
-            return json.load(f)
+        with open(os.path.join(ROOT, "profiles", "r1", name)) as f:
+            prof = json.load(f)
     except OSError:
-        return None
+        return None, name
+    return (prof, name) if (prof.get("n", 1024), prof.get("mb", 4)) == (n, mb) else (None, name)
 
 
 def measured_peaks():

@@ -251,15 +251,21 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
     return tot > 0.0 ? (double)nm * r : 0.0;
 }
 
+#ifndef SLO_RND_ROWS_WIDE
+#define SLO_RND_ROWS_WIDE 16
+#endif
+#ifndef SLO_RND_STRIDE_WIDE
+#define SLO_RND_STRIDE_WIDE 32
+#endif
 // Philox rows drawn per refill (one per lane): 32 proposals, 16 where shared memory is tight
 template <int UPL>
-__host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : 16; }
+__host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : SLO_RND_ROWS_WIDE; }
 
 // row stride (words): 36 = 9 x 16 B puts the 32 lanes' row stores on distinct bank groups
 // (conflict-free uint4 stores); where shared memory bounds the resident warps (2-4 units per
 // lane) the dense stride keeps one more warp per SM
 template <int UPL>
-__host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : kRndWords; }
+__host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : SLO_RND_STRIDE_WIDE; }
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {

@@ -16,12 +16,19 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ch
 # (prof_chains.py --bench evaluates 16384 chains x 7 levels x 100 proposals = 11468800)
 python tools/ncu_summary.py gpurun_out/k_chains.ncu-rep --proposals 11468800 --tag r1 > /dev/null 2>&1 && \
     cp profiles/r1/k_chains_summary.json gpurun_out/k_chains_summary.json
+# the same for configs[3]'s shard (N=4096: k_chains<4>; 3 levels ~ what its 7 ms device budget allows)
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 \
+    -o gpurun_out/k_chains_n4096 python tools/prof_chains.py --bench --n 4096 --levels 3 > gpurun_out/ncu_full_n4096.log 2>&1
+python tools/ncu_summary.py gpurun_out/k_chains_n4096.ncu-rep --proposals 4915200 --tag r1 --n 4096 --mb 4 \
+    --out k_chains_summary_n4096_mb4.json --desc "k_chains<4> (N=4096, mb=4, 16384 chains, prof_chains.py --bench --n 4096 --levels 3)" \
+    > /dev/null 2>&1 && cp profiles/r1/k_chains_summary_n4096_mb4.json gpurun_out/
 # launch list of the bench command (times are cold-cache and serialised: use the shares)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 2 \
     > gpurun_out/b_ncu.log 2>&1
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
+timeout 600 python bench.py --n 4096 > gpurun_out/bench_n4096.json 2> gpurun_out/bench_n4096.err
 for t in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > gpurun_out/san_$t.log 2>&1
 done

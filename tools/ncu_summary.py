@@ -91,6 +91,9 @@ def main():
     ap.add_argument("--proposals", type=float, required=True)
     ap.add_argument("--tag", required=True)
     ap.add_argument("--launches", default=None)
+    ap.add_argument("--n", type=int, default=1024, help="requests of the captured configuration")
+    ap.add_argument("--mb", type=int, default=4, help="max batch of the captured configuration")
+    ap.add_argument("--out", default="k_chains_summary.json", help="file name under profiles/<tag>/")
     args = ap.parse_args()
     d = details(args.rep)
     rw = raw(args.rep)
@@ -107,6 +110,7 @@ def main():
         "report": os.path.basename(args.rep),
         "kernel": args.desc,
         "metrics": {k: {"value": d[k][0], "unit": d[k][1]} for k in keys if k in d},
+        "n": args.n, "mb": args.mb,
         "proposals": args.proposals,
         "instr_per_proposal": instr / args.proposals if instr else None,
         "dram_bytes": dram,
@@ -144,7 +148,7 @@ def main():
                                   for k, (c, v) in sorted(agg.items(), key=lambda kv: -kv[1][1])}
     out_dir = os.path.join(ROOT, "profiles", args.tag)
     os.makedirs(out_dir, exist_ok=True)
-    with open(os.path.join(out_dir, "k_chains_summary.json"), "w") as f:
+    with open(os.path.join(out_dir, args.out), "w") as f:
         json.dump(summary, f, indent=1)
     print(json.dumps(summary, indent=1))
 
