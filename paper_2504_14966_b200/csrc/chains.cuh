@@ -30,10 +30,18 @@
 #ifndef SLO_CHAIN_THREADS
 #define SLO_CHAIN_THREADS 896  // k_chains<1> block size (28 warps, 72 registers; 768 and 1024 measured slower)
 #endif
+#ifndef SLO_CHAIN_THREADS2
+#define SLO_CHAIN_THREADS2 768
+#endif
+#ifndef SLO_CHAIN_THREADS4
+#define SLO_CHAIN_THREADS4 512
+#endif
 // block-size bound per units-per-lane (N <= 1024 / 2048 / 4096): more resident warps hide the
 // dependent-latency stalls until registers spill (measured: UPL 2 768 > 640 > 512, UPL 4 512 > 640)
 template <int UPL>
-__host__ __device__ constexpr int chain_threads() { return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? 768 : 512); }
+__host__ __device__ constexpr int chain_threads() {
+    return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? SLO_CHAIN_THREADS2 : SLO_CHAIN_THREADS4);
+}
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
 constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
 constexpr int kRndWords = 32;                        // words of a proposal's row (stride: rnd_stride)
