@@ -31,13 +31,15 @@
 #define SLO_CHAIN_THREADS 896  // k_chains<1> block size (28 warps, 72 registers; 768 and 1024 measured slower)
 #endif
 #ifndef SLO_CHAIN_THREADS2
-#define SLO_CHAIN_THREADS2 768
+#define SLO_CHAIN_THREADS2 896
 #endif
 #ifndef SLO_CHAIN_THREADS4
 #define SLO_CHAIN_THREADS4 512
 #endif
 // block-size bound per units-per-lane (N <= 1024 / 2048 / 4096): more resident warps hide the
-// dependent-latency stalls until registers spill (measured: UPL 2 768 > 640 > 512, UPL 4 512 > 640)
+// dependent-latency stalls until registers spill (measured with tools/prof_chains.py --bench:
+// UPL 2 896 > 768 > 640 > 512, UPL 4 512 > 608 > 576). 16384 chains over 148 x 28 warps is 3.95
+// chains per warp, so 896 also balances; 832 and 960 leave a fifth/fourth round partly empty.
 template <int UPL>
 __host__ __device__ constexpr int chain_threads() {
     return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? SLO_CHAIN_THREADS2 : SLO_CHAIN_THREADS4);
