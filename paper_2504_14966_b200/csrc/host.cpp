@@ -7,7 +7,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdint>
 #include <cstdlib>
+#include <cstring>
 #include <future>
 #include <limits>
 #include <memory>
@@ -238,6 +240,43 @@ const Request& require_predicted(const Workload& w, int id, const char* what) {
     return *r;
 }
 double max_of(double a, double b) { return a < b ? b : a; }  // std::max semantics
+
+// Positions 0..n-1 in ascending (key[i], tie[i], i) order (tie: optional secondary key) -- the
+// order of a stable sort -- by an LSD radix sort of order-preserving bit patterns (8-bit digits,
+// constant digits skipped): a comparison sort of a few thousand doubles is dominated by branch
+// mispredictions. Keys are never NaN (execs, latest starts and arrival times).
+std::vector<int> order_by_key(const std::vector<double>& key, const std::vector<int>* tie = nullptr) {
+    const int n = static_cast<int>(key.size());
+    std::vector<uint64_t> k(n), k2(n);
+    std::vector<int> idx(n), idx2(n);
+    for (int i = 0; i < n; ++i) idx[i] = i;
+    auto passes = [&](int bits, auto&& digit_key) {
+        uint64_t all_or = 0, all_and = ~0ull;
+        for (int i = 0; i < n; ++i) {
+            k[i] = digit_key(idx[i]);
+            all_or |= k[i], all_and &= k[i];
+        }
+        for (int shift = 0; shift < bits; shift += 8) {
+            if ((((all_or ^ all_and) >> shift) & 0xffu) == 0) continue;  // every key has this digit
+            int cnt[257] = {};
+            for (int i = 0; i < n; ++i) ++cnt[((k[i] >> shift) & 0xffu) + 1];
+            for (int d = 0; d < 256; ++d) cnt[d + 1] += cnt[d];
+            for (int i = 0; i < n; ++i) {
+                const int at = cnt[(k[i] >> shift) & 0xffu]++;
+                k2[at] = k[i], idx2[at] = idx[i];
+            }
+            k.swap(k2), idx.swap(idx2);
+        }
+    };
+    if (tie) passes(32, [&](int i) { return (uint64_t)((uint32_t)(*tie)[i] ^ 0x80000000u); });
+    passes(64, [&](int i) {
+        const double d = key[i] == 0.0 ? 0.0 : key[i];  // -0 ties +0, as under <
+        uint64_t b;
+        std::memcpy(&b, &d, sizeof b);
+        return (b >> 63) ? ~b : (b | (1ull << 63));
+    });
+    return idx;
+}
 }  // namespace
 
 std::vector<ExecProfile> batch_exec_profile(const Schedule& s, const LatencyCoefficients& c, const Workload& w) {
@@ -276,28 +315,44 @@ bool meets_slo(const SloSpec& slo, double e2e_ms, double ttft_ms, double tpot_ms
     return ttft_ms <= *slo.ttft_ms && tpot_ms <= *slo.tpot_ms;
 }
 
-EvaluatedSchedule evaluate(const Schedule& s, const LatencyCoefficients& c, const Workload& w) {
+namespace {
+// batch_exec_profile + waiting_times + the metrics pass of P:src/objective.cpp fused into one pass
+// over the schedule (one request lookup each); the same operations in the same order, so every
+// metric, n, t and g are bit-identical to the three-pass form
+EvaluatedSchedule evaluate_owned(Schedule&& s, const LatencyCoefficients& c, const Workload& w) {
     EvaluatedSchedule ev;
-    ev.schedule = s;
-    const auto prof = batch_exec_profile(s, c, w);
-    const auto waits = waiting_times(s, prof);
-    ev.per_request.reserve(prof.size());
-    for (std::size_t i = 0; i < prof.size(); ++i) {
-        RequestMetrics m;
-        m.request_id = prof[i].request_id;
-        m.wait_ms = waits[i];
-        m.exec_ms = prof[i].exec_ms;
-        m.e2e_ms = prof[i].exec_ms + waits[i];
-        m.ttft_ms = prof[i].prefill_ms + waits[i];
-        m.tpot_ms = prof[i].tpot_ms;
-        m.extrapolated = prof[i].extrapolated;
-        m.slo_met = meets_slo(w.class_of(*w.find_request(m.request_id)).slo, m.e2e_ms, m.ttft_ms, m.tpot_ms);
-        ev.n += m.slo_met ? 1 : 0;
-        ev.t_ms += m.e2e_ms;
-        ev.per_request.push_back(m);
+    ev.per_request.reserve(s.request_count());
+    double elapsed = 0.0;
+    for (const auto& batch : s.batches) {
+        const int b = static_cast<int>(batch.size());
+        double makespan = 0.0;
+        for (int id : batch) {
+            const Request& r = require_predicted(w, id, "schedule");
+            const int lo = *r.predicted_output_len;
+            RequestMetrics m;
+            m.request_id = id;
+            m.wait_ms = elapsed;
+            m.exec_ms = predict_exec(c, b, r.input_len, lo);
+            m.e2e_ms = m.exec_ms + elapsed;
+            m.ttft_ms = predict_prefill(c, b, r.input_len) + elapsed;
+            m.tpot_ms = predict_tpot(c, b, r.input_len, lo);
+            m.extrapolated = is_extrapolated(r.input_len, lo);
+            m.slo_met = meets_slo(w.class_of(r).slo, m.e2e_ms, m.ttft_ms, m.tpot_ms);
+            makespan = max_of(makespan, m.exec_ms);
+            ev.n += m.slo_met ? 1 : 0;
+            ev.t_ms += m.e2e_ms;
+            ev.per_request.push_back(m);
+        }
+        elapsed += makespan;
     }
     ev.g = ev.t_ms > 0.0 ? static_cast<double>(ev.n) / ev.t_ms : 0.0;
+    ev.schedule = std::move(s);
     return ev;
+}
+}  // namespace
+
+EvaluatedSchedule evaluate(const Schedule& s, const LatencyCoefficients& c, const Workload& w) {
+    return evaluate_owned(Schedule(s), c, w);
 }
 
 // ================================================================ priority mapper
@@ -334,31 +389,26 @@ Schedule pack_greedy(const std::vector<int>& ordered, int max_batch) {
     return s;
 }
 
-// (key, id) pairs sorted ascending -- the comparator of P:src/priority_mapper.cpp:297-308
-// evaluated once per id instead of inside every comparison
-std::vector<int> order_by(std::vector<std::pair<double, int>> keyed) {
-    std::sort(keyed.begin(), keyed.end(), [](const auto& a, const auto& b) {
-        return a.first != b.first ? a.first < b.first : a.second < b.second;
-    });
-    std::vector<int> out;
-    out.reserve(keyed.size());
-    for (const auto& kv : keyed) out.push_back(kv.second);
-    return out;
-}
-
 }  // namespace
 
 std::pair<Schedule, Schedule> initial_candidates(const Workload& w, const std::vector<int>& ids,
                                                  const LatencyCoefficients& c, int max_batch) {
-    std::vector<std::pair<double, int>> by_exec, by_arrival;
-    by_exec.reserve(ids.size());
-    by_arrival.reserve(ids.size());
-    for (int id : ids) {
-        const Request& r = require_predicted(w, id, "initial_candidates");
-        by_exec.emplace_back(predict_exec(c, max_batch, r.input_len, *r.predicted_output_len), id);
-        by_arrival.emplace_back(r.arrival_time_ms, id);
+    // ascending (key, id): the comparator of P:src/priority_mapper.cpp:297-308, its keys computed
+    // once per id
+    const std::size_t n = ids.size();
+    std::vector<double> exec_key(n), arrival_key(n);
+    for (std::size_t i = 0; i < n; ++i) {
+        const Request& r = require_predicted(w, ids[i], "initial_candidates");
+        exec_key[i] = predict_exec(c, max_batch, r.input_len, *r.predicted_output_len);
+        arrival_key[i] = r.arrival_time_ms;
     }
-    return {pack_greedy(order_by(std::move(by_exec)), max_batch), pack_greedy(order_by(std::move(by_arrival)), max_batch)};
+    auto ordered = [&](const std::vector<double>& key) {
+        std::vector<int> out(n);
+        const std::vector<int> pos = order_by_key(key, &ids);
+        for (std::size_t i = 0; i < n; ++i) out[i] = ids[pos[i]];
+        return out;
+    };
+    return {pack_greedy(ordered(exec_key), max_batch), pack_greedy(ordered(arrival_key), max_batch)};
 }
 
 std::optional<EvaluatedSchedule> shortcut_check(const Schedule& sorted_schedule, const LatencyCoefficients& c,
@@ -558,16 +608,17 @@ namespace {
 // feasible, and the exact evaluation decides). O(n * kept).
 constexpr int kDeadlineVariants = 3;
 
+
+// exec_order: every dense index in ascending (full-batch exec, index) order (shared by the variants)
 void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const std::vector<double>& deadline,
-                          int variant, std::vector<int>& perm, std::vector<int>& sizes) {
+                          int variant, const std::vector<int>& exec_order, std::vector<int>& perm,
+                          std::vector<int>& sizes) {
     const double* ef = exec.data() + (std::size_t)(mb - 1) * n;
     const double* df = deadline.data() + (std::size_t)(mb - 1) * n;
     std::vector<double> due(n);
     for (int i = 0; i < n; ++i)
         due[i] = variant == 1 ? deadline[i] : (variant == 2 ? df[i] + ef[i] : df[i]);
-    std::vector<int> order(n);
-    for (int i = 0; i < n; ++i) order[i] = i;
-    std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return due[a] < due[b]; });
+    const std::vector<int> order = order_by_key(due);  // ascending due, ties by index
     auto by_exec = [&](int a, int b) { return ef[a] != ef[b] ? ef[a] < ef[b] : a < b; };
     std::vector<int> kept;
     std::vector<double> start;  // start time of kept batch k (valid for batches before `dirty`)
@@ -608,10 +659,10 @@ void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const 
     for (int i : kept) perm.push_back(i), in[i] = 1;
     for (int b0 = 0; b0 < static_cast<int>(kept.size()); b0 += mb)
         sizes.push_back(std::min(mb, static_cast<int>(kept.size()) - b0));
-    std::vector<int> rest;
-    for (int i = 0; i < n; ++i)
+    std::vector<int> rest;  // the dropped requests in (exec, index) order: a filter of exec_order
+    rest.reserve(n - kept.size());
+    for (int i : exec_order)
         if (!in[i]) rest.push_back(i);
-    std::stable_sort(rest.begin(), rest.end(), by_exec);
     for (std::size_t b0 = 0; b0 < rest.size(); b0 += mb) {
         const int sz = static_cast<int>(std::min<std::size_t>(mb, rest.size() - b0));
         for (int j = 0; j < sz; ++j) perm.push_back(rest[b0 + j]);
@@ -653,17 +704,19 @@ double dense_score(int n, const std::vector<double>& exec, const std::vector<dou
 }
 
 // All variants (one host thread each), scored exactly; the best by G (lowest variant on ties).
-void best_deadline_first(const Workload& w, const LatencyCoefficients& c, const std::vector<int>& sorted_ids, int mb,
-                         const std::vector<double>& exec, const std::vector<double>& deadline, std::vector<int>& perm,
-                         std::vector<int>& sizes, EvaluatedSchedule& ev) {
-    const int n = static_cast<int>(sorted_ids.size());
+// Returns its G (dense_score == evaluate().g bit-for-bit); the full evaluation is left to the
+// caller, which needs it only when this candidate is the answer.
+double best_deadline_first(int n, int mb, const std::vector<double>& exec, const std::vector<double>& deadline,
+                           std::vector<int>& perm, std::vector<int>& sizes) {
     struct Cand {
         std::vector<int> perm, sizes;
         double g = 0.0;
     };
     std::vector<Cand> cand(kDeadlineVariants);
+    const std::vector<int> exec_order =  // (full-batch exec, index): a strict total order
+        order_by_key(std::vector<double>(exec.begin() + (std::size_t)(mb - 1) * n, exec.begin() + (std::size_t)mb * n));
     auto build = [&](int v) {
-        deadline_first_dense(n, mb, exec, deadline, v, cand[v].perm, cand[v].sizes);
+        deadline_first_dense(n, mb, exec, deadline, v, exec_order, cand[v].perm, cand[v].sizes);
         cand[v].g = dense_score(n, exec, deadline, cand[v].perm, cand[v].sizes);
     };
     std::vector<std::future<void>> others;
@@ -674,7 +727,7 @@ void best_deadline_first(const Workload& w, const LatencyCoefficients& c, const 
     for (int v = 1; v < kDeadlineVariants; ++v)
         if (cand[v].g > cand[best].g) best = v;
     perm = std::move(cand[best].perm), sizes = std::move(cand[best].sizes);
-    ev = evaluate(schedule_of(perm, sizes, sorted_ids), c, w);
+    return cand[best].g;
 }
 
 }  // namespace
@@ -686,9 +739,8 @@ Schedule deadline_first_candidate(const Workload& w, const std::vector<int>& ids
     cost_tables(w, ids, c, max_batch, exec, deadline);
     std::vector<int> sorted_ids = ids, perm, sizes;
     std::sort(sorted_ids.begin(), sorted_ids.end());
-    EvaluatedSchedule ev;
-    best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, perm, sizes, ev);
-    return ev.schedule;
+    best_deadline_first(static_cast<int>(sorted_ids.size()), max_batch, exec, deadline, perm, sizes);
+    return schedule_of(perm, sizes, sorted_ids);
 }
 
 AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
@@ -703,7 +755,7 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     std::sort(sorted_ids.begin(), sorted_ids.end());
     std::vector<double> exec, deadline;
     std::vector<int> dl_perm, dl_sizes;
-    std::optional<EvaluatedSchedule> ev_dl;
+    std::optional<double> g_dl;  // G of the deadline-first candidate (evaluated in full only if returned)
     const bool want_dl = cfg.engine.mode == SearchMode::Chains && cfg.engine.deadline_start;
     // the engine context is acquired and the tables uploaded on the same thread, as soon as they exist
     const int device = resolve_device(cfg.engine.device);
@@ -727,11 +779,7 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
                 ctx_ok = true;
             }
         });
-        if (want_dl) {
-            EvaluatedSchedule ev;
-            best_deadline_first(w, c, sorted_ids, max_batch, exec, deadline, dl_perm, dl_sizes, ev);
-            ev_dl = std::move(ev);
-        }
+        if (want_dl) g_dl = best_deadline_first(n, max_batch, exec, deadline, dl_perm, dl_sizes);
         upload.get();
     });
     auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
@@ -762,9 +810,9 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     // score(start) == evaluate(start).g bit-for-bit (same operand order), :362-370
     double f = use_sorted ? ev_sorted.g : ev_input.g;
     // engine extension: the chains start from the deadline-first candidate when it scores higher
-    if (ev_dl) {
-        res.stats.g_deadline_start = ev_dl->g;
-        if (ev_dl->g > f) f = ev_dl->g, start_perm = std::move(dl_perm), start_sizes = std::move(dl_sizes);
+    if (g_dl) {
+        res.stats.g_deadline_start = *g_dl;
+        if (*g_dl > f) f = *g_dl, start_perm = dl_perm, start_sizes = dl_sizes;
     }
     const double scale = cfg.objective_scale ? *cfg.objective_scale : (f > 0.0 ? cfg.t0 / f : cfg.t0);
     res.stats.objective_scale_used = scale;
@@ -813,10 +861,10 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
         best.batches.push_back(std::move(b));
     }
     // final evaluation through the objective; both starts stay a floor, :404-410
-    EvaluatedSchedule ev_best = evaluate(best, c, w);
+    EvaluatedSchedule ev_best = evaluate_owned(std::move(best), c, w);
     const double floor_g = std::max(ev_sorted.g, ev_input.g);
-    if (ev_best.g >= floor_g && (!ev_dl || ev_best.g >= ev_dl->g)) res.best = std::move(ev_best);
-    else if (ev_dl && ev_dl->g > floor_g) res.best = std::move(*ev_dl);
+    if (ev_best.g >= floor_g && (!g_dl || ev_best.g >= *g_dl)) res.best = std::move(ev_best);
+    else if (g_dl && *g_dl > floor_g) res.best = evaluate(schedule_of(dl_perm, dl_sizes, sorted_ids), c, w);
     else res.best = use_sorted ? std::move(ev_sorted) : std::move(ev_input);
     return res;
 }
@@ -870,13 +918,16 @@ AssignmentResult assign_instances(const Workload& w, const std::vector<InstanceS
                                   const LatencyCoefficients& c) {
     if (instances.empty()) throw DataError("assign_instances: need at least one instance");
     for (const auto& inst : instances) inst.validate();
-    std::vector<std::pair<double, int>> keyed;
-    keyed.reserve(w.requests.size());
+    std::vector<double> key;
+    std::vector<int> rid;
+    key.reserve(w.requests.size()), rid.reserve(w.requests.size());
     for (const auto& r : w.requests) {
         if (!r.predicted_output_len) throw DataError("assign_instances: request missing predicted length");
-        keyed.emplace_back(predict_exec(c, 1, r.input_len, *r.predicted_output_len), r.id);
+        key.push_back(predict_exec(c, 1, r.input_len, *r.predicted_output_len)), rid.push_back(r.id);
     }
-    const std::vector<int> order = order_by(std::move(keyed));
+    std::vector<int> order;  // ids in ascending (exec alone, id)
+    order.reserve(rid.size());
+    for (int i : order_by_key(key, &rid)) order.push_back(rid[i]);
     const std::size_t k = instances.size();
     std::vector<double> remaining(k);
     for (std::size_t i = 0; i < k; ++i) remaining[i] = static_cast<double>(instances[i].remaining_mem);

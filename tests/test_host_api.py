@@ -93,6 +93,29 @@ def test_initial_candidates_and_neighbor_match_golden():
         assert out.batches == case["out"]
 
 
+def test_initial_candidates_break_ties_by_id():
+    """The candidates order by (key, id) (P:src/priority_mapper.cpp:297-308): with every key tied,
+    both are the ids in ascending order whatever order the caller passes them in (negative ids
+    included), and evaluate() agrees with a direct restatement of the objective on them."""
+    c = S.table_coefficients()
+    code, chat = S.default_slo_classes()
+    rs = np.random.RandomState(5)
+    ids = [int(x) for x in rs.choice(np.arange(-5000, 5000), 300, replace=False)]
+    reqs = [S.Request(i, code.id if k % 2 else chat.id, 120, 60, 60, 7.0) for k, i in enumerate(ids)]
+    w = S.Workload(reqs, [code, chat])
+    for mb in (1, 3, 4):
+        s, inp = S.initial_candidates(w, ids, c, mb)
+        assert s.flatten() == sorted(ids) and inp.flatten() == sorted(ids)
+        ev = S.evaluate(s, c, w)
+        elapsed, tot, met = 0.0, 0.0, 0
+        for b in s.batches:
+            e = S.predict_exec(c, len(b), 120, 60)
+            for _ in b:
+                tot += elapsed + e
+            elapsed += e
+        assert ev.t_ms == tot and len(ev.per_request) == 300
+
+
 def test_errors_follow_reference_contract():
     code, chat = S.default_slo_classes()
     with pytest.raises(S.DataError):  # duplicate id
