@@ -131,6 +131,10 @@ struct Workload {
 private:
     friend Workload validate_workload(std::vector<Request>, std::vector<TaskClass>);
     std::unordered_map<int, std::size_t> class_index_, request_index_;
+    // request ids spanning a small range (the common case) index a flat table instead of the
+    // hash map: position + 1 at id - dense_lo_, 0 where no request has that id
+    long long dense_lo_ = 0;
+    std::vector<std::uint32_t> dense_;
 };
 
 Workload validate_workload(std::vector<Request> requests, std::vector<TaskClass> classes);

@@ -115,18 +115,27 @@ void InstanceState::validate() const {
 }
 
 const TaskClass& Workload::class_of(const Request& r) const {
-    auto it = class_index_.find(r.task_class_id);
-    if (it == class_index_.end())
-        throw DataError("request " + std::to_string(r.id) + ": unknown task_class_id " + std::to_string(r.task_class_id));
-    return classes[it->second];
+    const TaskClass* t = find_class(r.task_class_id);
+    if (!t) throw DataError("request " + std::to_string(r.id) + ": unknown task_class_id " + std::to_string(r.task_class_id));
+    return *t;
 }
 
 const TaskClass* Workload::find_class(int class_id) const {
+    if (classes.size() <= 8) {  // a handful of classes: a scan beats hashing
+        for (const auto& t : classes)
+            if (t.id == class_id) return &t;
+        return nullptr;
+    }
     auto it = class_index_.find(class_id);
     return it == class_index_.end() ? nullptr : &classes[it->second];
 }
 
 const Request* Workload::find_request(int request_id) const {
+    if (!dense_.empty()) {
+        const long long k = (long long)request_id - dense_lo_;
+        if (k < 0 || k >= (long long)dense_.size() || !dense_[k]) return nullptr;
+        return &requests[dense_[k] - 1];
+    }
     auto it = request_index_.find(request_id);
     return it == request_index_.end() ? nullptr : &requests[it->second];
 }
@@ -135,16 +144,34 @@ Workload validate_workload(std::vector<Request> requests, std::vector<TaskClass>
     Workload w;
     w.classes = std::move(classes);
     w.requests = std::move(requests);
+    w.class_index_.reserve(w.classes.size());
     for (std::size_t i = 0; i < w.classes.size(); ++i) {
         w.classes[i].validate();
         if (!w.class_index_.emplace(w.classes[i].id, i).second)
             throw DataError("duplicate task class id " + std::to_string(w.classes[i].id));
     }
-    for (std::size_t i = 0; i < w.requests.size(); ++i) {
+    const std::size_t n = w.requests.size();
+    long long lo = 0, hi = -1;
+    for (std::size_t i = 0; i < n; ++i) {
+        const long long id = w.requests[i].id;
+        lo = i ? std::min(lo, id) : id, hi = i ? std::max(hi, id) : id;
+    }
+    const bool dense = n > 0 && hi - lo < 4 * (long long)n + 64;
+    if (dense) w.dense_lo_ = lo, w.dense_.assign((std::size_t)(hi - lo + 1), 0u);
+    else w.request_index_.reserve(n);
+    for (std::size_t i = 0; i < n; ++i) {
         const Request& r = w.requests[i];
         r.validate();
-        if (!w.request_index_.emplace(r.id, i).second) throw DataError("duplicate request id " + std::to_string(r.id));
-        if (!w.class_index_.count(r.task_class_id))
+        bool fresh;
+        if (dense) {
+            std::uint32_t& slot = w.dense_[(std::size_t)(r.id - lo)];
+            fresh = slot == 0;
+            if (fresh) slot = (std::uint32_t)(i + 1);
+        } else {
+            fresh = w.request_index_.emplace(r.id, i).second;
+        }
+        if (!fresh) throw DataError("duplicate request id " + std::to_string(r.id));
+        if (!w.find_class(r.task_class_id))
             throw DataError("request " + std::to_string(r.id) + ": unknown task_class_id " + std::to_string(r.task_class_id));
     }
     return w;
