@@ -239,6 +239,7 @@ def run_ours(args):
     w = synthetic_workload(args.n)
     c = S.table_coefficients()
     ids = sorted(w.ids())
+    ids_host = np.asarray(ids, dtype=np.int32)  # the request ids as a caller holds them: a host int32 array
     n, mb = len(ids), args.mb
     chains_total = args.chains * world
     cb, ce = rank * args.chains, (rank + 1) * args.chains
@@ -272,11 +273,11 @@ def run_ours(args):
     cal = S.AnnealConfig(t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                          chains=chains_total, chain_begin=cb, chain_end=ce, budget_ms=2.0,
                          scale_ladder=SCALE_LADDER, device=local)
-    S.anneal_flat(w, ids, c, cal, mb)
+    S.anneal_flat(w, ids_host, c, cal, mb)
     host_ms = 0.0
     for _ in range(5):
         t0 = time.perf_counter()
-        st = S.anneal_flat(w, ids, c, cal, mb)[5]
+        st = S.anneal_flat(w, ids_host, c, cal, mb)[5]
         host_ms = max(host_ms, (time.perf_counter() - t0) * 1e3 - st.kernel_ms)
     if dist:
         hm = torch.tensor([host_ms], dtype=torch.float64, device=xdev or "cpu")
@@ -346,13 +347,13 @@ def run_ours(args):
     cfg = S.AnnealConfig(t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                          chains=chains_total, chain_begin=cb, chain_end=ce, budget_ms=kernel_budget_ms,
                          scale_ladder=SCALE_LADDER, device=local)
-    S.anneal_flat(w, ids, c, cfg, mb)  # warm the context pool
+    S.anneal_flat(w, ids_host, c, cfg, mb)  # warm the context pool
     e2e_props, e2e_s, final = 0.0, 0.0, None
     if dist:
         dist.barrier()
     for _ in range(args.e2e_steps):
         t0 = time.perf_counter()
-        seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids, c, cfg, mb)
+        seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids_host, c, cfg, mb)
         if dist:
             _, seq, sizes, (g, n_met) = exchange_best(
                 LocalBest(st.engine_g, st.engine_t, st.best_chain, seq, sizes, g, n_met), n, device=xdev,
