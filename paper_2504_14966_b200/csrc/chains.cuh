@@ -494,30 +494,138 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
             }
             const double scale = p.n_mult > 0 ? p.scale * p.scale_mult[cid % (uint32_t)p.n_mult] : p.scale;
             sinv = scale * inv_t;
+            // live units form a prefix (E is nondecreasing along the schedule): the count and the
+            // anchor of the first dead unit, for the speculative rejection stage
+            int u_live = 0;
+            long long e_dead = kPadE;
+            auto refresh_live = [&]() {
+                if constexpr (UPL == 1) {
+                    u_live = __popc(__ballot_sync(FULL, cur.E[0] <= dg));
+                    e_dead = u_live < 32 ? __shfl_sync(FULL, cur.E[0], u_live & 31) : kPadE;
+                }
+            };
+            refresh_live();
 
+            int next_check = 8;
             for (int it = 0; it < p.iter; ++it) {
-                if ((it & 7) == 0 && it > 0) {
+                if (it >= next_check) {
                     // the device budget is checked every 8 proposals (warp-uniform), so a launch
                     // overruns it by at most ~8 proposal latencies; the chain is parked as usual
+                    next_check = (it & ~7) + 8;
                     if (p.budget_ns > 0 && __shfl_sync(FULL, gtimer() > deadline ? 1 : 0, 0)) {
                         stop = 1;
                         break;
                     }
                 }
-                const uint32_t prop = (uint32_t)(lev * p.iter + it);
                 if ((it & (kRows - 1)) == 0) {  // lane j draws the row of proposal prop + j
+                    const uint32_t prop0 = (uint32_t)(lev * p.iter + it);
                     __syncwarp();                // every lane is done reading the previous rows
                     if (lane < kRows) {
                         // Philox block b of a row = counter (proposal, chain, b, tag)
                         uint4* dst = reinterpret_cast<uint4*>(rnd + rnd_stride<UPL>() * lane);
 #pragma unroll
                         for (int b = 0; b < kRndBlocks; ++b) {
-                            uint32_t r[4] = {prop + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
+                            uint32_t r[4] = {prop0 + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
                             philox10(r, p.key0, p.key1);
                             dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
                         }
                     }
                     __syncwarp();
+                }
+                if constexpr (UPL == 1) {
+                    if (mb <= 4) {
+                        // Speculative rejection (exact): the next G <= 4 proposals are scored at
+                        // once against the current state, one per 8-lane group. A proposal whose
+                        // first valid attempt (of 8) is a swap in the dead region -- every unit it
+                        // touches or shifts is dead and stays dead -- changes n_met only through
+                        // its +inf-deadline count, so its score needs no walk. While such
+                        // proposals are rejected the state does not change, so each was scored
+                        // against exactly the state the sequential chain would see: the leading
+                        // run of rejected ones is consumed here; the first other proposal (an
+                        // accept, a squeeze/delay, a live-region swap) goes through the general
+                        // path below with the same random words.
+                        const int G = min(4, min(p.iter - it, kRows - (it & (kRows - 1))));
+                        const int g = lane >> 3, sub = lane & 7;
+                        const uint32_t* rg = rnd + rnd_stride<UPL>() * ((it + g) & (kRows - 1));
+                        const uint32_t first = __umulhi(ent[0], magic) + 1u;
+                        const uint32_t r0 = rg[3 * sub], r1 = rg[3 * sub + 1], r2 = rg[3 * sub + 2];
+                        const uint32_t op = lemire32(r0, 3);
+                        const uint32_t a = lemire32(r1, nn);
+                        const uint32_t ps = first + lemire32(r1, nn - first);
+                        uint32_t b = lemire32(r2, nn - 1);
+                        b += b >= a ? 1u : 0u;
+                        const uint32_t pos = op == 0 ? ps : a;
+                        const uint32_t qf = min(pos, nn - 1);
+                        const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
+                        const bool ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
+                        const unsigned gm = (__ballot_sync(FULL, ok) >> (8 * g)) & 0xffu;
+                        const int src = (g << 3) + (gm ? __ffs(gm) - 1 : 0);
+                        const uint32_t opw = __shfl_sync(FULL, op, src);
+                        const uint32_t aw = __shfl_sync(FULL, a, src), bw = __shfl_sync(FULL, b, src);
+                        const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
+                        const uint32_t ea_ = ent[pa], eb_ = ent[pb];
+                        const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
+                        const uint32_t ba = za * nn, bb = zb * nn;
+                        const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
+                        const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
+                        const int ea = sa + (int)za, eb = sb + (int)zb;
+                        const bool firsth = sub < 4;
+                        const int q = firsth ? sa + sub : sb + sub - 4;
+                        const bool act = q <= (firsth ? ea : eb);
+                        uint32_t eo = 0, en = 0;
+                        if (act) {
+                            eo = ent[q];
+                            en = q == pa ? na : (q == pb ? nb : eo);
+                        }
+                        const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
+                        const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
+                        const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
+                        // per-batch maxima over 4-lane halves, the exec delta over the 8 lanes
+                        uint32_t mo = max(xo, __shfl_xor_sync(FULL, xo, 1));
+                        uint32_t mn = max(xn, __shfl_xor_sync(FULL, xn, 1));
+                        mo = max(mo, __shfl_xor_sync(FULL, mo, 2));
+                        mn = max(mn, __shfl_xor_sync(FULL, mn, 2));
+                        const uint32_t mo_x = __shfl_xor_sync(FULL, mo, 4), mn_x = __shfl_xor_sync(FULL, mn, 4);
+                        int dx = (int)xn - (int)xo;
+                        dx += __shfl_xor_sync(FULL, dx, 1);
+                        dx += __shfl_xor_sync(FULL, dx, 2);
+                        dx += __shfl_xor_sync(FULL, dx, 4);
+                        const unsigned gmask = 0xffu << (8 * g);
+                        int dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u) & gmask) -
+                                 __popc(__ballot_sync(FULL, (vo & kAlways) != 0u) & gmask);
+                        const int da = (int)(firsth ? mn : mn_x) - (int)(firsth ? mo : mo_x);
+                        const int db = (int)(firsth ? mn_x : mn) - (int)(firsth ? mo_x : mo);
+                        long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
+                        if (sa == sb) dtot = 0, dA = 0;
+                        const bool elig = g < G && gm != 0 && opw == 2u && (pa >> 5) >= u_live &&
+                                          e_dead + (long long)min(0, min(da, da + db)) > dg;
+                        const double f_g = objective_fast(nm_cur + dA, (double)(tot + dtot) * p.tick);
+                        bool acc = f_g > f;
+                        if (!acc) {
+                            const float x = (float)((f - f_g) * sinv);
+                            const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
+                            acc = u < __expf(-x);
+                        }
+                        const unsigned lead = __ballot_sync(FULL, sub == 0 && elig && !acc);
+                        const unsigned span = (unsigned)(ea - sa + eb - sb + 2);
+                        int k = 0;
+                        unsigned sk = 0;
+#pragma unroll
+                        for (int gg = 0; gg < 4; ++gg) {
+                            const unsigned sp = __shfl_sync(FULL, span, gg << 3);
+                            if (k == gg && gg < G && ((lead >> (8 * gg)) & 1u)) k = gg + 1, sk += sp;
+                        }
+                        props += (unsigned)k, sc1 += sk;
+#ifdef SLO_SPEC_COUNT
+                        sc2 += (unsigned)k << 16;  // diagnostics: proposals consumed by this stage
+#endif
+                        it += k;
+                        __syncwarp();
+                        if (k == G) {
+                            --it;  // the loop increment moves on to the next unconsumed proposal
+                            continue;
+                        }
+                    }
                 }
                 const uint32_t* rw = rnd + rnd_stride<UPL>() * (it & (kRows - 1));
                 const uint32_t pk = draw_move(ent, sqb, dlb, n, magic, rw, lane);
@@ -691,6 +799,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
+                    refresh_live();
                     if (f > best_f) {
                         best_f = f;
                         copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,

@@ -8,6 +8,8 @@
    against a full evaluation of its winner on the tick grid (and within the grid's rounding
    of the exact objective); attainment >= the reference's single chain.
 """
+import math
+
 import numpy as np
 import pytest
 
@@ -530,6 +532,56 @@ def test_chain_trajectory_matches_model(eng, n, mb, three, kind, chains):
         got.append([int(x) for x in bp[q:q + s]])
         q += s
     assert got == runs[win]["best_batches"]
+
+
+@pytest.mark.parametrize("start_kind", ["deadline_first", "mixed"])
+def test_chain_trajectory_through_the_speculative_stage(eng, start_kind):
+    """The bench shape (N=1024, mb=4, generate_mixed): only a short prefix of the 32-position
+    units is live (elapsed <= the largest finite deadline), so most proposals are swaps in the
+    dead region and K3 scores up to four of them at once, consuming the leading rejected ones.
+    The chains must still follow the sequential model exactly."""
+    import k3_model as K
+    n, mb = 1024, 4
+    w = S.generate_mixed(n, 11)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    if start_kind == "deadline_first":
+        pos = {r: k for k, r in enumerate(ids)}
+        start = [[pos[r] for r in b] for b in S.deadline_first_candidate(w, ids, c, mb).batches]
+    else:
+        perm, sizes = _start_schedule(n, mb, "mixed", 7)
+        start, q = [], 0
+        for sz in sizes:
+            start.append(perm[q:q + sz])
+            q += sz
+    # the dead region exists: live units (E <= largest finite deadline, in ticks) are a short prefix
+    finite = dl[np.isfinite(dl) & (dl >= 0)]
+    dg = math.floor(finite.max() / eng.tick_ms)
+    elapsed, unit_e, q = 0, [], 0
+    for bt in start:
+        for _ in bt:
+            if q % 32 == 0:
+                unit_e.append(elapsed)
+            q += 1
+        elapsed += max(int(prob.xt[len(bt) - 1, i]) for i in bt)
+    assert sum(e <= dg for e in unit_e) <= 8
+    f0 = prob.score(start)[2]
+    seed, t0, t_thres, tau, it, chains = 4242, 500.0, 20.0, 0.7, 40, 2
+    perm = [i for b in start for i in b]
+    bp, bs, r = eng.anneal_chains(perm, [len(b) for b in start], chains=chains, t0=t0, t_thres=t_thres, tau=tau,
+                                  iter=it, seed=seed, objective_scale=t0 / f0 * 1e5)
+    runs = [K.run_chain(prob, start, cid, seed, t0, t_thres, tau, it, t0 / f0 * 1e5) for cid in range(chains)]
+    win = min(range(chains), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                   sum(x["accepted"] for x in runs))
+    got, q = [], 0
+    for sz in bs:
+        got.append([int(x) for x in bp[q:q + sz]])
+        q += sz
+    assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
 
 
 @pytest.mark.parametrize("scale", [1e-3, 1e4])
