@@ -499,10 +499,15 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
             int u_live = 0;
             long long e_dead = kPadE;
             auto refresh_live = [&]() {
-                if constexpr (UPL == 1) {
-                    u_live = __popc(__ballot_sync(FULL, cur.E[0] <= dg));
-                    e_dead = u_live < 32 ? __shfl_sync(FULL, cur.E[0], u_live & 31) : kPadE;
-                }
+                int cnt = 0;
+#pragma unroll
+                for (int kk = 0; kk < UPL; ++kk) cnt += __popc(__ballot_sync(FULL, cur.E[kk] <= dg));
+                u_live = cnt;  // unit u = lane * UPL + kk
+                long long ed = kPadE;
+#pragma unroll
+                for (int kk = 0; kk < UPL; ++kk)
+                    if (kk == cnt % UPL) ed = cur.E[kk];
+                e_dead = cnt < 32 * UPL ? __shfl_sync(FULL, ed, (cnt / UPL) & 31) : kPadE;
             };
             refresh_live();
 
@@ -532,7 +537,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                     __syncwarp();
                 }
-                if constexpr (UPL == 1) {
+                {
                     if (mb <= 4) {
                         // Speculative rejection (exact): the next G <= 4 proposals are scored at
                         // once against the current state, one per 8-lane group. A proposal whose

@@ -534,14 +534,15 @@ def test_chain_trajectory_matches_model(eng, n, mb, three, kind, chains):
     assert got == runs[win]["best_batches"]
 
 
-@pytest.mark.parametrize("start_kind", ["deadline_first", "mixed"])
-def test_chain_trajectory_through_the_speculative_stage(eng, start_kind):
+@pytest.mark.parametrize("n,start_kind", [(1024, "deadline_first"), (1024, "mixed"), (2048, "deadline_first"),
+                                          (3000, "deadline_first")])
+def test_chain_trajectory_through_the_speculative_stage(eng, n, start_kind):
     """The bench shape (N=1024, mb=4, generate_mixed): only a short prefix of the 32-position
     units is live (elapsed <= the largest finite deadline), so most proposals are swaps in the
     dead region and K3 scores up to four of them at once, consuming the leading rejected ones.
-    The chains must still follow the sequential model exactly."""
+    The chains must still follow the sequential model exactly (1, 2 and 4 units per lane)."""
     import k3_model as K
-    n, mb = 1024, 4
+    mb = 4
     w = S.generate_mixed(n, 11)
     c = S.table_coefficients()
     ids = sorted(w.ids())
