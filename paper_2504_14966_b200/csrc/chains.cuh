@@ -541,7 +541,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     if (mb <= 4) {
                         // Speculative rejection (exact): the next G <= 4 proposals are scored at
                         // once against the current state, one per 8-lane group. A proposal whose
-                        // first valid attempt (of 8) is a swap in the dead region -- every unit it
+                        // move (first valid attempt of 8, else the forced swap) is a swap in the
+                        // dead region -- every unit it
                         // touches or shifts is dead and stays dead -- changes n_met only through
                         // its +inf-deadline count, so its score needs no walk. While such
                         // proposals are rejected the state does not change, so each was scored
@@ -565,8 +566,13 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const bool ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
                         const unsigned gm = (__ballot_sync(FULL, ok) >> (8 * g)) & 0xffu;
                         const int src = (g << 3) + (gm ? __ffs(gm) - 1 : 0);
-                        const uint32_t opw = __shfl_sync(FULL, op, src);
-                        const uint32_t aw = __shfl_sync(FULL, a, src), bw = __shfl_sync(FULL, b, src);
+                        // no valid attempt among the 8: the reference's forced swap (attempt 8)
+                        const uint32_t a8 = lemire32(rg[3 * (kAttempts - 1) + 1], nn);
+                        uint32_t b8 = lemire32(rg[3 * (kAttempts - 1) + 2], nn - 1);
+                        b8 += b8 >= a8 ? 1u : 0u;
+                        const uint32_t ops = __shfl_sync(FULL, op, src);
+                        const uint32_t as = __shfl_sync(FULL, a, src), bs = __shfl_sync(FULL, b, src);
+                        const uint32_t opw = gm ? ops : 2u, aw = gm ? as : a8, bw = gm ? bs : b8;
                         const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
                         const uint32_t ea_ = ent[pa], eb_ = ent[pb];
                         const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
@@ -602,7 +608,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const int db = (int)(firsth ? mn_x : mn) - (int)(firsth ? mo_x : mo);
                         long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
                         if (sa == sb) dtot = 0, dA = 0;
-                        const bool elig = g < G && gm != 0 && opw == 2u && (pa >> 5) >= u_live &&
+                        const bool elig = g < G && n >= 2 && opw == 2u && (pa >> 5) >= u_live &&
                                           e_dead + (long long)min(0, min(da, da + db)) > dg;
                         const double f_g = objective_fast(nm_cur + dA, (double)(tot + dtot) * p.tick);
                         bool acc = f_g > f;
