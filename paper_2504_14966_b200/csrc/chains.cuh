@@ -512,6 +512,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
             refresh_live();
 
             int next_check = 8;
+            int pass_it0 = 0, pass_end = 0;  // the speculative pass covering proposals [pass_it0, pass_end)
+            unsigned lead_c = 0, span_c = 0;
             for (int it = 0; it < p.iter; ++it) {
                 if (it >= next_check) {
                     // the device budget is checked every 8 proposals (warp-uniform), so a launch
@@ -550,81 +552,87 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         // run of rejected ones is consumed here; the first other proposal (an
                         // accept, a squeeze/delay, a live-region swap) goes through the general
                         // path below with the same random words.
-                        const int G = min(4, min(p.iter - it, kRows - (it & (kRows - 1))));
-                        const int g = lane >> 3, sub = lane & 7;
-                        const uint32_t* rg = rnd + rnd_stride<UPL>() * ((it + g) & (kRows - 1));
-                        const uint32_t first = __umulhi(ent[0], magic) + 1u;
-                        const uint32_t r0 = rg[3 * sub], r1 = rg[3 * sub + 1], r2 = rg[3 * sub + 2];
-                        const uint32_t op = lemire32(r0, 3);
-                        const uint32_t a = lemire32(r1, nn);
-                        const uint32_t ps = first + lemire32(r1, nn - first);
-                        uint32_t b = lemire32(r2, nn - 1);
-                        b += b >= a ? 1u : 0u;
-                        const uint32_t pos = op == 0 ? ps : a;
-                        const uint32_t qf = min(pos, nn - 1);
-                        const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
-                        const bool ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
-                        const unsigned gm = (__ballot_sync(FULL, ok) >> (8 * g)) & 0xffu;
-                        const int src = (g << 3) + (gm ? __ffs(gm) - 1 : 0);
-                        // no valid attempt among the 8: the reference's forced swap (attempt 8)
-                        const uint32_t a8 = lemire32(rg[3 * (kAttempts - 1) + 1], nn);
-                        uint32_t b8 = lemire32(rg[3 * (kAttempts - 1) + 2], nn - 1);
-                        b8 += b8 >= a8 ? 1u : 0u;
-                        const uint32_t ops = __shfl_sync(FULL, op, src);
-                        const uint32_t as = __shfl_sync(FULL, a, src), bs = __shfl_sync(FULL, b, src);
-                        const uint32_t opw = gm ? ops : 2u, aw = gm ? as : a8, bw = gm ? bs : b8;
-                        const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
-                        const uint32_t ea_ = ent[pa], eb_ = ent[pb];
-                        const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
-                        const uint32_t ba = za * nn, bb = zb * nn;
-                        const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
-                        const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
-                        const int ea = sa + (int)za, eb = sb + (int)zb;
-                        const bool firsth = sub < 4;
-                        const int q = firsth ? sa + sub : sb + sub - 4;
-                        const bool act = q <= (firsth ? ea : eb);
-                        uint32_t eo = 0, en = 0;
-                        if (act) {
-                            eo = ent[q];
-                            en = q == pa ? na : (q == pb ? nb : eo);
+                        if (it >= pass_end) {  // score a new pass of G proposals
+                            const int G = min(4, min(p.iter - it, kRows - (it & (kRows - 1))));
+                            const int g = lane >> 3, sub = lane & 7;
+                            const uint32_t* rg = rnd + rnd_stride<UPL>() * ((it + g) & (kRows - 1));
+                            const uint32_t first = __umulhi(ent[0], magic) + 1u;
+                            const uint32_t r0 = rg[3 * sub], r1 = rg[3 * sub + 1], r2 = rg[3 * sub + 2];
+                            const uint32_t op = lemire32(r0, 3);
+                            const uint32_t a = lemire32(r1, nn);
+                            const uint32_t ps = first + lemire32(r1, nn - first);
+                            uint32_t b = lemire32(r2, nn - 1);
+                            b += b >= a ? 1u : 0u;
+                            const uint32_t pos = op == 0 ? ps : a;
+                            const uint32_t qf = min(pos, nn - 1);
+                            const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
+                            const bool ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
+                            const unsigned gm = (__ballot_sync(FULL, ok) >> (8 * g)) & 0xffu;
+                            const int src = (g << 3) + (gm ? __ffs(gm) - 1 : 0);
+                            // no valid attempt among the 8: the reference's forced swap (attempt 8)
+                            const uint32_t a8 = lemire32(rg[3 * (kAttempts - 1) + 1], nn);
+                            uint32_t b8 = lemire32(rg[3 * (kAttempts - 1) + 2], nn - 1);
+                            b8 += b8 >= a8 ? 1u : 0u;
+                            const uint32_t ops = __shfl_sync(FULL, op, src);
+                            const uint32_t as = __shfl_sync(FULL, a, src), bs = __shfl_sync(FULL, b, src);
+                            const uint32_t opw = gm ? ops : 2u, aw = gm ? as : a8, bw = gm ? bs : b8;
+                            const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
+                            const uint32_t ea_ = ent[pa], eb_ = ent[pb];
+                            const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
+                            const uint32_t ba = za * nn, bb = zb * nn;
+                            const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
+                            const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
+                            const int ea = sa + (int)za, eb = sb + (int)zb;
+                            const bool firsth = sub < 4;
+                            const int q = firsth ? sa + sub : sb + sub - 4;
+                            const bool act = q <= (firsth ? ea : eb);
+                            uint32_t eo = 0, en = 0;
+                            if (act) {
+                                eo = ent[q];
+                                en = q == pa ? na : (q == pb ? nb : eo);
+                            }
+                            const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
+                            const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
+                            const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
+                            // per-batch maxima over 4-lane halves, the exec delta over the 8 lanes
+                            uint32_t mo = max(xo, __shfl_xor_sync(FULL, xo, 1));
+                            uint32_t mn = max(xn, __shfl_xor_sync(FULL, xn, 1));
+                            mo = max(mo, __shfl_xor_sync(FULL, mo, 2));
+                            mn = max(mn, __shfl_xor_sync(FULL, mn, 2));
+                            const uint32_t mo_x = __shfl_xor_sync(FULL, mo, 4), mn_x = __shfl_xor_sync(FULL, mn, 4);
+                            int dx = (int)xn - (int)xo;
+                            dx += __shfl_xor_sync(FULL, dx, 1);
+                            dx += __shfl_xor_sync(FULL, dx, 2);
+                            dx += __shfl_xor_sync(FULL, dx, 4);
+                            const unsigned gmask = 0xffu << (8 * g);
+                            int dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u) & gmask) -
+                                     __popc(__ballot_sync(FULL, (vo & kAlways) != 0u) & gmask);
+                            const int da = (int)(firsth ? mn : mn_x) - (int)(firsth ? mo : mo_x);
+                            const int db = (int)(firsth ? mn_x : mn) - (int)(firsth ? mo_x : mo);
+                            long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
+                            if (sa == sb) dtot = 0, dA = 0;
+                            const bool elig = g < G && n >= 2 && opw == 2u && (pa >> 5) >= u_live &&
+                                              e_dead + (long long)min(0, min(da, da + db)) > dg;
+                            const double f_g = objective_fast(nm_cur + dA, (double)(tot + dtot) * p.tick);
+                            bool acc = f_g > f;
+                            if (!acc) {
+                                const float x = (float)((f - f_g) * sinv);
+                                const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
+                                acc = u < __expf(-x);
+                            }
+                            lead_c = __ballot_sync(FULL, sub == 0 && elig && !acc);
+                            span_c = (unsigned)(ea - sa + eb - sb + 2);
+                            pass_it0 = it, pass_end = it + G;
                         }
-                        const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
-                        const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
-                        const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
-                        // per-batch maxima over 4-lane halves, the exec delta over the 8 lanes
-                        uint32_t mo = max(xo, __shfl_xor_sync(FULL, xo, 1));
-                        uint32_t mn = max(xn, __shfl_xor_sync(FULL, xn, 1));
-                        mo = max(mo, __shfl_xor_sync(FULL, mo, 2));
-                        mn = max(mn, __shfl_xor_sync(FULL, mn, 2));
-                        const uint32_t mo_x = __shfl_xor_sync(FULL, mo, 4), mn_x = __shfl_xor_sync(FULL, mn, 4);
-                        int dx = (int)xn - (int)xo;
-                        dx += __shfl_xor_sync(FULL, dx, 1);
-                        dx += __shfl_xor_sync(FULL, dx, 2);
-                        dx += __shfl_xor_sync(FULL, dx, 4);
-                        const unsigned gmask = 0xffu << (8 * g);
-                        int dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u) & gmask) -
-                                 __popc(__ballot_sync(FULL, (vo & kAlways) != 0u) & gmask);
-                        const int da = (int)(firsth ? mn : mn_x) - (int)(firsth ? mo : mo_x);
-                        const int db = (int)(firsth ? mn_x : mn) - (int)(firsth ? mo_x : mo);
-                        long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
-                        if (sa == sb) dtot = 0, dA = 0;
-                        const bool elig = g < G && n >= 2 && opw == 2u && (pa >> 5) >= u_live &&
-                                          e_dead + (long long)min(0, min(da, da + db)) > dg;
-                        const double f_g = objective_fast(nm_cur + dA, (double)(tot + dtot) * p.tick);
-                        bool acc = f_g > f;
-                        if (!acc) {
-                            const float x = (float)((f - f_g) * sinv);
-                            const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
-                            acc = u < __expf(-x);
-                        }
-                        const unsigned lead = __ballot_sync(FULL, sub == 0 && elig && !acc);
-                        const unsigned span = (unsigned)(ea - sa + eb - sb + 2);
+                        // consume the leading rejected run from proposal it; a pass stays valid
+                        // across general-path rejections (the state is unchanged by them)
+                        const int g0 = it - pass_it0, G = pass_end - pass_it0;
                         int k = 0;
                         unsigned sk = 0;
 #pragma unroll
                         for (int gg = 0; gg < 4; ++gg) {
-                            const unsigned sp = __shfl_sync(FULL, span, gg << 3);
-                            if (k == gg && gg < G && ((lead >> (8 * gg)) & 1u)) k = gg + 1, sk += sp;
+                            const unsigned sp = __shfl_sync(FULL, span_c, gg << 3);
+                            if (gg >= g0 && k == gg - g0 && gg < G && ((lead_c >> (8 * gg)) & 1u)) ++k, sk += sp;
                         }
                         props += (unsigned)k, sc1 += sk;
 #ifdef SLO_SPEC_COUNT
@@ -632,7 +640,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
 #endif
                         it += k;
                         __syncwarp();
-                        if (k == G) {
+                        if (it == pass_end) {
                             --it;  // the loop increment moves on to the next unconsumed proposal
                             continue;
                         }
@@ -811,6 +819,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
                     refresh_live();
+                    pass_end = 0;  // the state changed: later speculative scores are stale
                     if (f > best_f) {
                         best_f = f;
                         copy_state<UPL>(p.best_ent + (size_t)c * kEnt, p.best_bits + (size_t)c * kBits, ent, bits,
