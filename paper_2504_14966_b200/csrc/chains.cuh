@@ -620,20 +620,20 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
                                 acc = u < __expf(-x);
                             }
-                            lead_c = __ballot_sync(FULL, sub == 0 && elig && !acc);
-                            span_c = (unsigned)(ea - sa + eb - sb + 2);
+                            // rejected groups as bits 0-3; positions scanned per group as nibbles
+                            const unsigned rj = __ballot_sync(FULL, sub == 0 && elig && !acc);
+                            lead_c = (rj & 1u) | ((rj >> 7) & 2u) | ((rj >> 14) & 4u) | ((rj >> 21) & 8u);
+                            span_c = __reduce_add_sync(FULL, sub == 0 ? (unsigned)(ea - sa + eb - sb + 2) << (4 * g) : 0u);
                             pass_it0 = it, pass_end = it + G;
                         }
                         // consume the leading rejected run from proposal it; a pass stays valid
                         // across general-path rejections (the state is unchanged by them)
                         const int g0 = it - pass_it0, G = pass_end - pass_it0;
-                        int k = 0;
-                        unsigned sk = 0;
-#pragma unroll
-                        for (int gg = 0; gg < 4; ++gg) {
-                            const unsigned sp = __shfl_sync(FULL, span_c, gg << 3);
-                            if (gg >= g0 && k == gg - g0 && gg < G && ((lead_c >> (8 * gg)) & 1u)) ++k, sk += sp;
-                        }
+                        // k = the run of rejected groups from g0 (trailing ones), sk their scan nibbles
+                        const int k = min(__ffs(~(lead_c >> g0)) - 1, G - g0);
+                        unsigned sk = (span_c >> (4 * g0)) & ((1u << (4 * k)) - 1u);
+                        sk = (sk & 0x0f0fu) + ((sk >> 4) & 0x0f0fu);
+                        sk = (sk & 0xffu) + (sk >> 8);
                         props += (unsigned)k, sc1 += sk;
 #ifdef SLO_SPEC_COUNT
                         sc2 += (unsigned)k << 16;  // diagnostics: proposals consumed by this stage
