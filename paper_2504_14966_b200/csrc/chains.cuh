@@ -327,7 +327,9 @@ __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UP
             const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
             const int cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, ln * UPL + k, lane, Eu, Fu);
             if (lane == ln) ls.W[k] = cnt;
+#ifndef SLO_DIAG
             sc2 += 32;  // only lane 0's count is stored
+#endif
         }
     }
 }
@@ -634,7 +636,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         unsigned sk = (span_c >> (4 * g0)) & ((1u << (4 * k)) - 1u);
                         sk = (sk & 0x0f0fu) + ((sk >> 4) & 0x0f0fu);
                         sk = (sk & 0xffu) + (sk >> 8);
-                        props += (unsigned)k, sc1 += sk;
+                        props += (unsigned)k;
+#ifndef SLO_DIAG
+                        sc1 += sk;
+#endif
 #ifdef SLO_SPEC_COUNT
                         sc2 += (unsigned)k << 16;  // diagnostics: proposals consumed by this stage
 #endif
@@ -650,6 +655,15 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 const uint32_t pk = draw_move(ent, sqb, dlb, n, magic, rw, lane);
                 const uint32_t op = pk >> 30;
                 const int kind = op == 3u ? 0 : (op == 2u ? 2 : 1);
+#ifdef SLO_DIAG
+                if (kind == 2) {  // diagnostics (tools/spec_diag.py): why a proposal took this path
+                    const int a0 = (int)(pk & 0x1fffu), b0 = (int)((pk >> 13) & 0x1fffu);
+                    if ((min(a0, b0) >> 5) < u_live) sc2 += 1u << 16;  // live-region swap
+                    else sc1 += 1u;                                     // accept / shift into the live region
+                } else if (kind == 1) {
+                    sc2 += 1u;  // squeeze / delay
+                }
+#endif
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
@@ -725,7 +739,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         }
                         need[kk] = pu + 31 >= lo && (pu <= hi || delta != 0) && nx.E[kk] <= dg;
                     }
+#ifndef SLO_DIAG
                     sc1 += (unsigned)(hi - lo + 1);
+#endif
                     __syncwarp();
                 } else if (kind == 2) {
                     // swap: batches [sa, ea] and [sb, eb] (sa < sb, or the same batch) keep their
@@ -775,7 +791,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const bool chg = u == (pa >> 5) || u == (pb >> 5) || (pu >= sa && da != 0) || (pu >= sb && db != 0);
                         need[kk] = chg && nx.E[kk] <= dg;
                     }
+#ifndef SLO_DIAG
                     sc1 += (unsigned)(ea - sa + eb - sb + 2);
+#endif
                     bool any = false;
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) any |= need[kk];
