@@ -277,11 +277,17 @@ __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : SLO_RND_RO
 template <int UPL>
 __host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : SLO_RND_STRIDE_WIDE; }
 
+// units at the head of the schedule whose per-position slacks are cached (UPL 1): the live
+// prefix at the bench shape is two to four units
+constexpr int kLiveCap = 3;
+
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
     // entries + a zero word (bits[-1]) and padding + batch-end bitmask + two move-flag bitmasks +
-    // Philox rows (next_end16 may read one word past the bitmask: the first flag word)
-    return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4;
+    // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + (UPL 1)
+    // the slack cache of the first kLiveCap units
+    return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4 +
+           (UPL == 1 ? kLiveCap * 32 * 4 : 0);
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -444,6 +450,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     uint32_t* sqb = bits + kBits;  // move flags (state: copied and parked with the bitmask)
     uint32_t* dlb = bits + 2 * kBits;
     uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16 + 3 * kBits * 4);
+    // sig[q] (UPL 1, q < 32 * min(live units, kLiveCap)): deadline minus batch start of position q
+    // in the committed state, clamped to int32 (INT_MIN: +inf deadline or past the end). A unit
+    // whose contents and batch structure are unchanged and whose anchor moves by d meets
+    // exactly #{q : sig[q] >= d} finite-deadline SLOs (|d| < 2^28), so its walk is a ballot.
+    int* sig = reinterpret_cast<int*>(rnd + rnd_rows<UPL>() * rnd_stride<UPL>());
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
 
@@ -511,7 +522,41 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     if (kk == cnt % UPL) ed = cur.E[kk];
                 e_dead = cnt < 32 * UPL ? __shfl_sync(FULL, ed, (cnt / UPL) & 31) : kPadE;
             };
+            auto refresh_sig = [&]() {
+                if constexpr (UPL == 1) {
+                    __syncwarp();
+                    const int nu = min(u_live, kLiveCap);
+                    for (int u = 0; u < nu; ++u) {
+                        const long long Eu = __shfl_sync(FULL, cur.E[0], u);
+                        const uint32_t Fu = __shfl_sync(FULL, cur.F[0], u);
+                        const int q = (u << 5) + lane;
+                        const uint32_t w = bits[u];
+                        uint32_t x = 0;
+                        long long D = 0;
+                        bool fin = false;
+                        if (q < n) {
+                            const uint32_t e = ent[q];
+                            const uint32_t v = xt_ld<SMEM>(tab, e);
+                            x = v & kTickMask;
+                            if (!(v & kAlways)) D = __ldg(p.dt + e), fin = true;
+                        }
+                        const uint32_t m = seg_max(x, w, lane, mb);
+                        const int f0 = w ? __ffs(w) - 1 : 32;
+                        const uint32_t vv = ((w >> lane) & 1u) ? (lane == f0 ? Fu : m) : 0u;
+                        uint32_t sc = vv;
+#pragma unroll
+                        for (int d = 1; d < 32; d <<= 1) {
+                            const uint32_t up = __shfl_up_sync(FULL, sc, d);
+                            if (lane >= d) sc += up;
+                        }
+                        const long long sl = D - (Eu + (long long)(sc - vv));
+                        sig[q] = fin ? (int)max(min(sl, (long long)INT_MAX), (long long)INT_MIN + 1) : INT_MIN;
+                    }
+                    __syncwarp();
+                }
+            };
             refresh_live();
+            refresh_sig();
 
             int next_check = 8;
             int pass_it0 = 0, pass_end = 0;  // the speculative pass covering proposals [pass_it0, pass_end)
@@ -667,7 +712,24 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
-                bool need[UPL];
+                bool need[UPL], shf[UPL];
+                // live units of the committed state (cached slacks) whose contents and batch
+                // structure the move leaves alone and whose anchor only shifts: count by ballot
+                auto take_cached = [&]() {
+                    if constexpr (UPL == 1) {
+                        const bool ch = need[0] && shf[0] && lane < min(u_live, kLiveCap);
+                        unsigned cm = __ballot_sync(FULL, ch);
+                        const int dE = (int)(nx.E[0] - cur.E[0]);
+                        while (cm) {
+                            const int ln = __ffs(cm) - 1;
+                            cm &= cm - 1;
+                            const int d = __shfl_sync(FULL, dE, ln);
+                            const int cnt = __popc(__ballot_sync(FULL, sig[(ln << 5) + lane] >= d));
+                            if (lane == ln) nx.W[0] = cnt;
+                        }
+                        need[0] = need[0] && !ch;
+                    }
+                };
                 long long dtot = 0;
                 int dA = 0;
                 int q = 0;
@@ -738,7 +800,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             nx.F[kk] = pu > nsp ? mN1 : mN0;
                         }
                         need[kk] = pu + 31 >= lo && (pu <= hi || delta != 0) && nx.E[kk] <= dg;
+                        shf[kk] = pu > hi;
                     }
+                    take_cached();
 #ifndef SLO_DIAG
                     sc1 += (unsigned)(hi - lo + 1);
 #endif
@@ -790,7 +854,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const int u = lane * UPL + kk;
                         const bool chg = u == (pa >> 5) || u == (pb >> 5) || (pu >= sa && da != 0) || (pu >= sb && db != 0);
                         need[kk] = chg && nx.E[kk] <= dg;
+                        shf[kk] = u != (pa >> 5) && u != (pb >> 5) && !(pu >= sa && pu <= ea) && !(pu >= sb && pu <= eb);
                     }
+                    take_cached();
 #ifndef SLO_DIAG
                     sc1 += (unsigned)(ea - sa + eb - sb + 2);
 #endif
@@ -837,6 +903,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
                     refresh_live();
+                    refresh_sig();
                     pass_end = 0;  // the state changed: later speculative scores are stale
                     if (f > best_f) {
                         best_f = f;
