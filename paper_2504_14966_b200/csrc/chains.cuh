@@ -561,6 +561,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
             int next_check = 8;
             int pass_it0 = 0, pass_end = 0;  // the speculative pass covering proposals [pass_it0, pass_end)
             unsigned lead_c = 0, span_c = 0;
+            uint32_t pk_c = kNoMove;  // lane 8g: the move of the pass's proposal g
             for (int it = 0; it < p.iter; ++it) {
                 if (it >= next_check) {
                     // the device budget is checked every 8 proposals (warp-uniform), so a launch
@@ -623,6 +624,9 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             const uint32_t ops = __shfl_sync(FULL, op, src);
                             const uint32_t as = __shfl_sync(FULL, a, src), bs = __shfl_sync(FULL, b, src);
                             const uint32_t opw = gm ? ops : 2u, aw = gm ? as : a8, bw = gm ? bs : b8;
+                            // the group's move packed as draw_move returns it (the general path reuses it)
+                            const uint32_t pks = __shfl_sync(FULL, op << 30 | pos | (op == 2u ? b << 13 : 0u), src);
+                            pk_c = gm ? pks : (n >= 2 ? (2u << 30 | a8 | b8 << 13) : kNoMove);
                             const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
                             const uint32_t ea_ = ent[pa], eb_ = ent[pb];
                             const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
@@ -697,7 +701,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                 }
                 const uint32_t* rw = rnd + rnd_stride<UPL>() * (it & (kRows - 1));
-                const uint32_t pk = draw_move(ent, sqb, dlb, n, magic, rw, lane);
+                const uint32_t pk = mb <= 4 ? __shfl_sync(FULL, pk_c, (it - pass_it0) << 3)
+                                            : draw_move(ent, sqb, dlb, n, magic, rw, lane);
                 const uint32_t op = pk >> 30;
                 const int kind = op == 3u ? 0 : (op == 2u ? 2 : 1);
 #ifdef SLO_DIAG
