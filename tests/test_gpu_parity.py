@@ -585,6 +585,36 @@ def test_chain_trajectory_through_the_speculative_stage(eng, n, start_kind):
     assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
 
 
+def test_parked_chains_match_model(eng):
+    """More chains than resident warps (one block: each warp runs two or three chains, parking
+    each in HBM between temperature levels): every chain still follows the sequential model,
+    through the speculative stage and across park/resume."""
+    import k3_model as K
+    n, mb, chains = 256, 4, 60
+    w = S.generate_mixed(n, 21)
+    c = S.table_coefficients()
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    pos = {r: k for k, r in enumerate(ids)}
+    start = [[pos[r] for r in b] for b in S.deadline_first_candidate(w, ids, c, mb).batches]
+    f0 = prob.score(start)[2]
+    seed, t0, t_thres, tau, it = 777, 500.0, 20.0, 0.7, 20
+    scale = t0 / f0 * 1e4
+    bp, bs, r = eng.anneal_chains([i for b in start for i in b], [len(b) for b in start], chains=chains, t0=t0,
+                                  t_thres=t_thres, tau=tau, iter=it, seed=seed, objective_scale=scale, max_blocks=1)
+    runs = [K.run_chain(prob, start, cid, seed, t0, t_thres, tau, it, scale) for cid in range(chains)]
+    win = min(range(chains), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                   sum(x["accepted"] for x in runs))
+    got, q = [], 0
+    for sz in bs:
+        got.append([int(x) for x in bp[q:q + sz]])
+        q += sz
+    assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
+
+
 @pytest.mark.parametrize("scale", [1e-3, 1e4])
 def test_chain_trajectory_matches_model_at_other_time_scales(eng, scale):
     """The tick grid follows the problem's scale (largest exec < 2^27 ticks): the same queue with
