@@ -280,6 +280,8 @@ __host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : SLO_RND_
 // units at the head of the schedule whose per-position slacks are cached (UPL 1): the live
 // prefix at the bench shape is two to four units
 constexpr int kLiveCap = 3;
+// words of a speculative pass's per-group swap record (the general path reads it back)
+constexpr int kSwapRecWords = 12;
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
@@ -287,7 +289,7 @@ __host__ __device__ constexpr int slot_bytes() {
     // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + (UPL 1)
     // the slack cache of the first kLiveCap units
     return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4 +
-           (UPL == 1 ? kLiveCap * 32 * 4 : 0);
+           (UPL == 1 ? kLiveCap * 32 * 4 : 0) + 4 * kSwapRecWords * 4;
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -455,6 +457,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     // whose contents and batch structure are unchanged and whose anchor moves by d meets
     // exactly #{q : sig[q] >= d} finite-deadline SLOs (|d| < 2^28), so its walk is a ballot.
     int* sig = reinterpret_cast<int*>(rnd + rnd_rows<UPL>() * rnd_stride<UPL>());
+    // per group of the current speculative pass: its swap decoded and scored (pa|pb, sa|sb, ea|eb,
+    // na|nb, old entries, new makespans, makespan deltas, total delta, +inf delta), so a swap
+    // that goes on to the general path is not decoded and gathered twice
+    uint32_t* prec = reinterpret_cast<uint32_t*>(sig + (UPL == 1 ? kLiveCap * 32 : 0));
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
 
@@ -671,6 +677,15 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
                                 acc = u < __expf(-x);
                             }
+                            __syncwarp();  // the general path is done reading the previous pass's records
+                            if (sub == 0) {
+                                uint4* rec = reinterpret_cast<uint4*>(prec + kSwapRecWords * g);
+                                rec[0] = make_uint4((uint32_t)pa | (uint32_t)pb << 16, (uint32_t)sa | (uint32_t)sb << 16,
+                                                    (uint32_t)ea | (uint32_t)eb << 16, na | nb << 16);
+                                rec[1] = make_uint4(ea_ | eb_ << 16, mn, mn_x, (uint32_t)da);
+                                rec[2] = make_uint4((uint32_t)db, (uint32_t)(unsigned long long)dtot,
+                                                    (uint32_t)((unsigned long long)dtot >> 32), (uint32_t)dA);
+                            }
                             // rejected groups as bits 0-3; positions scanned per group as nibbles
                             const unsigned rj = __ballot_sync(FULL, sub == 0 && elig && !acc);
                             lead_c = (rj & 1u) | ((rj >> 7) & 2u) | ((rj >> 14) & 4u) | ((rj >> 21) & 8u);
@@ -717,7 +732,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
 
                 // ---- apply in place (undo on reject) and score from the rebuilt batches
                 LaneState<UPL> nx = cur;
-                bool need[UPL], shf[UPL];
+                bool need[UPL] = {}, shf[UPL] = {};
                 // live units of the committed state (cached slacks) whose contents and batch
                 // structure the move leaves alone and whose anchor only shifts: count by ballot
                 auto take_cached = [&]() {
@@ -815,39 +830,54 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 } else if (kind == 2) {
                     // swap: batches [sa, ea] and [sb, eb] (sa < sb, or the same batch) keep their
                     // sizes; lanes 0-15 cover the first, 16-31 the second
-                    const int sa0 = (int)(pk & 0x1fffu), sb0 = (int)((pk >> 13) & 0x1fffu);
-                    const int pa = min(sa0, sb0), pb = max(sa0, sb0);
-                    const uint32_t ea_ = ent[pa], eb_ = ent[pb];
-                    ow0 = ea_, ow1 = eb_;
-                    const uint32_t za = __umulhi(ea_, magic);  // batch size - 1
-                    const uint32_t zb = __umulhi(eb_, magic);
-                    const uint32_t ba = za * nn, bb = zb * nn;
-                    const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
-                    const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
-                    const int ea = sa + (int)za, eb = sb + (int)zb;
-                    const bool first = lane < 16;
-                    q = first ? sa + lane : sb + lane - 16;
-                    const bool act = q <= (first ? ea : eb);
-                    uint32_t eo = 0, en = 0;
-                    if (act) {
-                        eo = ent[q];
-                        en = q == pa ? na : (q == pb ? nb : eo);
+                    int pa, pb, sa, sb, ea, eb, da, db;
+                    uint32_t na, nb, mN0, mN1;
+                    if (mb <= 4) {  // the speculative pass decoded and scored this swap already
+                        const uint4* rec = reinterpret_cast<const uint4*>(prec + kSwapRecWords * (it - pass_it0));
+                        const uint4 r0 = rec[0], r1 = rec[1], r2 = rec[2];
+                        pa = (int)(r0.x & 0xffffu), pb = (int)(r0.x >> 16);
+                        sa = (int)(r0.y & 0xffffu), sb = (int)(r0.y >> 16);
+                        ea = (int)(r0.z & 0xffffu), eb = (int)(r0.z >> 16);
+                        na = r0.w & 0xffffu, nb = r0.w >> 16;
+                        ow0 = r1.x & 0xffffu, ow1 = r1.x >> 16;
+                        mN0 = r1.y, mN1 = r1.z, da = (int)r1.w, db = (int)r2.x;
+                        dtot = (long long)((unsigned long long)r2.y | (unsigned long long)r2.z << 32);
+                        dA = (int)r2.w;
+                    } else {
+                        const int sa0 = (int)(pk & 0x1fffu), sb0 = (int)((pk >> 13) & 0x1fffu);
+                        pa = min(sa0, sb0), pb = max(sa0, sb0);
+                        const uint32_t ea_ = ent[pa], eb_ = ent[pb];
+                        ow0 = ea_, ow1 = eb_;
+                        const uint32_t za = __umulhi(ea_, magic);  // batch size - 1
+                        const uint32_t zb = __umulhi(eb_, magic);
+                        const uint32_t ba = za * nn, bb = zb * nn;
+                        na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
+                        sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
+                        ea = sa + (int)za, eb = sb + (int)zb;
+                        const bool first = lane < 16;
+                        q = first ? sa + lane : sb + lane - 16;
+                        const bool act = q <= (first ? ea : eb);
+                        uint32_t eo = 0, en = 0;
+                        if (act) {
+                            eo = ent[q];
+                            en = q == pa ? na : (q == pb ? nb : eo);
+                        }
+                        const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
+                        const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
+                        const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
+                        const uint32_t mO0 = __reduce_max_sync(FULL, first ? xo : 0u);
+                        const uint32_t mO1 = __reduce_max_sync(FULL, first ? 0u : xo);
+                        mN0 = __reduce_max_sync(FULL, first ? xn : 0u);
+                        mN1 = __reduce_max_sync(FULL, first ? 0u : xn);
+                        const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
+                        dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
+                        da = (int)mN0 - (int)mO0, db = (int)mN1 - (int)mO1;
+                        dtot = sN - sO + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
+                        if (sa == sb) dtot = 0, dA = 0;  // one batch: order inside a batch changes nothing
                     }
                     // the swap is written to shared memory only when an SLO walk or an accept needs
                     // it (the common rejected swap never touches the state)
                     sw_na = na, sw_nb = nb, sw_pa = pa, sw_pb = pb;
-                    const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
-                    const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
-                    const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
-                    const uint32_t mO0 = __reduce_max_sync(FULL, first ? xo : 0u);
-                    const uint32_t mO1 = __reduce_max_sync(FULL, first ? 0u : xo);
-                    const uint32_t mN0 = __reduce_max_sync(FULL, first ? xn : 0u);
-                    const uint32_t mN1 = __reduce_max_sync(FULL, first ? 0u : xn);
-                    const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
-                    dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
-                    const int da = (int)mN0 - (int)mO0, db = (int)mN1 - (int)mO1;
-                    dtot = sN - sO + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
-                    if (sa == sb) dtot = 0, dA = 0;  // one batch: order inside a batch changes nothing
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) {
                         const int pu = (lane * UPL + kk) << 5;
