@@ -86,7 +86,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("rep")
     ap.add_argument("--desc", default="k_chains<1> (N=1024, mb=4, 16384 chains, bench configuration via "
-                    "tools/prof_chains.py --bench: best of three starts, t0=500 tau=0.7 iter=100, 7 levels, "
+                    "tools/prof_chains.py --bench: best of three starts, t0=500 tau=0.7 iter=300, 8 levels, "
                     "scale ladder 1e4..1e8, no budget)")
     ap.add_argument("--proposals", type=float, required=True)
     ap.add_argument("--tag", required=True)

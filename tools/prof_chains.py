@@ -3,9 +3,9 @@ kernel does identical work).
 
     python tools/prof_chains.py [n] [chains] [reps] [3class]
         legacy shape: reference start, t0=500 tau=0.5 iter=32, scale ladder 1..1e5
-    python tools/prof_chains.py --bench [--n 1024] [--chains 16384] [--levels 7] [--reps 1]
-        bench.py's configuration (best of the three starts, t0=500 tau=0.7 iter=100, scale ladder
-        1e4..1e8) for a fixed number of temperature levels (7 ~ the levels the 8.9 ms device
+    python tools/prof_chains.py --bench [--n 1024] [--chains 16384] [--levels 8] [--reps 1]
+        bench.py's configuration (best of the three starts, t0=500 tau=0.7 iter=300, scale ladder
+        1e4..1e8) for a fixed number of temperature levels (8 ~ the levels the 9 ms device
         budget allows at N=1024), so the ncu instruction count per proposal describes the bench run
 """
 import argparse
@@ -27,7 +27,7 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--mb", type=int, default=4)
     ap.add_argument("--chains", type=int, default=16384)
-    ap.add_argument("--levels", type=int, default=7)
+    ap.add_argument("--levels", type=int, default=8)
     ap.add_argument("--reps", type=int, default=1)
     a = ap.parse_args()
     n, chains, reps, three = a.n, a.chains, a.reps, False
@@ -56,7 +56,7 @@ def main():
         ev_d = S.evaluate(d, c, w)
         if ev_d.g > f0:
             start, f0 = d, ev_d.g
-        t0, tau, it = 500.0, 0.7, 100
+        t0, tau, it = 500.0, 0.7, 300
         t_thres = t0 * tau ** (a.levels - 0.5)
         kw = dict(t0=t0, tau=tau, iter=it, t_thres=t_thres, seed=0, objective_scale=t0 / f0, chains=chains,
                   scale_ladder=BENCH_LADDER)
