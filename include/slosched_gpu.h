@@ -82,6 +82,16 @@ double slo_problem_tick_ms(slo_ctx* ctx);
 int slo_evaluate_batch(slo_ctx* ctx, int32_t count, const uint16_t* perms,
                        const uint32_t* batch_end_bits, int32_t* n_met, double* t, double* g);
 
+/* The chain kernel's own objective of `count` candidates (same layout as slo_evaluate_batch):
+ * n_met bit-exact with CostModel::score -- the tick grid decides an SLO test only where its
+ * rounding bound certifies it, the rest is re-summed in the reference's fp64 order -- and t (g)
+ * on the grid, within 2^-26 relative of the reference's. exact_walks (may be NULL) receives
+ * the number of 32-position units decided by the fp64 re-sum. Needs finite, non-negative exec
+ * times. */
+int slo_evaluate_batch_tick(slo_ctx* ctx, int32_t count, const uint16_t* perms,
+                            const uint32_t* batch_end_bits, int32_t* n_met, double* t, double* g,
+                            uint64_t* exact_walks);
+
 typedef struct {
     double t0, t_thres; /* AnnealConfig (P:include/slosched/priority_mapper.hpp:16-28) */
     int32_t iter;
@@ -99,7 +109,7 @@ typedef struct {
 } slo_chain_params;
 
 typedef struct {
-    double g;            /* best score found (chain kernel: exact on the 2^-k ms tick grid) */
+    double g;            /* best score found (chain kernel: n_met exact, t on the 2^-k ms tick grid) */
     double t;            /* its summed latency (ticks x tick) */
     int32_t n_met;
     int32_t chain;       /* winning chain id (ties: lower t, then lower id) */
@@ -110,6 +120,9 @@ typedef struct {
     float kernel_ms;     /* device time of the annealing launches (CUDA events) */
     uint64_t positions_pass1; /* Philox mode: positions of the rebuilt batches scored */
     uint64_t positions_pass2; /*   and positions re-walked for SLO counts (replay: 0) */
+    uint64_t exact_walks;     /* Philox mode: 32-position unit walks the tick grid could not certify,
+                                 decided by the reference's fp64 arithmetic (n_met is always the
+                                 reference's) */
 } slo_chain_result;
 
 /* Run chains from the start schedule (dense indices in position order + batch sizes) and

@@ -52,7 +52,7 @@ class SloChainResult(Structure):
     _fields_ = [("g", c_double), ("t", c_double), ("n_met", c_int32), ("chain", c_int32),
                 ("proposals", c_uint64), ("accepted", c_uint64), ("chains_run", c_int32),
                 ("levels_run", c_int32), ("kernel_ms", c_float), ("positions_pass1", c_uint64),
-                ("positions_pass2", c_uint64)]
+                ("positions_pass2", c_uint64), ("exact_walks", c_uint64)]
 
 
 _I = POINTER(c_int32)
@@ -70,6 +70,8 @@ _SIGNATURES = [
     ("slo_problem_set", c_int32, [c_void_p, c_int32, c_int32, _D, _D]),
     ("slo_problem_tick_ms", c_double, [c_void_p]),
     ("slo_evaluate_batch", c_int32, [c_void_p, c_int32, POINTER(ctypes.c_uint16), POINTER(c_uint32), _I, _D, _D]),
+    ("slo_evaluate_batch_tick", c_int32, [c_void_p, c_int32, POINTER(ctypes.c_uint16), POINTER(c_uint32), _I, _D, _D,
+                                          POINTER(c_uint64)]),
     ("slo_anneal_chains", c_int32, [c_void_p, POINTER(SloChainParams), _I, _I, c_int32, _I, _I, _I,
                                     POINTER(SloChainResult)]),
     ("slo_chains_prepare", c_int32, [c_void_p, POINTER(SloChainParams), _I, _I, c_int32]),
@@ -111,6 +113,8 @@ def lib():
                               "(the scheduler has no CPU fallback)")
         L = ctypes.CDLL(LIB_PATH)
         for name, res, args in _SIGNATURES:
+            if os.environ.get("SLOSCHED_LIB") and not hasattr(L, name):
+                continue  # an older variant library (A/B timing runs) may lack newer entry points
             fn = getattr(L, name)
             fn.restype = res
             fn.argtypes = args

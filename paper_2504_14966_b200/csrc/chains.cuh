@@ -66,7 +66,10 @@ struct ChainParams {
                          // umulhi(e, magic) == e / n exactly for e < 65536, 2 <= n <= 4096
     const uint32_t* xt;  // global [mb][n] exec ticks | kAlways
     const long long* dt; // global [mb][n] deadline ticks (-1: never met; unused where kAlways)
-    long long dg;        // largest finite deadline (ticks): units with E > dg are dead
+    long long dg;        // live bound (ticks): the largest finite deadline + cert_margin(n) (-1: none); units
+                         // with E > dg are dead -- no SLO met there, certified (unit_walk)
+    const double2* tab64; // global [mb][n] {exec, latest start} fp64: the reference's SLO test
+    unsigned long long* exact_count;  // SLO tests the grid could not certify (exact_met)
     double tick;         // 2^-k ms
     int smem_tab;
     double t0, tau, scale;
@@ -139,11 +142,74 @@ __device__ __forceinline__ uint32_t seg_max(uint32_t x, uint32_t w, int lane, in
     return m;
 }
 
+// ---- SLO tests: certified on the tick grid, the rest in the reference's fp64 arithmetic
+//
+// The reference's elapsed time at a batch start is a left-to-right fp64 sum of the makespans
+// before it (P:src/priority_mapper.cpp:264-276); the grid's is an exact integer sum of the same
+// makespans rounded to ticks. With j batches before position q (j <= q), the two differ by at most
+// j/2 ticks of rounding plus j * 2^-14 ticks of fp64 rounding (elapsed < 2^39 ticks), and the
+// deadline tick is floor(D * 2^k). So a test whose tick slack d = dt - elapsed has
+// |d| > cert_margin(q) = q/2 + 2 is met in the reference iff d >= 0. The rest (rare: ~1e-4 walks
+// per proposal at the bench shape) is decided by re-summing in fp64 (exact_chunk). n_met is the
+// reference's, bit for bit.
+__device__ __forceinline__ int cert_margin(int q) { return (q >> 1) + 2; }
+
+struct ExactRef {
+    const double2* tab;        // [mb][n] {exec, latest start} fp64
+    unsigned long long* count; // units decided by exact_chunk (statistics; may be null)
+};
+// Per block (set once by the kernels that walk): kept out of the walks' register arguments, since
+// only the rare exact path reads it.
+__shared__ ExactRef s_xr;
+
+// The reference's SLO tests of one 32-position chunk c (walk_units calls it for chunks 0..u): the
+// elapsed time goes on in fp64 makespan by makespan (elapsed += max(0.0, exec...)) and each batch
+// start is compared with the fp64 latest-start table (met <=> elapsed <= latest start). The
+// chunk's makespans come from a segmented max (exact in any order); only the additions are
+// sequential. Loop-free: a loop in any function the walk reaches costs the chain kernel registers.
+struct ExactStep {
+    double E;      // elapsed at the start of the batch open after the chunk (warp-uniform)
+    double mc;     // that batch's running makespan (warp-uniform)
+    unsigned met;  // finite-deadline positions of the chunk that meet their SLO
+};
+
+__device__ __noinline__ ExactStep exact_chunk(const uint16_t* ent, const uint32_t* bits, const double2* tab, int n,
+                                              int mb, int c, int lane, double E, double mc) {
+    const int q = (c << 5) + lane;
+    const uint32_t w = bits[c];
+    double2 v = make_double2(0.0, -INFINITY);
+    if (q < n) v = __ldg(&tab[ent[q]]);
+    const uint32_t below = w & ((1u << lane) - 1u);
+    const int span = lane - (below ? 32 - __clz(below) : 0);
+    double m = v.x;
+#pragma unroll
+    for (int d = 1; d < 16; d <<= 1) {  // batches <= 16
+        const double mu = __shfl_up_sync(FULL, m, d);
+        if (d < mb && d <= span) m = dmax(m, mu);
+    }
+    m = dmax(below ? 0.0 : mc, m);  // the open batch carries its partial makespan in
+    double Ec = E, Es = E;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) {
+        const double mk = __shfl_sync(FULL, m, k);
+        if ((w >> k) & 1u) {
+            Ec = Ec + mk;
+            if (lane > k) Es = Ec;
+        }
+    }
+    const double mlast = __shfl_sync(FULL, m, 31);
+    ExactStep r;
+    r.E = Ec;
+    r.mc = (w >> 31) & 1u ? 0.0 : mlast;
+    r.met = __ballot_sync(FULL, q < n && v.y != INFINITY && Es <= v.y);
+    return r;
+}
+
 // Cooperative count of the met finite-deadline SLOs of unit u, whose first batch started at
-// elapsed E with makespan F. Rare (live units whose inputs changed): kept out of line.
+// elapsed E with makespan F, on the tick grid; -1 when some test is not certified.
 template <bool SMEM>
-__device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
-                                      int n, int mb, int u, int lane, long long E, uint32_t F) {
+__device__ __forceinline__ int unit_count(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
+                                          int n, int mb, int u, int lane, long long E, uint32_t F) {
     const int q = (u << 5) + lane;
     const uint32_t w = bits[u];
     uint32_t x = 0;
@@ -163,8 +229,20 @@ __device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits,
         const uint32_t up = __shfl_up_sync(FULL, s, d);
         if (lane >= d) s += up;
     }
-    const bool met = q < n && E + (long long)(s - v) <= D;
-    return __popc(__ballot_sync(FULL, met));
+    // D < 0: no elapsed time >= 0 meets the deadline (the reference's elapsed is >= 0 too)
+    const long long sl = D - (E + (long long)(s - v));
+    const unsigned marg = (unsigned)cert_margin(q);
+    const bool amb = D >= 0 && (unsigned long long)(sl + marg) <= 2ull * marg;
+    const unsigned met = __ballot_sync(FULL, D >= 0 && sl >= 0);
+    if (__any_sync(FULL, amb)) return -1;
+    return __popc(met);
+}
+
+// -1: some test needs the reference arithmetic (walk_units then runs exact_chunk over the prefix)
+template <bool SMEM>
+__device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
+                                      int n, int mb, int u, int lane, long long E, uint32_t F) {
+    return unit_count<SMEM>(ent, bits, tab, dt, n, mb, u, lane, E, F);
 }
 
 struct Move {         // also the move record of K2 (replay.cuh)
@@ -321,23 +399,43 @@ __device__ __forceinline__ void rebuild_flags(const uint16_t* ent, const uint32_
 }
 
 // Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts.
+// Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts. A unit
+// the tick grid cannot certify (unit_walk returns -1) is decided by exact_chunk over chunks 0..u,
+// one chunk per trip of the same loop (a separate loop, anywhere on this path, costs the chain
+// kernel registers on every walk).
 template <int UPL, bool SMEM>
 __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UPL>& ls, const uint16_t* ent,
-                                           const uint32_t* bits, const TabRef& tab, const long long* dt, int n,
-                                           int mb, int lane, unsigned& sc2) {
+                                           const uint32_t* bits, const TabRef& tab, const long long* dt,
+                                           int n, int mb, int lane, unsigned& sc2) {
 #pragma unroll
     for (int k = 0; k < UPL; ++k) {
         unsigned mask = __ballot_sync(FULL, need[k]);
+        int c = -1;  // -1: the tick walk of the next unit; >= 0: its exact chunk c
+        ExactStep st{0.0, 0.0, 0u};
         while (mask) {
             const int ln = __ffs(mask) - 1;
-            mask &= mask - 1;
-            const long long Eu = __shfl_sync(FULL, ls.E[k], ln);
-            const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
-            const int cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, ln * UPL + k, lane, Eu, Fu);
-            if (lane == ln) ls.W[k] = cnt;
+            const int u = ln * UPL + k;
+            int cnt = -1;
+            if (c < 0) {
+                const long long Eu = __shfl_sync(FULL, ls.E[k], ln);
+                const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
+                cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, u, lane, Eu, Fu);
 #ifndef SLO_DIAG
-            sc2 += 32;  // only lane 0's count is stored
+                sc2 += 32;  // only lane 0's count is stored
 #endif
+                if (cnt < 0) {
+                    c = 0, st = ExactStep{0.0, 0.0, 0u};
+                    if (lane == 0 && s_xr.count) atomicAdd(s_xr.count, 1ull);
+                }
+            } else {
+                st = exact_chunk(ent, bits, s_xr.tab, n, mb, c, lane, st.E, st.mc);
+                if (c == u) cnt = __popc(st.met), c = -1;
+                else ++c;
+            }
+            if (cnt >= 0) {
+                if (lane == ln) ls.W[k] = cnt;
+                mask &= mask - 1;
+            }
         }
     }
 }
@@ -350,23 +448,17 @@ __device__ __forceinline__ int live_met(const LaneState<UPL>& ls, long long dg) 
     return (int)__reduce_add_sync(FULL, (unsigned)s);
 }
 
-// Prologue: one warp evaluates the start schedule shared by every chain and publishes its unit
-// anchors, so the chains start without a full evaluation each.
+// One warp evaluates a schedule from scratch with the chain kernel's arithmetic (tick totals, the
+// certified SLO walk): each lane owns its UPL units, sums their batches sequentially, one warp scan
+// gives the anchors. Es/Fs: kU-entry scratch. Returns the lane's anchors; tot, A, nm warp-uniform.
 template <int UPL>
-__global__ void __launch_bounds__(32) k_start(const ChainParams p) {
-    extern __shared__ __align__(16) unsigned char smem[];
+__device__ void eval_schedule(const ChainParams& p, const uint16_t* ent, const uint32_t* bits, long long* Es,
+                              uint32_t* Fs, int lane, LaneState<UPL>& ls, long long& tot_out, int& A_out,
+                              int& nm_out) {
     constexpr int kU = 32 * UPL;
-    const int lane = threadIdx.x;
     const int n = p.n;
-    long long* Es = reinterpret_cast<long long*>(smem);
-    uint32_t* Fs = reinterpret_cast<uint32_t*>(smem + kU * 8);
-    uint16_t* ent = reinterpret_cast<uint16_t*>(smem + kU * 12);
-    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + kU * 12 + 1024 * UPL * 2 + 16);  // bits[-1] = 0
-    copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
     for (int u = lane; u < kU; u += 32) Es[u] = kPadE, Fs[u] = 0;
-    if (lane == 0) bits[-1] = 0u, bits[kU] = 0u;
     __syncwarp();
-    rebuild_flags(ent, bits, p.start_bits + kU, p.start_bits + 2 * kU, n, p.mb, p.magic, 0, kU - 1, lane);
     // each lane owns positions [q0, q1) (its UPL units); every non-empty range holds a batch end
     // (ranges are >= 32 long, batches <= 16), so the batch open at a range start is closed in it
     const int q0 = lane * 32 * UPL, q1 = min(n, q0 + 32 * UPL);
@@ -410,9 +502,7 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
 #pragma unroll
     for (int d = 16; d; d >>= 1) tot += __shfl_xor_sync(FULL, tot, d);
     A = (int)__reduce_add_sync(FULL, (unsigned)A);
-    if (lane == 0) p.start_obj[0] = tot, p.start_obj[1] = A;
     __syncwarp();
-    LaneState<UPL> ls;
     bool need[UPL];
 #pragma unroll
     for (int k = 0; k < UPL; ++k) {
@@ -422,9 +512,107 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     unsigned sc2 = 0;
     const TabRef tab{p.xt, 0u};
     walk_units<UPL, false>(need, ls, ent, bits, tab, p.dt, n, p.mb, lane, sc2);
-    const int nm = live_met<UPL>(ls, p.dg);
+    tot_out = tot, A_out = A, nm_out = A + live_met<UPL>(ls, p.dg);
+    __syncwarp();
+}
+
+// Prologue: one warp evaluates the start schedule shared by every chain and publishes its unit
+// anchors, so the chains start without a full evaluation each.
+template <int UPL>
+__global__ void __launch_bounds__(32) k_start(const ChainParams p) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kU = 32 * UPL;
+    const int lane = threadIdx.x;
+    long long* Es = reinterpret_cast<long long*>(smem);
+    uint32_t* Fs = reinterpret_cast<uint32_t*>(smem + kU * 8);
+    uint16_t* ent = reinterpret_cast<uint16_t*>(smem + kU * 12);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(smem + kU * 12 + 1024 * UPL * 2 + 16);  // bits[-1] = 0
+    copy_state<UPL>(ent, bits, p.start_ent, p.start_bits, lane);
+    if (lane == 0) bits[-1] = 0u, bits[kU] = 0u, s_xr = ExactRef{p.tab64, p.exact_count};
+    __syncwarp();
+    rebuild_flags(ent, bits, p.start_bits + kU, p.start_bits + 2 * kU, p.n, p.mb, p.magic, 0, kU - 1, lane);
+    LaneState<UPL> ls;
+    long long tot;
+    int A, nm;
+    eval_schedule<UPL>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
     reinterpret_cast<LaneState<UPL>*>(p.start_lane)[lane] = ls;
-    if (lane == 0) p.start_obj[2] = p.start_obj[1] + nm;
+    if (lane == 0) p.start_obj[0] = tot, p.start_obj[1] = A, p.start_obj[2] = nm;
+}
+
+template <int UPL>
+__host__ __device__ constexpr int eval_slot_bytes() {
+    return 32 * UPL * 12 + 1024 * UPL * 2 + 16 + (32 * UPL + 1) * 4 + 12;
+}
+
+// K3 evaluator (slo_evaluate_batch_tick): the chain kernel's objective of given schedules, one
+// warp per candidate -- n_met exactly CostModel::score's (P:src/priority_mapper.cpp:259-279),
+// the total on the tick grid. perms: [count][n] dense indices; bits: [count][words] batch ends.
+// Invalid candidates set error bits 1 (last position not a batch end), 2 (batch > mb), 4 (index
+// out of range) and are not scored.
+template <int UPL>
+__global__ void __launch_bounds__(256) k_eval_tick(const ChainParams p, int count, int words,
+                                                   const uint16_t* __restrict__ perms,
+                                                   const uint32_t* __restrict__ cbits, int* __restrict__ n_met,
+                                                   double* __restrict__ t_out, double* __restrict__ g_out,
+                                                   int* __restrict__ err) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr int kU = 32 * UPL;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    unsigned char* slot = smem + (size_t)wid * eval_slot_bytes<UPL>();
+    long long* Es = reinterpret_cast<long long*>(slot);
+    uint32_t* Fs = reinterpret_cast<uint32_t*>(slot + kU * 8);
+    uint16_t* ent = reinterpret_cast<uint16_t*>(slot + kU * 12);
+    uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kU * 12 + 1024 * UPL * 2 + 16);
+    const int n = p.n;
+    if (threadIdx.x == 0) s_xr = ExactRef{p.tab64, p.exact_count};
+    __syncthreads();
+    for (int c = blockIdx.x * (blockDim.x >> 5) + wid; c < count; c += gridDim.x * (blockDim.x >> 5)) {
+        const uint32_t* cb = cbits + (size_t)c * words;
+        for (int w = lane; w <= kU; w += 32) bits[w] = w < words ? cb[w] : 0u;
+        if (lane == 0) bits[-1] = 0u;
+        __syncwarp();
+        // validation: bit n-1 ends a batch; no batch longer than mb; indices below n
+        bool bad1 = !((bits[(n - 1) >> 5] >> ((n - 1) & 31)) & 1u), bad2 = false, bad4 = false;
+        if (!bad1) {
+            for (int q = lane; q < n; q += 32) {
+                if ((bits[q >> 5] >> (q & 31)) & 1u) {
+                    int s = q - 1;  // previous end (linear search, at most mb + 1 steps when valid)
+                    while (s >= 0 && s >= q - p.mb && !((bits[s >> 5] >> (s & 31)) & 1u)) --s;
+                    if (q - s > p.mb) bad2 = true;
+                }
+            }
+            // bits past n - 1 must be clear
+            for (int w = lane; w < words; w += 32) {
+                const int lo = w << 5;
+                const uint32_t keep = lo + 32 <= n ? FULL : (lo >= n ? 0u : (1u << (n - lo)) - 1u);
+                if (cb[w] & ~keep) bad1 = true;
+            }
+        }
+        const bool fail_v = __any_sync(FULL, bad1 || bad2);
+        if (!fail_v) {
+            for (int q = lane; q < n; q += 32) {
+                const uint32_t i = perms[(size_t)c * n + q];
+                if (i >= (uint32_t)n) bad4 = true;
+                const int sz = next_end16(bits, q) - prev_end16(bits, q);
+                ent[q] = (uint16_t)((uint32_t)(sz - 1) * (uint32_t)n + min(i, (uint32_t)n - 1));
+            }
+        }
+        const unsigned e = (__any_sync(FULL, bad1) ? 1u : 0u) | (__any_sync(FULL, bad2) ? 2u : 0u) |
+                           (__any_sync(FULL, bad4) ? 4u : 0u);
+        __syncwarp();
+        if (e) {
+            if (lane == 0) atomicOr(err, (int)e);
+            continue;
+        }
+        LaneState<UPL> ls;
+        long long tot;
+        int A, nm;
+        eval_schedule<UPL>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
+        if (lane == 0) {
+            const double t = (double)tot * p.tick;
+            n_met[c] = nm, t_out[c] = t, g_out[c] = objective(nm, t);
+        }
+    }
 }
 
 template <int UPL, bool SMEM>
@@ -463,6 +651,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     uint32_t* prec = reinterpret_cast<uint32_t*>(sig + (UPL == 1 ? kLiveCap * 32 : 0));
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
+    if (threadIdx.x == 0) s_xr = ExactRef{p.tab64, p.exact_count};
+    __syncthreads();
 
     const int gw = blockIdx.x * W + wid, TW = gridDim.x * W;
     if (gw >= p.chain_count) return;
@@ -544,7 +734,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             const uint32_t e = ent[q];
                             const uint32_t v = xt_ld<SMEM>(tab, e);
                             x = v & kTickMask;
-                            if (!(v & kAlways)) D = __ldg(p.dt + e), fin = true;
+                            if (!(v & kAlways)) D = __ldg(p.dt + e), fin = D >= 0;
                         }
                         const uint32_t m = seg_max(x, w, lane, mb);
                         const int f0 = w ? __ffs(w) - 1 : 32;
@@ -740,14 +930,19 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const bool ch = need[0] && shf[0] && lane < min(u_live, kLiveCap);
                         unsigned cm = __ballot_sync(FULL, ch);
                         const int dE = (int)(nx.E[0] - cur.E[0]);
+                        bool walk = false;  // a slack the grid cannot certify: walk the unit
                         while (cm) {
                             const int ln = __ffs(cm) - 1;
                             cm &= cm - 1;
                             const int d = __shfl_sync(FULL, dE, ln);
-                            const int cnt = __popc(__ballot_sync(FULL, sig[(ln << 5) + lane] >= d));
-                            if (lane == ln) nx.W[0] = cnt;
+                            const int sg = sig[(ln << 5) + lane];
+                            const int cnt = __popc(__ballot_sync(FULL, sg >= d));
+                            // |sg - d| <= cert_margin(q), in wrapping u32 arithmetic (|sg - d| < 2^31 + 2^28)
+                            const uint32_t mq = (uint32_t)cert_margin((ln << 5) + lane);
+                            const bool amb = __any_sync(FULL, sg != INT_MIN && (uint32_t)sg - (uint32_t)d + mq <= 2u * mq);
+                            if (lane == ln) nx.W[0] = cnt, walk = amb;
                         }
-                        need[0] = need[0] && !ch;
+                        need[0] = need[0] && (!ch || walk);
                     }
                 };
                 long long dtot = 0;

@@ -298,12 +298,13 @@ struct slo_ctx {
     DevBuf tab, exec_soa, dl_soa, xt, dt;
     double tick = 1.0;   // K3 grid: 2^-k ms
     long long dg = -1;   // K3: largest finite deadline in ticks
+    long long marg = 0;  // K3: ticks within which the grid cannot certify an SLO test
     bool exec_nonneg = true;
     // chains
     DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
-        result, win_ent, win_bits;
-    // K1
-    DevBuf e_perms, e_bits, e_n, e_t, e_g, e_err;
+        result, win_ent, win_bits, exact_count;
+    // K1 (and the K3 evaluator)
+    DevBuf e_perms, e_bits, e_n, e_t, e_g, e_err, e_cnt;
     bool prepared = false;
     slo_chain_params prm{};
     int UPL = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
@@ -396,7 +397,8 @@ int slo_problem_set(slo_ctx* c, int32_t n, int32_t mb, const double* exec, const
         while (k > -60 && std::ldexp(emax, k) > (double)kTickMask) --k;
     }
     c->tick = std::ldexp(1.0, -k);
-    c->dg = dmax_fin >= 0.0 ? (long long)std::fmin(std::floor(std::ldexp(dmax_fin, k)), 0x1.0p62) : -1;
+    c->dg = dmax_fin >= 0.0 ? (long long)std::fmin(std::floor(std::ldexp(dmax_fin, k)), 0x1.0p61) : -1;
+    c->marg = n / 2 + 2;  // chains.cuh cert_margin(n): no batch start drifts further from the reference
     c->exec_nonneg = nonneg;
     CK(cudaMemcpyAsync(c->exec_soa.p, exec, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->dl_soa.p, deadline, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
@@ -450,6 +452,68 @@ int slo_evaluate_batch(slo_ctx* c, int32_t count, const uint16_t* perms, const u
 }  // extern "C"
 
 namespace {
+template <int UPL>
+void launch_eval_tick(slo_ctx* c, const ChainParams& kp, int count, int words) {
+    constexpr size_t slot = eval_slot_bytes<UPL>();
+    const int warps = 8;
+    const int grid = std::min((count + warps - 1) / warps, c->sm_count * 8);
+    static_assert(8 * slot <= 227 * 1024, "evaluator slots exceed shared memory");
+    cudaFuncSetAttribute(k_eval_tick<UPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(warps * slot));
+    k_eval_tick<UPL><<<grid, warps * 32, warps * slot, c->stream>>>(
+        kp, count, words, c->e_perms.as<uint16_t>(), c->e_bits.as<uint32_t>(), c->e_n.as<int>(), c->e_t.as<double>(),
+        c->e_g.as<double>(), c->e_err.as<int>());
+}
+}  // namespace
+
+extern "C" {
+
+int slo_evaluate_batch_tick(slo_ctx* c, int32_t count, const uint16_t* perms, const uint32_t* bits, int32_t* n_met,
+                            double* t, double* g, uint64_t* exact_walks) {
+    if (!c) return fail(SLO_ERR_ARG, "slo_evaluate_batch_tick: null context");
+    if (c->n == 0) return fail(SLO_ERR_STATE, "slo_evaluate_batch_tick: no problem set");
+    if (!c->exec_nonneg) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: the tick grid needs finite, non-negative exec times");
+    if (count <= 0) return SLO_OK;
+    const int n = c->n, words = (n + 31) / 32;
+    CK(cudaSetDevice(c->device));
+    CK(c->e_perms.reserve((size_t)count * n * sizeof(uint16_t)));
+    CK(c->e_bits.reserve((size_t)count * words * sizeof(uint32_t)));
+    CK(c->e_n.reserve((size_t)count * sizeof(int)));
+    CK(c->e_t.reserve((size_t)count * sizeof(double)));
+    CK(c->e_g.reserve((size_t)count * sizeof(double)));
+    CK(c->e_err.reserve(sizeof(int)));
+    CK(c->e_cnt.reserve(sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(c->e_err.p, 0, sizeof(int), c->stream));
+    CK(cudaMemsetAsync(c->e_cnt.p, 0, sizeof(unsigned long long), c->stream));
+    CK(cudaMemcpyAsync(c->e_perms.p, perms, (size_t)count * n * sizeof(uint16_t), cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpyAsync(c->e_bits.p, bits, (size_t)count * words * sizeof(uint32_t), cudaMemcpyHostToDevice, c->stream));
+    ChainParams kp{};
+    kp.n = n, kp.mb = c->mb, kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.tick = c->tick;
+    kp.dg = c->dg >= 0 ? c->dg + c->marg : -1, kp.tab64 = c->tab.as<double2>();
+    kp.exact_count = c->e_cnt.as<unsigned long long>();
+    switch (pick_upl(n)) {
+        case 1: launch_eval_tick<1>(c, kp, count, words); break;
+        case 2: launch_eval_tick<2>(c, kp, count, words); break;
+        default: launch_eval_tick<4>(c, kp, count, words); break;
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(n_met, c->e_n.p, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(t, c->e_t.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(g, c->e_g.p, (size_t)count * sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    int err = 0;
+    unsigned long long cnt = 0;
+    CK(cudaMemcpyAsync(&err, c->e_err.p, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaMemcpyAsync(&cnt, c->e_cnt.p, sizeof cnt, cudaMemcpyDeviceToHost, c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (exact_walks) *exact_walks = cnt;
+    if (err & 1) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: last position must end a batch");
+    if (err & 2) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: batch larger than max_batch");
+    if (err & 4) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: dense index out of range");
+    return SLO_OK;
+}
+
+}  // extern "C"
+
+namespace {
 
 int count_levels(double t0, double t_thres, double tau) {
     int L = 0;
@@ -460,24 +524,34 @@ int count_levels(double t0, double t_thres, double tau) {
 // The max-dynamic-smem attribute is per function and device (process-wide). Raise it to the
 // device maximum once: concurrent contexts then never race on it, and no call blocks behind a
 // running instance of the kernel (setting it while the kernel runs serialises the callers).
+// (The device maximum less the kernel's static shared memory, s_xr.)
 template <void (*K)(ChainParams)>
-cudaError_t ensure_smem_attr(int device, int bytes) {
+cudaError_t ensure_smem_attr(int device, size_t dyn_max) {
     static std::mutex mu;
     static bool done[64] = {};
     std::lock_guard<std::mutex> g(mu);
     if (device >= 0 && device < 64 && done[device]) return cudaSuccess;
-    const cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    const cudaError_t e = cudaFuncSetAttribute(K, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
     if (e == cudaSuccess && device >= 0 && device < 64) done[device] = true;
     return e;
+}
+
+// dynamic shared memory a block of K may use: the opt-in maximum less K's static allocation
+template <void (*K)(ChainParams)>
+size_t dyn_smem_max(const slo_ctx* c) {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, K) != cudaSuccess) return c->smem_optin - 64;
+    return c->smem_optin - a.sharedSizeBytes;
 }
 
 // W warps per block (bounded by max_w and shared memory), cpw chains per warp
 template <void (*K)(ChainParams)>
 int configure_kernel(slo_ctx* c, size_t base, size_t warp_bytes, int max_w, int cpw) {
-    int W = (int)std::min<size_t>(max_w, (c->smem_optin - base) / warp_bytes);
+    const size_t dyn_max = dyn_smem_max<K>(c);
+    int W = (int)std::min<size_t>(max_w, (dyn_max - base) / warp_bytes);
     W = std::max(1, std::min(W, (c->chain_count + cpw - 1) / cpw));
     c->smem = base + (size_t)W * warp_bytes;
-    CK(ensure_smem_attr<K>(c->device, (int)c->smem_optin));
+    CK(ensure_smem_attr<K>(c->device, dyn_max));
     int occ = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, W * 32, c->smem));
     if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: chain kernel does not fit on an SM");
@@ -498,9 +572,9 @@ int configure_chains(slo_ctx* c) {
     // read it through L1 instead (measured: 1.27e9 vs 1.16e9 proposals/s there)
     const size_t full = (size_t)max_w * slot;
 #ifdef SLO_TABLE_SMEM_IF_FITS
-    c->smem_tab = tab_smem + slot <= c->smem_optin;
+    c->smem_tab = tab_smem + slot <= dyn_smem_max<k_chains<UPL, true>>(c);
 #else
-    c->smem_tab = tab_smem + full <= c->smem_optin;
+    c->smem_tab = tab_smem + full <= dyn_smem_max<k_chains<UPL, true>>(c);
 #endif
     return c->smem_tab ? configure_kernel<k_chains<UPL, true>>(c, tab_smem, slot, max_w, 1)
                        : configure_kernel<k_chains<UPL, false>>(c, 0, slot, max_w, 1);
@@ -670,7 +744,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
 
     ChainParams& kp = c->kp;
     kp.n = n, kp.mb = c->mb, kp.smem_tab = c->smem_tab ? 1 : 0;
-    kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.dg = c->dg, kp.tick = c->tick;
+    kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.tick = c->tick;
+    kp.dg = c->dg >= 0 ? c->dg + c->marg : -1, kp.tab64 = c->tab.as<double2>();
     kp.magic = n >= 2 ? (uint32_t)((1ull << 32) / (uint64_t)n + 1) : 0u;
     kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;
     kp.iter = prm->iter, kp.levels = c->levels;
@@ -684,6 +759,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     kp.start_lane = c->start_sum.p, kp.start_obj = c->start_obj.as<long long>();
     kp.best_ent = c->best_ent.as<uint16_t>(), kp.best_bits = c->best_bits.as<uint32_t>();
     kp.rec = c->rec.as<ChainRec>();
+    CK(c->exact_count.reserve(sizeof(unsigned long long)));
+    kp.exact_count = c->exact_count.as<unsigned long long>();
     c->prepared = true;
     return SLO_OK;
 }
@@ -693,6 +770,8 @@ int slo_chains_launch(slo_ctx* c) {
     CK(cudaSetDevice(c->device));
     const size_t cc = c->chain_count;
     CK(cudaMemsetAsync(c->rec.p, 0, cc * sizeof(ChainRec), c->stream));
+    if (c->prm.rng_mode != SLO_RNG_XOSHIRO_REPLAY)
+        CK(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
     CK(cudaEventRecord(c->ev0, c->stream));
     if (c->prm.rng_mode == SLO_RNG_XOSHIRO_REPLAY) {
         k_replay<<<c->grid, c->block, c->smem, c->stream>>>(c->rp);
@@ -718,7 +797,10 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_fetch: not prepared");
     CK(cudaSetDevice(c->device));
     ChainResult r;
+    unsigned long long exact = 0;
     CK(cudaMemcpyAsync(&r, c->result.p, sizeof r, cudaMemcpyDeviceToHost, c->stream));
+    if (c->prm.rng_mode != SLO_RNG_XOSHIRO_REPLAY)
+        CK(cudaMemcpyAsync(&exact, c->exact_count.p, sizeof exact, cudaMemcpyDeviceToHost, c->stream));
     const int n = c->n;
     std::vector<uint16_t> ent;
     std::vector<uint32_t> bits;
@@ -750,6 +832,7 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
         out->kernel_ms = ms;
         out->positions_pass1 = r.scan1;
         out->positions_pass2 = r.scan2;
+        out->exact_walks = exact;
     }
     return SLO_OK;
 }

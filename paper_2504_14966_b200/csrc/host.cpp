@@ -6,6 +6,7 @@
 // P: = /root/reference/proj/.
 #include <algorithm>
 #include <chrono>
+#include <climits>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -394,17 +395,62 @@ void AnnealConfig::validate() const {
         if (!(m >= 0.0)) throw DataError("AnnealConfig: scale_ladder entries must be >= 0");
 }
 
+namespace {
+// doubles <-> integers in the same order (-0.0 and +0.0 share key 0)
+inline long long dkey(double x) {
+    long long b;
+    std::memcpy(&b, &x, sizeof b);
+    return b >= 0 ? b : LLONG_MIN - b;
+}
+inline double dval(long long k) {
+    const long long b = k >= 0 ? k : LLONG_MIN - k;
+    double x;
+    std::memcpy(&x, &b, sizeof x);
+    return x;
+}
+}  // namespace
+
+// The largest d with fl(d + c) <= s. fl(d + c) is nondecreasing in d, so the d that pass form a
+// down-set: bracket its end from s - c by doubling steps in key space, then bisect (<= ~130 probes;
+// a walk one ulp at a time would need up to 2^52 steps when s - c is near 0 and c is not).
 double latest_start(double s, double c) {
-    double d = s - c;
-    if (std::isnan(d)) return -std::numeric_limits<double>::infinity();
-    if (std::isinf(d)) return d;
-    while (d + c > s) d = std::nextafter(d, -std::numeric_limits<double>::infinity());
-    for (;;) {
-        const double up = std::nextafter(d, std::numeric_limits<double>::infinity());
-        if (up + c <= s && up != d) d = up;
-        else break;
+    const double d0 = s - c;
+    if (std::isnan(d0)) return -std::numeric_limits<double>::infinity();
+    if (std::isinf(d0)) return d0;
+    const long long kmax = dkey(std::numeric_limits<double>::max()), kmin = dkey(-std::numeric_limits<double>::max());
+    auto ok = [&](long long k) { return dval(k) + c <= s; };
+    long long lo, hi;  // ok(lo), !ok(hi) (hi may be one past the finite range)
+    const long long k0 = dkey(d0);
+    if (ok(k0)) {
+        lo = k0;
+        long long step = 1;
+        for (;;) {
+            const long long t = lo + step > kmax ? kmax + 1 : lo + step;
+            if (t > kmax || !ok(t)) {
+                hi = t;
+                break;
+            }
+            lo = t, step *= 2;
+        }
+    } else {
+        hi = k0;
+        long long step = 1;
+        for (;;) {
+            const long long t = hi - step < kmin ? kmin : hi - step;
+            if (ok(t)) {
+                lo = t;
+                break;
+            }
+            if (t == kmin) return -std::numeric_limits<double>::infinity();
+            hi = t, step *= 2;
+        }
     }
-    return d;
+    while (hi - lo > 1) {
+        const long long m = lo + (hi - lo) / 2;
+        if (ok(m)) lo = m;
+        else hi = m;
+    }
+    return dval(lo);
 }
 
 namespace {

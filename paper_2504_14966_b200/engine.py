@@ -94,6 +94,20 @@ class Engine:
                                                _p(bits, c_uint32), _p(n_met), _p(t, c_double), _p(g, c_double)))
         return n_met, t, g
 
+    def evaluate_batch_tick(self, perms: np.ndarray, bits: np.ndarray):
+        """K3's own objective of `count` candidates: n_met bit-exact with CostModel::score, t and g on
+        the tick grid. Returns (n_met, t, g, exact_walks)."""
+        perms = np.ascontiguousarray(perms, dtype=np.uint16)
+        bits = np.ascontiguousarray(bits, dtype=np.uint32)
+        count = perms.shape[0]
+        n_met, t, g = np.zeros(count, dtype=np.int32), np.zeros(count), np.zeros(count)
+        ex = ctypes.c_uint64()
+        _check_engine(lib().slo_evaluate_batch_tick(self._ctx, count,
+                                                    perms.ctypes.data_as(ctypes.POINTER(ctypes.c_uint16)),
+                                                    _p(bits, c_uint32), _p(n_met), _p(t, c_double), _p(g, c_double),
+                                                    byref(ex)))
+        return n_met, t, g, int(ex.value)
+
     def _params(self, t0=500.0, t_thres=20.0, iter=100, tau=0.95, seed=0, objective_scale=1.0, replay=False,
                 chains=1, chain_begin=0, chain_end=None, budget_ms=0.0, scale_ladder=(), max_blocks=0):
         ladder = _f64(list(scale_ladder)) if len(scale_ladder) else None

@@ -8,8 +8,10 @@ Semantics modelled:
 * draws from Philox4x32-10 (Random123 constants): the row of proposal `prop` of chain `cid` is
   32 words, block b = philox(ctr = (prop, cid, b, 0x5105c4ed), key = (seed lo, seed hi)); attempt a
   uses words 3a, 3a+1, 3a+2; U[0, m) = (word * m) >> 32; the acceptance uniform is word 27;
-* objective on the tick grid: exec rounded half-even to multiples of `tick`, every sum an integer,
-  met iff elapsed_ticks <= floor(deadline / tick) (deadline +inf: always met); G = n_met / t;
+* objective: the total latency on the tick grid (exec rounded half-even to multiples of `tick`,
+  every sum an integer); n_met exactly the reference's -- the batch-start elapsed time summed in
+  fp64 makespan by makespan (P:src/priority_mapper.cpp:264-276) against the fp64 latest-start
+  table (deadline +inf: always met); G = n_met / t;
 * Metropolis: accept if G_new > G, else u < exp(-x) in float32 with x = (G - G_new) * (scale / t)
   and u = (word27 >> 8) * 2^-24; temperature t = t0, t *= tau while t >= t_thres;
 * the best state is the first one reaching a new maximum G.
@@ -58,24 +60,27 @@ class TickProblem:
         self.tick = tick
         self.xt = np.rint(ex / tick).astype(np.int64)
         self.dl = dl
+        self.ex = ex
 
-    def met(self, elapsed, b, i):
-        d = float(self.dl[b - 1, i])
-        if d == math.inf:
-            return True
-        return d >= 0.0 and elapsed <= math.floor(d / self.tick)
+    def met(self, elapsed_f, b, i):
+        """the reference's test: fp64 batch-start elapsed <= latest start"""
+        return elapsed_f <= float(self.dl[b - 1, i])
 
     def score(self, batches):
         elapsed = total = met = 0
+        elapsed_f = 0.0  # the reference's elapsed: fp64, left to right
         for bt in batches:
             b = len(bt)
-            mk = 0
+            mk, mk_f = 0, 0.0
             for i in bt:
                 x = int(self.xt[b - 1, i])
                 total += elapsed + x
-                met += self.met(elapsed, b, i)
+                met += self.met(elapsed_f, b, i)
                 mk = max(mk, x)
+                e = float(self.ex[b - 1, i])
+                mk_f = e if mk_f < e else mk_f
             elapsed += mk
+            elapsed_f = elapsed_f + mk_f
         t = float(total) * self.tick
         return met, t, (met * (1.0 / t) if t > 0 else 0.0)
 

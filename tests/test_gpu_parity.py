@@ -353,19 +353,24 @@ def test_chains_valid_and_dominant(n, mb, chains):
 
 
 def tick_objective(ex, dl, tick, perm, sizes):
-    """Full evaluation on the chain kernel's grid, in Python integers: exec rounded to ticks
-    (round-half-even), met iff elapsed_ticks <= floor(deadline / tick); +inf deadlines always met."""
+    """Full evaluation with the chain kernel's arithmetic: the total latency in Python integers on
+    the grid (exec rounded half-even to ticks); n_met the reference's (fp64 elapsed, summed left to
+    right, <= the fp64 latest start; +inf deadlines always met)."""
     xt = np.rint(ex / tick).astype(np.int64)
     elapsed = total = met = pos = 0
+    elapsed_f = 0.0
     for sz in sizes:
-        mk = 0
+        mk, mk_f = 0, 0.0
         for _ in range(sz):
             i = int(perm[pos]); pos += 1
             x = int(xt[sz - 1, i]); d = float(dl[sz - 1, i])
             total += elapsed + x
-            met += d == np.inf or (d >= 0.0 and elapsed <= int(np.floor(d / tick)))
+            met += elapsed_f <= d
             mk = max(mk, x)
+            e = float(ex[sz - 1, i])
+            mk_f = e if mk_f < e else mk_f
         elapsed += mk
+        elapsed_f = elapsed_f + mk_f
     t = float(total) * tick
     return met, t, (met * (1.0 / t) if t > 0 else 0.0)
 

@@ -69,7 +69,8 @@ def main():
         eng.launch()
         bp, bs, res = eng.fetch()
         print(f"rep {r}: {res.proposals} proposals in {res.kernel_ms:.3f} ms = "
-              f"{res.proposals / res.kernel_ms * 1e3:.3e}/s, g={res.g:.4e} n={res.n_met} levels={res.levels_run}")
+              f"{res.proposals / res.kernel_ms * 1e3:.3e}/s, g={res.g:.4e} n={res.n_met} levels={res.levels_run} "
+              f"exact_tests={getattr(res, 'exact_walks', -1)}")
 
 
 if __name__ == "__main__":
