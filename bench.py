@@ -131,6 +131,16 @@ def synthetic_workload(n):
     return S.generate_mixed(n, SEED)  # generate_mixed + estimator cold start, as the reference CLI
 
 
+def bench_config(args, world):
+    """The workload both arms run, identical in both JSON lines (arm-specific setup goes in "setup")."""
+    n, mb = args.n, args.mb
+    cfg_name = {1024: "configs[2]", 4096: "configs[3]"}.get(n, f"N={n}")
+    return {"workload": f"{cfg_name}: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
+                        f"predictions, max_batch {mb}, {args.budget_ms} ms scheduling budget per decision, "
+                        f"{world} GPU(s)",
+            "n_requests": n, "max_batch": mb, "budget_ms": args.budget_ms, "seed": SEED, "n_gpus": world}
+
+
 def flat_of(w):
     from oracle import FlatWorkload
     a = w.arrays
@@ -138,11 +148,11 @@ def flat_of(w):
                                            "kind", "e2e", "ttft", "tpot")})
 
 
-def cpu_reference_run(w, mb, threads, target_s, reps=None):
-    """The reference anneal() (default AnnealConfig) on `threads` host threads, one chain each."""
+def cpu_reference_run(fw, mb, threads, target_s, reps=None):
+    """The reference anneal() (default AnnealConfig) on `threads` host threads, one chain each.
+    fw: the workload as an oracle.FlatWorkload."""
     from oracle import TABLE_COEFFS, ref
-    fw = flat_of(w)
-    ids = list(w.ids())
+    ids = [int(x) for x in fw.id]
     if ref.available():
         kind = "reference"
         probe = ref.anneal_parallel(fw, TABLE_COEFFS, ids, mb, threads=1, reps=1)
@@ -181,7 +191,10 @@ def run_reference(args):
     world, rank, _ = dist_env()
     if rank != 0:
         return
-    w = synthetic_workload(args.n)
+    # the workload from the reference's own generator and Estimator (oracle/_ref): this arm never
+    # loads the product library
+    from oracle import port, ref
+    w = (ref if ref.available() else port).generate_mixed(args.n, SEED)
     threads = os.cpu_count() or 1
     # a step = every host thread running `reps` reference anneal() calls back to back, reps sized
     # so a step lasts ~0.1 s: thread start-up and the slowest thread's tail are amortised
@@ -203,9 +216,9 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": wall / args.steps, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"generate_mixed({args.n}, seed {SEED}) + estimator lengths, max_batch {args.mb}, "
-                               f"reference CPU anneal, one chain per host thread", "n_requests": args.n,
-                   "max_batch": args.mb, "threads": threads},
+        "config": bench_config(args, args.gpus),
+        "setup": {"arm": "reference CPU anneal() (oracle/_ref, unmodified sources), default AnnealConfig, "
+                         "one chain per host thread", "threads": threads, "calls_per_thread_per_step": reps},
         "attainment": best_n / args.n, "g_req_per_ms": best_g,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -409,24 +422,22 @@ def run_ours(args):
     cpu = None
     if not args.no_cpu_baseline and world == 1:
         threads = os.cpu_count() or 1
-        kind, reps, cp, cw, cn, cg = cpu_reference_run(w, mb, threads, args.cpu_sample_s / max(threads, 1))
+        kind, reps, cp, cw, cn, cg = cpu_reference_run(flat_of(w), mb, threads, args.cpu_sample_s / max(threads, 1))
         cpu = {"value": cp / (cw / 1e3), "unit": UNIT, "cores": threads, "kind": kind,
                "sample": f"{threads} threads x {reps} reference anneal() calls (default AnnealConfig, 6300 "
                          f"proposals each) on the same N={n} mb={mb} workload; {cw / 1e3:.1f} s wall; "
                          f"host {lscpu_model()}",
                "attainment": cn / n, "g_req_per_ms": cg}
-    cfg_name = {1024: "configs[2]", 4096: "configs[3] (one GPU's shard)"}.get(n, f"N={n}")
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dev_ms_max / args.steps, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "i64", "data": "synthetic",
-        "config": {"workload": f"{cfg_name}: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
-                               f"predictions, {args.chains} chains/GPU, {args.budget_ms} ms budget",
-                   "n_requests": n, "max_batch": mb, "chains_per_gpu": args.chains, "chains_total": chains_total,
-                   "budget_ms": args.budget_ms, "kernel_budget_ms": kernel_budget_ms, "host_ms_measured": host_ms,
-                   "ladder": {"t0": args.t0, "t_thres": args.t_thres, "tau": args.tau, "iter": args.iter},
-                   "scale_ladder": list(SCALE_LADDER), "l2": "flushed between steps (512 MiB write)",
-                   "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather argmax"},
+        "config": bench_config(args, world),
+        "setup": {"arm": "B200 chains (k_chains)", "chains_per_gpu": args.chains, "chains_total": chains_total,
+                  "kernel_budget_ms": kernel_budget_ms, "host_ms_measured": host_ms,
+                  "ladder": {"t0": args.t0, "t_thres": args.t_thres, "tau": args.tau, "iter": args.iter},
+                  "scale_ladder": list(SCALE_LADDER), "l2": "flushed between steps (512 MiB write)",
+                  "parallelism": f"chains sharded over {world} GPU(s), NCCL all-gather argmax"},
         "attainment": attain_n / n, "g_req_per_ms": attain_g,
         "attainment_start": max(ev_s, ev_i, ev_d, key=lambda e: e.g).n / n,
         "attainment_reference_starts": max(ev_s, ev_i, key=lambda e: e.g).n / n,
@@ -486,10 +497,10 @@ def ensure_built():
 
 def main():
     args = parse()
-    ensure_built()
     if args.impl == "reference":
-        run_reference(args)
+        run_reference(args)  # the reference's CPU code only: the product library is not loaded
     else:
+        ensure_built()
         run_ours(args)
 
 

@@ -270,3 +270,24 @@ def test_bench_reference_arm_line():
     assert line["higher_is_better"] is True and line["n_gpus"] == 1
     assert line["cpu_baseline"]["kind"] == "reference" and line["cpu_baseline"]["value"] == line["value"]
     assert line["e2e"] == {"value": line["value"], "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}
+    # the same config object as the GPU arm's line (bench_config), so the driver can pair the arms
+    import argparse
+    sys.path.insert(0, ROOT)
+    import bench
+    assert line["config"] == bench.bench_config(argparse.Namespace(n=256, mb=4, budget_ms=10.0), 1)
+
+
+def test_bench_reference_arm_never_loads_the_product():
+    """The reference arm runs the reference's own generator and anneal(): libslosched_b200.so stays
+    unmapped in that process."""
+    import subprocess
+    import sys
+    from oracle import ref
+    if not ref.available():
+        pytest.skip("oracle/_ref not built")
+    code = ("import sys; sys.argv = ['bench.py', '--impl', 'reference', '--steps', '1', '--warmup', '0', '--n', '64'];"
+            "import bench; bench.main(); maps = open('/proc/self/maps').read();"
+            "print('MAPPED', 'libslosched_b200' in maps, 'libslosched_ref' in maps)")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    assert out.stdout.strip().splitlines()[-1] == "MAPPED False True"
