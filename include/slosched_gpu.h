@@ -86,8 +86,8 @@ int slo_evaluate_batch(slo_ctx* ctx, int32_t count, const uint16_t* perms,
  * n_met bit-exact with CostModel::score -- the tick grid decides an SLO test only where its
  * rounding bound certifies it, the rest is re-summed in the reference's fp64 order -- and t (g)
  * on the grid, within 2^-26 relative of the reference's. exact_walks (may be NULL) receives
- * the number of 32-position units decided by the fp64 re-sum. Needs finite, non-negative exec
- * times. */
+ * the number of 32-position units decided by the fp64 re-sum. Needs finite exec times
+ * (negative ones are valid: the grid is offset, makespans start at 0 as in the reference). */
 int slo_evaluate_batch_tick(slo_ctx* ctx, int32_t count, const uint16_t* perms,
                             const uint32_t* batch_end_bits, int32_t* n_met, double* t, double* g,
                             uint64_t* exact_walks);

@@ -53,6 +53,17 @@ constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline
 constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
 constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
 
+// Negative exec times (fitted coefficients with negative intercepts are valid reference inputs,
+// P:src/core.cpp:55-62): the tick table then holds exec + cofs >= 0, and a makespan -- the
+// reference's max starting at 0.0 (P:src/priority_mapper.cpp:267-273) -- is max(m - cofs, 0) of
+// the offset maximum m. Exec sums over the same positions cancel the offset. NEG is a template
+// flag so the common non-negative case compiles exactly as before.
+template <bool NEG>
+__device__ __forceinline__ uint32_t mkspan(uint32_t m, int cofs) {
+    if constexpr (NEG) return (uint32_t)max((int)m - cofs, 0);
+    else return m;
+}
+
 template <int UPL>
 struct __align__(16) LaneState {  // this lane's unit anchors
     long long E[UPL];  // elapsed (ticks) at the start of the batch holding the unit's first position
@@ -71,6 +82,7 @@ struct ChainParams {
     const double2* tab64; // global [mb][n] {exec, latest start} fp64: the reference's SLO test
     unsigned long long* exact_count;  // SLO tests the grid could not certify (exact_met)
     double tick;         // 2^-k ms
+    int cofs;            // exec tick offset: xt holds exec + cofs >= 0 (cofs > 0 only with negative execs)
     int smem_tab;
     double t0, tau, scale;
     int iter, levels;
@@ -207,9 +219,9 @@ __device__ __noinline__ ExactStep exact_chunk(const uint16_t* ent, const uint32_
 
 // Cooperative count of the met finite-deadline SLOs of unit u, whose first batch started at
 // elapsed E with makespan F, on the tick grid; -1 when some test is not certified.
-template <bool SMEM>
+template <bool SMEM, bool NEG>
 __device__ __forceinline__ int unit_count(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
-                                          int n, int mb, int u, int lane, long long E, uint32_t F) {
+                                          int n, int mb, int cofs, int u, int lane, long long E, uint32_t F) {
     const int q = (u << 5) + lane;
     const uint32_t w = bits[u];
     uint32_t x = 0;
@@ -217,7 +229,7 @@ __device__ __forceinline__ int unit_count(const uint16_t* ent, const uint32_t* b
     if (q < n) {
         const uint32_t e = ent[q];
         const uint32_t v = xt_ld<SMEM>(tab, e);
-        x = v & kTickMask;
+        x = mkspan<NEG>(v & kTickMask, cofs);
         if (!(v & kAlways)) D = __ldg(dt + e);  // +inf deadlines are counted in A, not here
     }
     const uint32_t m = seg_max(x, w, lane, mb);
@@ -239,10 +251,10 @@ __device__ __forceinline__ int unit_count(const uint16_t* ent, const uint32_t* b
 }
 
 // -1: some test needs the reference arithmetic (walk_units then runs exact_chunk over the prefix)
-template <bool SMEM>
+template <bool SMEM, bool NEG>
 __device__ __noinline__ int unit_walk(const uint16_t* ent, const uint32_t* bits, TabRef tab, const long long* dt,
-                                      int n, int mb, int u, int lane, long long E, uint32_t F) {
-    return unit_count<SMEM>(ent, bits, tab, dt, n, mb, u, lane, E, F);
+                                      int n, int mb, int cofs, int u, int lane, long long E, uint32_t F) {
+    return unit_count<SMEM, NEG>(ent, bits, tab, dt, n, mb, cofs, u, lane, E, F);
 }
 
 struct Move {         // also the move record of K2 (replay.cuh)
@@ -398,15 +410,14 @@ __device__ __forceinline__ void rebuild_flags(const uint16_t* ent, const uint32_
     }
 }
 
-// Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts.
 // Re-walk the live units flagged in `need` (per unit k of this lane); W receives the counts. A unit
 // the tick grid cannot certify (unit_walk returns -1) is decided by exact_chunk over chunks 0..u,
 // one chunk per trip of the same loop (a separate loop, anywhere on this path, costs the chain
 // kernel registers on every walk).
-template <int UPL, bool SMEM>
+template <int UPL, bool SMEM, bool NEG>
 __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UPL>& ls, const uint16_t* ent,
                                            const uint32_t* bits, const TabRef& tab, const long long* dt,
-                                           int n, int mb, int lane, unsigned& sc2) {
+                                           int n, int mb, int cofs, int lane, unsigned& sc2) {
 #pragma unroll
     for (int k = 0; k < UPL; ++k) {
         unsigned mask = __ballot_sync(FULL, need[k]);
@@ -419,7 +430,7 @@ __device__ __forceinline__ void walk_units(const bool (&need)[UPL], LaneState<UP
             if (c < 0) {
                 const long long Eu = __shfl_sync(FULL, ls.E[k], ln);
                 const uint32_t Fu = __shfl_sync(FULL, ls.F[k], ln);
-                cnt = unit_walk<SMEM>(ent, bits, tab, dt, n, mb, u, lane, Eu, Fu);
+                cnt = unit_walk<SMEM, NEG>(ent, bits, tab, dt, n, mb, cofs, u, lane, Eu, Fu);
 #ifndef SLO_DIAG
                 sc2 += 32;  // only lane 0's count is stored
 #endif
@@ -451,7 +462,7 @@ __device__ __forceinline__ int live_met(const LaneState<UPL>& ls, long long dg) 
 // One warp evaluates a schedule from scratch with the chain kernel's arithmetic (tick totals, the
 // certified SLO walk): each lane owns its UPL units, sums their batches sequentially, one warp scan
 // gives the anchors. Es/Fs: kU-entry scratch. Returns the lane's anchors; tot, A, nm warp-uniform.
-template <int UPL>
+template <int UPL, bool NEG>
 __device__ void eval_schedule(const ChainParams& p, const uint16_t* ent, const uint32_t* bits, long long* Es,
                               uint32_t* Fs, int lane, LaneState<UPL>& ls, long long& tot_out, int& A_out,
                               int& nm_out) {
@@ -466,7 +477,7 @@ __device__ void eval_schedule(const ChainParams& p, const uint16_t* ent, const u
     long long inner = 0;      // makespans of the batches that start after the first end
     bool seen = false;
     for (int q = q0; q < q1; ++q) {
-        const uint32_t x = __ldg(p.xt + ent[q]) & kTickMask;
+        const uint32_t x = mkspan<NEG>(__ldg(p.xt + ent[q]) & kTickMask, p.cofs);
         if (!seen) hm = max(hm, x);
         else tm = max(tm, x);
         if ((bits[q >> 5] >> (q & 31)) & 1u) {
@@ -490,9 +501,9 @@ __device__ void eval_schedule(const ChainParams& p, const uint16_t* ent, const u
     for (int q = q0; q < q1; ++q) {
         if ((q & 31) == 0) Es[q >> 5] = E, pend = q >> 5;
         const uint32_t v = __ldg(p.xt + ent[q]);
-        const uint32_t x = v & kTickMask;
+        const uint32_t x = mkspan<NEG>(v & kTickMask, p.cofs);
         A += v >> 31;
-        tot += E + x;
+        tot += E + ((long long)(v & kTickMask) - p.cofs);  // the exec itself may be negative
         mk = max(mk, x);
         if ((bits[q >> 5] >> (q & 31)) & 1u) {
             if (pend >= 0) Fs[pend] = mk, pend = -1;
@@ -511,14 +522,14 @@ __device__ void eval_schedule(const ChainParams& p, const uint16_t* ent, const u
     }
     unsigned sc2 = 0;
     const TabRef tab{p.xt, 0u};
-    walk_units<UPL, false>(need, ls, ent, bits, tab, p.dt, n, p.mb, lane, sc2);
+    walk_units<UPL, false, NEG>(need, ls, ent, bits, tab, p.dt, n, p.mb, p.cofs, lane, sc2);
     tot_out = tot, A_out = A, nm_out = A + live_met<UPL>(ls, p.dg);
     __syncwarp();
 }
 
 // Prologue: one warp evaluates the start schedule shared by every chain and publishes its unit
 // anchors, so the chains start without a full evaluation each.
-template <int UPL>
+template <int UPL, bool NEG>
 __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr int kU = 32 * UPL;
@@ -534,7 +545,7 @@ __global__ void __launch_bounds__(32) k_start(const ChainParams p) {
     LaneState<UPL> ls;
     long long tot;
     int A, nm;
-    eval_schedule<UPL>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
+    eval_schedule<UPL, NEG>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
     reinterpret_cast<LaneState<UPL>*>(p.start_lane)[lane] = ls;
     if (lane == 0) p.start_obj[0] = tot, p.start_obj[1] = A, p.start_obj[2] = nm;
 }
@@ -549,7 +560,7 @@ __host__ __device__ constexpr int eval_slot_bytes() {
 // the total on the tick grid. perms: [count][n] dense indices; bits: [count][words] batch ends.
 // Invalid candidates set error bits 1 (last position not a batch end), 2 (batch > mb), 4 (index
 // out of range) and are not scored.
-template <int UPL>
+template <int UPL, bool NEG>
 __global__ void __launch_bounds__(256) k_eval_tick(const ChainParams p, int count, int words,
                                                    const uint16_t* __restrict__ perms,
                                                    const uint32_t* __restrict__ cbits, int* __restrict__ n_met,
@@ -607,7 +618,7 @@ __global__ void __launch_bounds__(256) k_eval_tick(const ChainParams p, int coun
         LaneState<UPL> ls;
         long long tot;
         int A, nm;
-        eval_schedule<UPL>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
+        eval_schedule<UPL, NEG>(p, ent, bits, Es, Fs, lane, ls, tot, A, nm);
         if (lane == 0) {
             const double t = (double)tot * p.tick;
             n_met[c] = nm, t_out[c] = t, g_out[c] = objective(nm, t);
@@ -615,7 +626,7 @@ __global__ void __launch_bounds__(256) k_eval_tick(const ChainParams p, int coun
     }
 }
 
-template <int UPL, bool SMEM>
+template <int UPL, bool SMEM, bool NEG>
 __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainParams p) {
     extern __shared__ __align__(16) unsigned char smem[];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, W = blockDim.x >> 5;
@@ -733,7 +744,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         if (q < n) {
                             const uint32_t e = ent[q];
                             const uint32_t v = xt_ld<SMEM>(tab, e);
-                            x = v & kTickMask;
+                            x = mkspan<NEG>(v & kTickMask, p.cofs);
                             if (!(v & kAlways)) D = __ldg(p.dt + e), fin = D >= 0;
                         }
                         const uint32_t m = seg_max(x, w, lane, mb);
@@ -844,8 +855,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             // per-batch maxima over 4-lane halves, the exec delta over the 8 lanes
                             uint32_t mo = max(xo, __shfl_xor_sync(FULL, xo, 1));
                             uint32_t mn = max(xn, __shfl_xor_sync(FULL, xn, 1));
-                            mo = max(mo, __shfl_xor_sync(FULL, mo, 2));
-                            mn = max(mn, __shfl_xor_sync(FULL, mn, 2));
+                            mo = mkspan<NEG>(max(mo, __shfl_xor_sync(FULL, mo, 2)), p.cofs);
+                            mn = mkspan<NEG>(max(mn, __shfl_xor_sync(FULL, mn, 2)), p.cofs);
                             const uint32_t mo_x = __shfl_xor_sync(FULL, mo, 4), mn_x = __shfl_xor_sync(FULL, mn, 4);
                             int dx = (int)xn - (int)xo;
                             dx += __shfl_xor_sync(FULL, dx, 1);
@@ -987,10 +998,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     const uint32_t vo = act ? xt_ld<SMEM>(tab, old_q) : 0u;
                     const uint32_t vn = act ? xt_ld<SMEM>(tab, nw) : 0u;
                     const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
-                    const uint32_t mO0 = __reduce_max_sync(FULL, q <= osp ? xo : 0u);
-                    const uint32_t mO1 = __reduce_max_sync(FULL, q > osp ? xo : 0u);
-                    const uint32_t mN0 = __reduce_max_sync(FULL, q <= nsp ? xn : 0u);
-                    const uint32_t mN1 = __reduce_max_sync(FULL, q > nsp ? xn : 0u);
+                    const uint32_t mO0 = mkspan<NEG>(__reduce_max_sync(FULL, q <= osp ? xo : 0u), p.cofs);
+                    const uint32_t mO1 = mkspan<NEG>(__reduce_max_sync(FULL, q > osp ? xo : 0u), p.cofs);
+                    const uint32_t mN0 = mkspan<NEG>(__reduce_max_sync(FULL, q <= nsp ? xn : 0u), p.cofs);
+                    const uint32_t mN1 = mkspan<NEG>(__reduce_max_sync(FULL, q > nsp ? xn : 0u), p.cofs);
                     const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
                     dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
                     // makespan * positions-after products: 27 x 12 bits, one widening multiply each
@@ -1060,10 +1071,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
                         const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
                         const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
-                        const uint32_t mO0 = __reduce_max_sync(FULL, first ? xo : 0u);
-                        const uint32_t mO1 = __reduce_max_sync(FULL, first ? 0u : xo);
-                        mN0 = __reduce_max_sync(FULL, first ? xn : 0u);
-                        mN1 = __reduce_max_sync(FULL, first ? 0u : xn);
+                        const uint32_t mO0 = mkspan<NEG>(__reduce_max_sync(FULL, first ? xo : 0u), p.cofs);
+                        const uint32_t mO1 = mkspan<NEG>(__reduce_max_sync(FULL, first ? 0u : xo), p.cofs);
+                        mN0 = mkspan<NEG>(__reduce_max_sync(FULL, first ? xn : 0u), p.cofs);
+                        mN1 = mkspan<NEG>(__reduce_max_sync(FULL, first ? 0u : xn), p.cofs);
                         const long long sN = __reduce_add_sync(FULL, xn), sO = __reduce_add_sync(FULL, xo);
                         dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u)) - __popc(__ballot_sync(FULL, (vo & kAlways) != 0u));
                         da = (int)mN0 - (int)mO0, db = (int)mN1 - (int)mO1;
@@ -1103,7 +1114,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
 #pragma unroll
                     for (int kk = 0; kk < UPL; ++kk) need[kk] = false;
                 }
-                walk_units<UPL, SMEM>(need, nx, ent, bits, tab, p.dt, n, mb, lane, sc2);
+                walk_units<UPL, SMEM, NEG>(need, nx, ent, bits, tab, p.dt, n, mb, p.cofs, lane, sc2);
                 const long long tot_new = tot + dtot;
                 const int A_new = A + dA;
                 const int nm = A_new + live_met<UPL>(nx, dg);

@@ -235,14 +235,14 @@ __global__ void __launch_bounds__(1024) k_smem_probe(int iters, uint4* sink) {
 // interleave the SoA tables into {exec, deadline} pairs (K1, K2, exhaustive) and build the
 // tick tables of K3: exec rounded to the 2^-k ms grid (| kAlways where the deadline is +inf) and
 // deadline ticks floor(D * 2^k) (-1 where no elapsed time >= 0 meets it)
-__global__ void k_tables(int total, const double* exec, const double* dl, double scale, double2* tab, uint32_t* xt,
-                         long long* dt) {
+__global__ void k_tables(int total, const double* exec, const double* dl, double scale, int cofs, double2* tab,
+                         uint32_t* xt, long long* dt) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= total) return;
     const double e = exec[i], d = dl[i];
     tab[i] = make_double2(e, d);
     const bool always = d == INFINITY;
-    xt[i] = (uint32_t)__double2ull_rn(e * scale) | (always ? kAlways : 0u);
+    xt[i] = (uint32_t)(__double2ll_rn(e * scale) + cofs) | (always ? kAlways : 0u);
     dt[i] = always || !(d >= 0.0) ? -1ll : (long long)fmin(floor(d * scale), 0x1.0p62);
 }
 
@@ -299,7 +299,8 @@ struct slo_ctx {
     double tick = 1.0;   // K3 grid: 2^-k ms
     long long dg = -1;   // K3: largest finite deadline in ticks
     long long marg = 0;  // K3: ticks within which the grid cannot certify an SLO test
-    bool exec_nonneg = true;
+    bool exec_finite = true;
+    int cofs = 0;        // K3: exec tick offset (> 0 only when some exec is negative)
     // chains
     DevBuf st_ent, st_bits, st_sum, best_ent, best_bits, rec, start_ent, start_bits, start_sum, start_obj, scale_mult,
         result, win_ent, win_bits, exact_count;
@@ -382,28 +383,31 @@ int slo_problem_set(slo_ctx* c, int32_t n, int32_t mb, const double* exec, const
     CK(c->dl_soa.reserve(total * sizeof(double)));
     CK(c->xt.reserve(total * sizeof(uint32_t)));
     CK(c->dt.reserve(total * sizeof(long long)));
-    // K3 tick grid: the largest power of two 2^k with max exec * 2^k <= kTickMask
-    double emax = 0.0, dmax_fin = -1.0;
-    bool nonneg = true;
+    // K3 tick grid: the largest power of two 2^k with (max exec - min(min exec, 0)) * 2^k below
+    // kTickMask (negative execs are stored offset by cofs ticks, chains.cuh mkspan)
+    double emax = 0.0, emin = 0.0, dmax_fin = -1.0;
+    bool finite = true;
     for (size_t i = 0; i < total; ++i) {
-        if (!(exec[i] >= 0.0) || !std::isfinite(exec[i])) nonneg = false;
-        else emax = std::max(emax, exec[i]);
+        if (!std::isfinite(exec[i])) finite = false;
+        else emax = std::max(emax, exec[i]), emin = std::min(emin, exec[i]);
         if (std::isfinite(deadline[i]) && deadline[i] >= 0.0) dmax_fin = std::max(dmax_fin, deadline[i]);
     }
+    const double range = emax - emin;
     int k = 40;
-    if (emax > 0.0) {
+    if (range > 0.0) {
         k = 0;
-        while (k < 60 && std::ldexp(emax, k + 1) <= (double)kTickMask) ++k;
-        while (k > -60 && std::ldexp(emax, k) > (double)kTickMask) --k;
+        while (k < 60 && std::ldexp(range, k + 1) <= (double)kTickMask - 1.0) ++k;
+        while (k > -60 && std::ldexp(range, k) > (double)kTickMask - 1.0) --k;
     }
     c->tick = std::ldexp(1.0, -k);
+    c->cofs = emin < 0.0 ? (int)-std::nearbyint(std::ldexp(emin, k)) : 0;
     c->dg = dmax_fin >= 0.0 ? (long long)std::fmin(std::floor(std::ldexp(dmax_fin, k)), 0x1.0p61) : -1;
     c->marg = n / 2 + 2;  // chains.cuh cert_margin(n): no batch start drifts further from the reference
-    c->exec_nonneg = nonneg;
+    c->exec_finite = finite;
     CK(cudaMemcpyAsync(c->exec_soa.p, exec, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     CK(cudaMemcpyAsync(c->dl_soa.p, deadline, total * sizeof(double), cudaMemcpyHostToDevice, c->stream));
     k_tables<<<(unsigned)((total + 255) / 256), 256, 0, c->stream>>>((int)total, c->exec_soa.as<double>(),
-                                                                       c->dl_soa.as<double>(), std::ldexp(1.0, k),
+                                                                       c->dl_soa.as<double>(), std::ldexp(1.0, k), c->cofs,
                                                                        c->tab.as<double2>(), c->xt.as<uint32_t>(),
                                                                        c->dt.as<long long>());
     CK(cudaGetLastError());
@@ -452,14 +456,14 @@ int slo_evaluate_batch(slo_ctx* c, int32_t count, const uint16_t* perms, const u
 }  // extern "C"
 
 namespace {
-template <int UPL>
+template <int UPL, bool NEG>
 void launch_eval_tick(slo_ctx* c, const ChainParams& kp, int count, int words) {
     constexpr size_t slot = eval_slot_bytes<UPL>();
     const int warps = 8;
     const int grid = std::min((count + warps - 1) / warps, c->sm_count * 8);
     static_assert(8 * slot <= 227 * 1024, "evaluator slots exceed shared memory");
-    cudaFuncSetAttribute(k_eval_tick<UPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(warps * slot));
-    k_eval_tick<UPL><<<grid, warps * 32, warps * slot, c->stream>>>(
+    cudaFuncSetAttribute(k_eval_tick<UPL, NEG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(warps * slot));
+    k_eval_tick<UPL, NEG><<<grid, warps * 32, warps * slot, c->stream>>>(
         kp, count, words, c->e_perms.as<uint16_t>(), c->e_bits.as<uint32_t>(), c->e_n.as<int>(), c->e_t.as<double>(),
         c->e_g.as<double>(), c->e_err.as<int>());
 }
@@ -471,7 +475,7 @@ int slo_evaluate_batch_tick(slo_ctx* c, int32_t count, const uint16_t* perms, co
                             double* t, double* g, uint64_t* exact_walks) {
     if (!c) return fail(SLO_ERR_ARG, "slo_evaluate_batch_tick: null context");
     if (c->n == 0) return fail(SLO_ERR_STATE, "slo_evaluate_batch_tick: no problem set");
-    if (!c->exec_nonneg) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: the tick grid needs finite, non-negative exec times");
+    if (!c->exec_finite) return fail(SLO_ERR_DATA, "slo_evaluate_batch_tick: the tick grid needs finite exec times");
     if (count <= 0) return SLO_OK;
     const int n = c->n, words = (n + 31) / 32;
     CK(cudaSetDevice(c->device));
@@ -490,10 +494,12 @@ int slo_evaluate_batch_tick(slo_ctx* c, int32_t count, const uint16_t* perms, co
     kp.n = n, kp.mb = c->mb, kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.tick = c->tick;
     kp.dg = c->dg >= 0 ? c->dg + c->marg : -1, kp.tab64 = c->tab.as<double2>();
     kp.exact_count = c->e_cnt.as<unsigned long long>();
+    kp.cofs = c->cofs;
+    const bool neg = c->cofs > 0;
     switch (pick_upl(n)) {
-        case 1: launch_eval_tick<1>(c, kp, count, words); break;
-        case 2: launch_eval_tick<2>(c, kp, count, words); break;
-        default: launch_eval_tick<4>(c, kp, count, words); break;
+        case 1: neg ? launch_eval_tick<1, true>(c, kp, count, words) : launch_eval_tick<1, false>(c, kp, count, words); break;
+        case 2: neg ? launch_eval_tick<2, true>(c, kp, count, words) : launch_eval_tick<2, false>(c, kp, count, words); break;
+        default: neg ? launch_eval_tick<4, true>(c, kp, count, words) : launch_eval_tick<4, false>(c, kp, count, words); break;
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(n_met, c->e_n.p, (size_t)count * sizeof(int), cudaMemcpyDeviceToHost, c->stream));
@@ -571,21 +577,30 @@ int configure_chains(slo_ctx* c) {
     // count beside it: where it would cost resident warps (N = 4096, mb = 4: 14 of 16) the chains
     // read it through L1 instead (measured: 1.27e9 vs 1.16e9 proposals/s there)
     const size_t full = (size_t)max_w * slot;
+    if (c->cofs > 0) {  // negative execs (rare inputs): one variant, table through L1
+        c->smem_tab = false;
+        return configure_kernel<k_chains<UPL, false, true>>(c, 0, slot, max_w, 1);
+    }
 #ifdef SLO_TABLE_SMEM_IF_FITS
-    c->smem_tab = tab_smem + slot <= dyn_smem_max<k_chains<UPL, true>>(c);
+    c->smem_tab = tab_smem + slot <= dyn_smem_max<k_chains<UPL, true, false>>(c);
 #else
-    c->smem_tab = tab_smem + full <= dyn_smem_max<k_chains<UPL, true>>(c);
+    c->smem_tab = tab_smem + full <= dyn_smem_max<k_chains<UPL, true, false>>(c);
 #endif
-    return c->smem_tab ? configure_kernel<k_chains<UPL, true>>(c, tab_smem, slot, max_w, 1)
-                       : configure_kernel<k_chains<UPL, false>>(c, 0, slot, max_w, 1);
+    return c->smem_tab ? configure_kernel<k_chains<UPL, true, false>>(c, tab_smem, slot, max_w, 1)
+                       : configure_kernel<k_chains<UPL, false, false>>(c, 0, slot, max_w, 1);
 }
 
 template <int UPL>
 void launch_t(slo_ctx* c) {
     const size_t ss = 32 * (size_t)UPL * 12 + 1024 * (size_t)UPL * 2 + 16 + 32 * (size_t)UPL * 4 + 16;
-    k_start<UPL><<<1, 32, ss, c->stream>>>(c->kp);
-    if (c->smem_tab) k_chains<UPL, true><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
-    else k_chains<UPL, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+    if (c->cofs > 0) {
+        k_start<UPL, true><<<1, 32, ss, c->stream>>>(c->kp);
+        k_chains<UPL, false, true><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+        return;
+    }
+    k_start<UPL, false><<<1, 32, ss, c->stream>>>(c->kp);
+    if (c->smem_tab) k_chains<UPL, true, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+    else k_chains<UPL, false, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
 }
 
 // prologue (start-state summaries, one warp) then the chain kernel
@@ -698,7 +713,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
         return SLO_OK;
     }
     if (prm->rng_mode != SLO_RNG_PHILOX) return fail(SLO_ERR_ARG, "slo_chains_prepare: unknown rng_mode");
-    if (!c->exec_nonneg) return fail(SLO_ERR_DATA, "slo_chains_prepare: the chain kernel needs finite, non-negative exec times");
+    if (!c->exec_finite) return fail(SLO_ERR_DATA, "slo_chains_prepare: the chain kernel needs finite exec times");
 
     const int UPL = pick_upl(n);
     c->UPL = UPL;
@@ -744,7 +759,7 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
 
     ChainParams& kp = c->kp;
     kp.n = n, kp.mb = c->mb, kp.smem_tab = c->smem_tab ? 1 : 0;
-    kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.tick = c->tick;
+    kp.xt = c->xt.as<uint32_t>(), kp.dt = c->dt.as<long long>(), kp.tick = c->tick, kp.cofs = c->cofs;
     kp.dg = c->dg >= 0 ? c->dg + c->marg : -1, kp.tab64 = c->tab.as<double2>();
     kp.magic = n >= 2 ? (uint32_t)((1ull << 32) / (uint64_t)n + 1) : 0u;
     kp.t0 = prm->t0, kp.tau = prm->tau, kp.scale = prm->objective_scale;

@@ -181,7 +181,8 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
                 const double o = __shfl_up_sync(FULL, m, d);
                 if (lane - d >= seg) m = dmax(m, o);
             }
-            if (q < n) xa[q] = make_double2(x, end ? m : 0.0);
+            // the reference's makespan starts at 0.0 (:267-273): a batch of negative execs adds 0
+            if (q < n) xa[q] = make_double2(x, end ? dmax(0.0, m) : 0.0);
             if (lane == 31) trail[w] = end ? 0.0 : m;
         }
         __syncwarp();

@@ -647,17 +647,97 @@ def test_chain_trajectory_matches_model_at_other_time_scales(eng, scale):
     assert (r.n_met, r.t, r.g) == model["best"] and r.accepted == model["accepted"]
 
 
-def test_chains_reject_negative_exec_times(eng):
-    """The chain kernel's integer grid needs finite, non-negative exec times: anything else is a
-    DataError from the engine, never a silent result."""
-    n, mb = 16, 2
-    ex = np.full((mb, n), 10.0)
-    dl = np.full((mb, n), 100.0)
-    ex[1, 3] = -1.0
+@pytest.mark.parametrize("n,mb,delta_p", [(64, 4, -400.0), (300, 8, -120.0), (1024, 4, -60.0)])
+def test_chains_with_negative_exec_times(eng, port, n, mb, delta_p):
+    """Fitted coefficients with a negative intercept (delta_p < 0) are valid reference inputs
+    (P:src/core.cpp:55-62) and give negative exec times for short requests. The chain kernel offsets
+    its tick grid (makespans start at 0 as in the reference, :267-273) and still follows the model
+    move for move, with the reference's n_met; the replay mode (K2) stays bit-identical to the
+    reference walk; the public anneal() returns a valid schedule no worse than its starts."""
+    import k3_model as K
+    base = S.table_coefficients()
+    c = S.LatencyCoefficients(base.alpha_p, base.beta_p, base.gamma_p, delta_p, base.alpha_d, base.beta_d,
+                              base.gamma_d, base.delta_d)
+    w = _three_class(n, 90 + n)
+    ids = sorted(w.ids())
+    ex, dl = E.build_tables(w, ids, c, mb)
+    assert (ex < 0).any(), "the coefficients must produce negative exec times"
     eng.set_problem(ex, dl)
-    with pytest.raises(Exception) as e:
-        eng.anneal_chains(list(range(n)), [2] * (n // 2), chains=4, t0=50.0, iter=5)
-    assert "non-negative" in str(e.value)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    perm, sizes = _start_schedule(n, mb, "mixed", 5)
+    start, q = [], 0
+    for s_ in sizes:
+        start.append(perm[q:q + s_])
+        q += s_
+    f0 = prob.score(start)[2]
+    seed, t0, tau, it = 31 + n, 100.0, 0.7, 30
+    scale = t0 / f0 if f0 > 0 else t0
+    bp, bs, r = eng.anneal_chains(perm, sizes, chains=2, t0=t0, t_thres=20.0, tau=tau, iter=it, seed=seed,
+                                  objective_scale=scale)
+    runs = [K.run_chain(prob, start, cid, seed, t0, 20.0, tau, it, scale) for cid in range(2)]
+    win = min(range(2), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    got, q = [], 0
+    for s_ in bs:
+        got.append([int(x) for x in bp[q:q + s_]])
+        q += s_
+    assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                   sum(x["accepted"] for x in runs))
+    assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
+    # the K3 evaluator agrees with the reference score on random schedules
+    rs = np.random.default_rng(n)
+    perms, szs = _random_partitions(rs, n, mb, 500)
+    coeffs = np.asarray(c.as_array(), dtype=np.float64)
+    nm, t, g, _ = eng.evaluate_batch_tick(perms, E.end_bits(szs, n))
+    o_n, o_t, o_g = port.score_batch(_flat(w), coeffs, ids, mb, perms.astype(np.int32), szs)
+    np.testing.assert_array_equal(nm, o_n)
+    np.testing.assert_allclose(t, o_t, rtol=1e-6, atol=1e-6 * np.abs(o_t).max())
+    # replay: the reference walk, bit for bit
+    r2 = S.anneal(w, w.ids(), c, S.AnnealConfig(seed=3, t0=60.0, iter=15, mode=S.SearchMode.REPLAY), mb)
+    o = port.anneal(_flat(w), coeffs, w.ids(), mb, seed=3, t0=60.0, iter=15)
+    assert r2.best.schedule.batches == o["batches"] and r2.best.g == o["g"] and r2.best.n == o["n"]
+    # chains through the public entry point
+    r3 = S.anneal(w, w.ids(), c, S.AnnealConfig(seed=1, chains=512, t0=100.0, iter=20), mb)
+    assert r3.best.schedule.is_partition_of(w.ids(), mb)
+    assert r3.best.g >= max(r3.stats.g_sorted_start, r3.stats.g_input_start)
+
+
+@pytest.mark.parametrize("n,mb", [(40, 4), (200, 8), (700, 2)])
+def test_chains_negative_exec_raw_tables(eng, n, mb):
+    """Raw tables where a third of the exec times are negative (whole batches of them: the
+    makespan floors at 0): the chains still follow the model move for move, and the K3 evaluator's
+    n_met equals K1's exact count."""
+    import k3_model as K
+    rs = np.random.default_rng(n)
+    ex = rs.uniform(-60.0, 120.0, size=(mb, n))
+    elapsed_scale = 120.0 * n / mb
+    dl = rs.uniform(-10.0, 0.6 * elapsed_scale, size=(mb, n))
+    dl[rs.random((mb, n)) < 0.1] = np.inf
+    eng.set_problem(ex, dl)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    perm, sizes = _start_schedule(n, mb, "mixed", 9)
+    start, q = [], 0
+    for s_ in sizes:
+        start.append(perm[q:q + s_])
+        q += s_
+    f0 = prob.score(start)[2]
+    seed, t0, tau, it = 77 + n, 100.0, 0.7, 30
+    scale = t0 / f0 if f0 > 0 else t0
+    bp, bs, r = eng.anneal_chains(perm, sizes, chains=2, t0=t0, t_thres=20.0, tau=tau, iter=it, seed=seed,
+                                  objective_scale=scale)
+    runs = [K.run_chain(prob, start, cid, seed, t0, 20.0, tau, it, scale) for cid in range(2)]
+    win = min(range(2), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    got, q = [], 0
+    for s_ in bs:
+        got.append([int(x) for x in bp[q:q + s_]])
+        q += s_
+    assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                   sum(x["accepted"] for x in runs))
+    assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
+    perms, szs = _random_partitions(rs, n, mb, 300)
+    bits = E.end_bits(szs, n)
+    nm, _, _, _ = eng.evaluate_batch_tick(perms, bits)
+    k1, _, _ = eng.evaluate_batch(perms, bits)
+    np.testing.assert_array_equal(nm, k1)
 
 
 def test_chain_trajectory_random_shapes(eng):
