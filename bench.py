@@ -62,6 +62,7 @@ def parse():
 
 # per-chain objective_scale multipliers: the reference default (x1) walks randomly at N=1024
 # (SURVEY 6.3); larger factors make greedier chains. Chain c uses ladder[c % len].
+PROFILE_TAGS = ("r2", "r1")  # newest ncu summaries first (profiles/<tag>/k_chains_summary*.json)
 SCALE_LADDER = (1e4, 1e5, 1e6, 1e7, 1e8)  # best of tools/quality_sweep.py (profiles/r1/quality_sweep.jsonl)
 
 
@@ -412,8 +413,8 @@ def run_ours(args):
             "frac": (achieved_ginst / peak_ginst) if achieved_ginst else None,
             "traffic": (prof["dram_bytes_per_proposal"] * props / args.steps) if prof else None,
             "kernel": "k_chains", "kernel_share_of_step": kern_ms / dev_ms if dev_ms else None,
-            "instr_per_proposal": ipp, "instr_source": (f"profiles/r1/{prof_file} (ncu --set full, tools/prof_chains.py --bench --n {n})"
-                             if prof else f"none: no ncu capture of N={n} mb={mb} under profiles/r1"),
+            "instr_per_proposal": ipp, "instr_source": (f"profiles/{prof_file} (ncu --set full, tools/prof_chains.py --bench --n {n})"
+                             if prof else f"none: no ncu capture of N={n} mb={mb} under profiles/"),
             "peak_source": f"4 warp-inst/clk/SM x {n_sms} SMs x {sm_mhz:.0f} MHz (sampled under load)",
             "smem_view": {"achieved_gbs": smem_bytes / (kern_ms / 1e3) / 1e9, "peak_gbs": smem_peak_gbs,
                           "peak_source": "slo_probe_smem_bandwidth (conflict-free LDS.128, all SMs, measured here)",
@@ -459,10 +460,15 @@ def load_profile_summary(n, mb):
     """The ncu summary of k_chains captured at this (n, mb) (instructions per proposal depend on
     the units per lane and the live units), or None: a capture of another shape is not used."""
     name = "k_chains_summary.json" if (n, mb) == (1024, 4) else f"k_chains_summary_n{n}_mb{mb}.json"
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1", name)) as f:
-            prof = json.load(f)
-    except OSError:
+    for tag in PROFILE_TAGS:
+        try:
+            with open(os.path.join(ROOT, "profiles", tag, name)) as f:
+                prof = json.load(f)
+            name = f"{tag}/{name}"
+            break
+        except OSError:
+            continue
+    else:
         return None, name
     return (prof, name) if (prof.get("n", 1024), prof.get("mb", 4)) == (n, mb) else (None, name)
 

@@ -12,16 +12,16 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 300 python tools/prof_chains.py --bench --reps 3 > gpurun_out/prof_chains.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 \
     -o gpurun_out/k_chains python tools/prof_chains.py --bench > gpurun_out/ncu_full.log 2>&1
-# the bench's roofline reads profiles/r1/k_chains_summary.json: refresh it from this capture
+# the bench's roofline reads profiles/${TAG:-r2}/k_chains_summary.json: refresh it from this capture
 # (prof_chains.py --bench evaluates 16384 chains x 8 levels x 300 proposals = 39321600)
-python tools/ncu_summary.py gpurun_out/k_chains.ncu-rep --proposals 39321600 --tag r1 > /dev/null 2>&1 && \
-    cp profiles/r1/k_chains_summary.json gpurun_out/k_chains_summary.json
+python tools/ncu_summary.py gpurun_out/k_chains.ncu-rep --proposals 39321600 --tag ${TAG:-r2} > /dev/null 2>&1 && \
+    cp profiles/${TAG:-r2}/k_chains_summary.json gpurun_out/k_chains_summary.json
 # the same for configs[3]'s shard (N=4096: k_chains<4>; 4 levels ~ what its 7.9 ms device budget allows)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 \
     -o gpurun_out/k_chains_n4096 python tools/prof_chains.py --bench --n 4096 --levels 4 > gpurun_out/ncu_full_n4096.log 2>&1
-python tools/ncu_summary.py gpurun_out/k_chains_n4096.ncu-rep --proposals 19660800 --tag r1 --n 4096 --mb 4 \
+python tools/ncu_summary.py gpurun_out/k_chains_n4096.ncu-rep --proposals 19660800 --tag ${TAG:-r2} --n 4096 --mb 4 \
     --out k_chains_summary_n4096_mb4.json --desc "k_chains<4> (N=4096, mb=4, 16384 chains, prof_chains.py --bench --n 4096 --levels 4)" \
-    > /dev/null 2>&1 && cp profiles/r1/k_chains_summary_n4096_mb4.json gpurun_out/
+    > /dev/null 2>&1 && cp profiles/${TAG:-r2}/k_chains_summary_n4096_mb4.json gpurun_out/
 # launch list of the bench command (times are cold-cache and serialised: use the shares)
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-cpu-baseline --e2e-steps 2 \
