@@ -235,20 +235,12 @@ def run_ours(args):
     from paper_2504_14966_b200 import engine as E
 
     world, rank, local = dist_env()
-    # SLO_BENCH_BACKEND=gloo runs the N > 1 path with host-side exchanges, ranks sharing GPUs
-    # round-robin (a functional check of the multi-rank code on a one-GPU box; not a measurement)
-    backend = os.environ.get("SLO_BENCH_BACKEND", "nccl")
-    if backend != "nccl":
-        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dist = None
-    xdev = f"cuda:{local}" if backend == "nccl" else None  # exchange tensors
+    xdev = f"cuda:{local}"  # tensors of the host-side bookkeeping reductions (timing, counters)
     if world > 1:
         import torch.distributed as dist
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     w = synthetic_workload(args.n)
     c = S.table_coefficients()
@@ -272,7 +264,13 @@ def run_ours(args):
     start_perm = [pos[x] for x in start.flatten()]
     start_sizes = [len(b) for b in start.batches]
 
-    eng = E.Engine(local)
+    comm = None
+    if world > 1:  # the rank's engine context carries the NCCL communicator of the device-side exchange
+        from paper_2504_14966_b200.distributed import RankComm
+        comm = RankComm(local)
+        eng = comm.engine
+    else:
+        eng = E.Engine(local)
     ex, dl = E.build_tables(w, ids, c, mb)
     eng.set_problem(ex, dl)
     smem_peak_gbs = None
@@ -286,40 +284,34 @@ def run_ours(args):
     # get the rest of the budget minus a 0.3 ms margin (the kernel stops within 8 proposals of it)
     cal = S.AnnealConfig(t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                          chains=chains_total, chain_begin=cb, chain_end=ce, budget_ms=2.0,
-                         scale_ladder=SCALE_LADDER, device=local)
+                         scale_ladder=SCALE_LADDER, device=local, comm_ctx=comm.handle if comm else None)
     S.anneal_flat(w, ids_host, c, cal, mb)
-    host_ms = 0.0
+    host_ms, exch_ms = 0.0, 0.0
     for _ in range(5):
         t0 = time.perf_counter()
         st = S.anneal_flat(w, ids_host, c, cal, mb)[5]
-        host_ms = max(host_ms, (time.perf_counter() - t0) * 1e3 - st.kernel_ms)
+        host_ms = max(host_ms, (time.perf_counter() - t0) * 1e3 - st.kernel_ms - st.exchange_ms)
+        exch_ms = max(exch_ms, st.exchange_ms)
     if dist:
-        hm = torch.tensor([host_ms], dtype=torch.float64, device=xdev or "cpu")
+        hm = torch.tensor([host_ms, exch_ms], dtype=torch.float64, device=xdev)
         dist.all_reduce(hm, op=dist.ReduceOp.MAX)
-        host_ms = float(hm[0])
-    kernel_budget_ms = max(0.5, args.budget_ms - host_ms - 0.3)
+        host_ms, exch_ms = float(hm[0]), float(hm[1])
+    # the exchange (N > 1: argmax + all-gather + pick, measured above) comes out of the budget too
+    kernel_budget_ms = max(0.5, args.budget_ms - host_ms - exch_ms - 0.3)
     eng.prepare(start_perm, start_sizes, t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                 objective_scale=scale, chains=chains_total, chain_begin=cb, chain_end=ce,
                 budget_ms=kernel_budget_ms, scale_ladder=SCALE_LADDER)
     stream = torch.cuda.ExternalStream(eng.stream, device=torch.device("cuda", local))
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=f"cuda:{local}")  # > 126 MB L2
 
-    from paper_2504_14966_b200.distributed import LocalBest, exchange_best
-
     def step():
         with torch.cuda.stream(stream):
             flush.zero_()  # L2 flush between steps (outside the events)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        eng.launch()
-        if world == 1:
-            e1.record(stream)
-            bp, bs, res = eng.fetch()
-        else:  # best-of-GPUs inside the step: all-gather (g, t, chain), broadcast the winner
-            bp, bs, res = eng.fetch()
-            exchange_best(LocalBest(res.g, res.t, res.chain, np.asarray(ids, dtype=np.int32)[bp], bs), n,
-                          device=xdev)
-            e1.record(torch.cuda.current_stream())  # after the exchange completed
+        eng.launch()  # N > 1: chains, argmax, then the device-side exchange (all-gather + pick)
+        e1.record(stream)
+        bp, bs, res = eng.fetch()  # the job-wide winner on every rank
         return e0, e1, res
 
     for _ in range(args.warmup):
@@ -336,8 +328,9 @@ def run_ours(args):
         for _ in range(args.steps):
             e0, e1, res = step()
             events.append((e0, e1))
-            results.append((res.proposals, res.kernel_ms, res.positions_pass1, res.positions_pass2, res.g, res.n_met,
-                            res.levels_run, res.chains_run))
+            # this rank's own counts (after the exchange the others are job-wide sums)
+            results.append((res.local_proposals, res.kernel_ms, res.local_positions_pass1, res.local_positions_pass2,
+                            res.g, res.n_met, res.levels_run, res.chains_run, res.exchange_ms))
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -360,20 +353,16 @@ def run_ours(args):
     # ---- e2e: the public C-ABI call from host arrays, per step (+ the cross-GPU exchange)
     cfg = S.AnnealConfig(t0=args.t0, t_thres=args.t_thres, iter=args.iter, tau=args.tau, seed=SEED,
                          chains=chains_total, chain_begin=cb, chain_end=ce, budget_ms=kernel_budget_ms,
-                         scale_ladder=SCALE_LADDER, device=local)
+                         scale_ladder=SCALE_LADDER, device=local, comm_ctx=comm.handle if comm else None)
     S.anneal_flat(w, ids_host, c, cfg, mb)  # warm the context pool
     e2e_props, e2e_s, final = 0.0, 0.0, None
     if dist:
         dist.barrier()
     for _ in range(args.e2e_steps):
         t0 = time.perf_counter()
-        seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids_host, c, cfg, mb)
-        if dist:
-            _, seq, sizes, (g, n_met) = exchange_best(
-                LocalBest(st.engine_g, st.engine_t, st.best_chain, seq, sizes, g, n_met), n, device=xdev,
-                return_record=True)
+        seq, sizes, n_met, t_ms, g, st = S.anneal_flat(w, ids_host, c, cfg, mb)  # job-wide result on every rank
         e2e_s += time.perf_counter() - t0
-        e2e_props += st.proposals
+        e2e_props += st.proposals / world  # job-wide count, identical on every rank (SUM below)
         final = (n_met, g, st)
     if dist:
         t = torch.tensor([e2e_s, e2e_props], dtype=torch.float64, device=xdev or "cpu")

@@ -51,6 +51,10 @@ typedef struct {
     int32_t max_blocks;             /* > 0: cap the chain grid (concurrent callers share the GPU) */
     int32_t start_policy;           /* chains: 0 = best of the reference's two starts and the deadline-first
                                        candidate (default), 1 = the reference's two only */
+    int32_t n_devices;              /* multi-GPU, one process: > 1 devices share the chains (slo_group) */
+    const int32_t* devices;
+    void* comm_ctx;                 /* multi-process: this rank's slo_ctx with an NCCL communicator
+                                       (slo_ctx_comm_init); NULL otherwise */
 } slosched_anneal_config;
 
 typedef struct {
@@ -60,6 +64,8 @@ typedef struct {
     int32_t chains_run, levels_run, best_chain;
     double engine_g, engine_t, kernel_ms;
     double g_deadline_start;
+    double exchange_ms;             /* multi-GPU: chain kernel end -> job-wide winner (device time) */
+    int32_t devices;                /* devices whose chains the result covers */
 } slosched_anneal_stats;
 
 const char* slosched_last_error(void);

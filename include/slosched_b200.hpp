@@ -28,6 +28,8 @@
 #include <variant>
 #include <vector>
 
+struct slo_ctx;  // include/slosched_gpu.h
+
 namespace slosched {
 
 // ---------------------------------------------------------------- errors
@@ -200,6 +202,13 @@ struct EngineOptions {
     int max_blocks = 0;                 // > 0: cap the chain grid (concurrent launches share the GPU)
     bool concurrent_instances = true;   // schedule_all: anneal the instances concurrently (Chains mode)
     bool deadline_start = true;         // Chains mode: the deadline-first candidate joins the two starts
+    // multi-GPU (Chains mode; see include/slosched_gpu.h). The chains [chain_begin, chain_end) of
+    // one call shard across devices and one device-side exchange picks the job-wide best:
+    std::vector<int> devices;           // > 1 entry: this process drives all of them (slo_group, NCCL);
+                                        //   1 entry: that device (overrides `device`)
+    ::slo_ctx* comm_ctx = nullptr;      // one rank of a multi-process job: a context with an NCCL
+                                        //   communicator (slo_ctx_comm_init); chain_end < 0 runs this
+                                        //   rank's balanced share of `chains`
 };
 
 struct AnnealConfig {
@@ -228,6 +237,8 @@ struct AnnealStats {
     double engine_t = 0.0;    // its summed latency (tie-break of the best-of-chains argmax)
     double kernel_ms = 0.0;   // device time of the annealing launch
     double g_deadline_start = 0.0;  // G of the deadline-first candidate (Chains mode; 0 if not built)
+    double exchange_ms = 0.0; // multi-GPU: device time from the chain kernel's end to the job-wide winner
+    int devices = 1;          // devices whose chains the result covers
 };
 
 struct AnnealResult {

@@ -123,6 +123,11 @@ typedef struct {
     uint64_t exact_walks;     /* Philox mode: 32-position unit walks the tick grid could not certify,
                                  decided by the reference's fp64 arithmetic (n_met is always the
                                  reference's) */
+    float exchange_ms;        /* multi-device: device time from the end of the chain kernel to the
+                                 job-wide winner (argmax + slot pack + all-gather + pick); 0 otherwise */
+    int32_t nranks;           /* devices whose chains the result covers (1 without an exchange) */
+    uint64_t local_proposals; /* this device's share of proposals / positions_pass1 / positions_pass2 */
+    uint64_t local_positions_pass1, local_positions_pass2;
 } slo_chain_result;
 
 /* Run chains from the start schedule (dense indices in position order + batch sizes) and
@@ -140,6 +145,45 @@ int slo_chains_prepare(slo_ctx* ctx, const slo_chain_params* params, const int32
 int slo_chains_launch(slo_ctx* ctx);
 int slo_chains_fetch(slo_ctx* ctx, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb,
                      slo_chain_result* result);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * Chains shard across devices by global chain id (each chain's moves depend only on the seed and
+ * its id, so the sharded job runs the same chains as one device would); after every device's
+ * best-of-chains one device-side exchange -- an NCCL all-gather of one slot per device (header +
+ * winner state), then an on-device pick in the k_argmax order -- leaves the job-wide winner on
+ * every device. Nothing crosses the host between the chain kernel and the winner.
+ * Replaces: nothing in the reference (one CPU chain per instance, P:src/scheduler.cpp:109-123). */
+#define SLO_COMM_ID_BYTES 128
+
+/* Multi-process (one rank per GPU): rank 0 creates the id, the launcher distributes it (e.g.
+ * torch.distributed), every rank attaches it to its context (ncclCommInitRank; collective).
+ * Afterwards slo_chains_launch also enqueues the exchange, slo_chains_fetch returns the job-wide
+ * winner on every rank (chain ids global), and a rank may be given an empty slice
+ * (chain_begin == chain_end). */
+int slo_comm_unique_id(uint8_t id[SLO_COMM_ID_BYTES]);
+int slo_ctx_comm_init(slo_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[SLO_COMM_ID_BYTES]);
+int slo_ctx_comm_info(slo_ctx* ctx, int32_t* nranks, int32_t* rank);
+/* ncclCommGetAsyncError of the attached communicator (SLO_ERR_COMM on a failed peer). */
+int slo_comm_check(slo_ctx* ctx);
+
+/* Single process, several devices: one context (stream) per listed device and one NCCL
+ * communicator over them (ncclCommInitAll). A device listed twice cannot join an NCCL
+ * communicator; such groups (and SLOSCHED_EXCHANGE=peer) gather the slots with peer copies
+ * onto member 0 instead (transport "peer"). */
+typedef struct slo_group slo_group;
+int slo_group_create(int32_t ndev, const int32_t* devices, slo_group** out);
+void slo_group_destroy(slo_group* group);
+int32_t slo_group_size(slo_group* group);
+slo_ctx* slo_group_ctx(slo_group* group, int32_t i);
+const char* slo_group_transport(slo_group* group);  /* "nccl" or "peer" */
+/* slo_problem_set on every member (host threads in parallel). */
+int slo_group_problem_set(slo_group* group, int32_t n, int32_t mb, const double* exec, const double* deadline);
+/* slo_anneal_chains over the group: chain ids [chain_begin, chain_end < 0 ? chains : chain_end)
+ * split into contiguous balanced slices, one per member; Philox mode only. kernel_ms is the
+ * slowest member's. Synchronous. */
+int slo_group_anneal_chains(slo_group* group, const slo_chain_params* params, const int32_t* start_perm,
+                            const int32_t* start_sizes, int32_t start_nb, int32_t* best_perm,
+                            int32_t* best_sizes, int32_t* best_nb, slo_chain_result* result);
 
 /* Exhaustive search of the current problem: every permutation x every ordered batch-size
  * composition with parts <= mb, one candidate stream per thread, best by the reference's order

@@ -14,6 +14,7 @@ LIB_PATH = os.environ.get("SLOSCHED_LIB") or os.path.join(PKG, "libslosched_b200
 # slo_status codes (include/slosched_gpu.h)
 SLO_OK, SLO_ERR_DATA, SLO_ERR_CAPACITY, SLO_ERR_CUDA, SLO_ERR_COMM, SLO_ERR_STATE, SLO_ERR_ARG = range(7)
 SLO_MAX_N, SLO_MAX_MB = 4096, 16
+SLO_COMM_ID_BYTES = 128
 SLO_RNG_PHILOX, SLO_RNG_XOSHIRO_REPLAY = 0, 1
 
 
@@ -30,7 +31,8 @@ class SloAnnealConfig(Structure):
                 ("chains", c_int32), ("budget_ms", c_double), ("n_scale_ladder", c_int32),
                 ("scale_ladder", POINTER(c_double)), ("device", c_int32), ("chain_begin", c_int32),
                 ("chain_end", c_int32), ("sequential_instances", c_int32), ("max_blocks", c_int32),
-                ("start_policy", c_int32)]
+                ("start_policy", c_int32), ("n_devices", c_int32), ("devices", POINTER(c_int32)),
+                ("comm_ctx", c_void_p)]
 
 
 class SloAnnealStats(Structure):
@@ -38,7 +40,7 @@ class SloAnnealStats(Structure):
                 ("g_sorted_start", c_double), ("g_input_start", c_double), ("objective_scale_used", c_double),
                 ("chains_run", c_int32), ("levels_run", c_int32), ("best_chain", c_int32),
                 ("engine_g", c_double), ("engine_t", c_double), ("kernel_ms", c_double),
-                ("g_deadline_start", c_double)]
+                ("g_deadline_start", c_double), ("exchange_ms", c_double), ("devices", c_int32)]
 
 
 class SloChainParams(Structure):
@@ -52,7 +54,9 @@ class SloChainResult(Structure):
     _fields_ = [("g", c_double), ("t", c_double), ("n_met", c_int32), ("chain", c_int32),
                 ("proposals", c_uint64), ("accepted", c_uint64), ("chains_run", c_int32),
                 ("levels_run", c_int32), ("kernel_ms", c_float), ("positions_pass1", c_uint64),
-                ("positions_pass2", c_uint64), ("exact_walks", c_uint64)]
+                ("positions_pass2", c_uint64), ("exact_walks", c_uint64), ("exchange_ms", c_float),
+                ("nranks", c_int32), ("local_proposals", c_uint64), ("local_positions_pass1", c_uint64),
+                ("local_positions_pass2", c_uint64)]
 
 
 _I = POINTER(c_int32)
@@ -78,6 +82,18 @@ _SIGNATURES = [
     ("slo_chains_launch", c_int32, [c_void_p]),
     ("slo_chains_fetch", c_int32, [c_void_p, _I, _I, _I, POINTER(SloChainResult)]),
     ("slo_probe_smem_bandwidth", c_int32, [c_void_p, POINTER(c_double)]),
+    ("slo_comm_unique_id", c_int32, [POINTER(ctypes.c_uint8)]),
+    ("slo_ctx_comm_init", c_int32, [c_void_p, c_int32, c_int32, POINTER(ctypes.c_uint8)]),
+    ("slo_ctx_comm_info", c_int32, [c_void_p, _I, _I]),
+    ("slo_comm_check", c_int32, [c_void_p]),
+    ("slo_group_create", c_int32, [c_int32, _I, POINTER(c_void_p)]),
+    ("slo_group_destroy", None, [c_void_p]),
+    ("slo_group_size", c_int32, [c_void_p]),
+    ("slo_group_ctx", c_void_p, [c_void_p, c_int32]),
+    ("slo_group_transport", c_char_p, [c_void_p]),
+    ("slo_group_problem_set", c_int32, [c_void_p, c_int32, c_int32, _D, _D]),
+    ("slo_group_anneal_chains", c_int32, [c_void_p, POINTER(SloChainParams), _I, _I, c_int32, _I, _I, _I,
+                                          POINTER(SloChainResult)]),
     ("slo_philox4x32_10", None, [POINTER(c_uint32), POINTER(c_uint32), POINTER(c_uint32)]),
     ("slosched_last_error", c_char_p, []),
     ("slosched_predict", c_int32, [_D, c_int32, c_int32, c_int32, _D]),

@@ -69,15 +69,19 @@ def build(verbose=False, force=False, ptxas_info=False) -> str:
         tmp = LIB + ".tmp"
         # -Bsymbolic: the library's own C++ calls bind inside it even when a process also loads
         # the reference's slosched:: symbols (the integration shim does exactly that)
-        log += _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-Xlinker", "-Bsymbolic"], verbose)
+        log += _run([NVCC] + ARCH + ["-shared", "-o", tmp] + objs + ["-lpthread", "-ldl", "-Xlinker", "-Bsymbolic"], verbose)
         os.replace(tmp, LIB)
-    # the C++ example (a reference-style caller of include/slosched_b200.hpp)
-    ex_src = os.path.join(ROOT, "examples", "anneal_example.cpp")
-    ex_bin = os.path.join(ROOT, "examples", "_build", "anneal_example")
-    if os.path.exists(ex_src) and (force or _stale(ex_bin, [ex_src, LIB] + headers)):
-        os.makedirs(os.path.dirname(ex_bin), exist_ok=True)
-        log += _run(["g++", "-std=c++17", "-O2", f"-I{INC}", ex_src, "-o", ex_bin, f"-L{PKG}", "-lslosched_b200",
-                     f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_2504_14966_b200"], verbose)
+    # the C++ examples (reference-style callers of include/slosched_b200.hpp / slosched_gpu.h)
+    ex_dir = os.path.join(ROOT, "examples")
+    for name in sorted(os.listdir(ex_dir)) if os.path.isdir(ex_dir) else []:
+        if not name.endswith(".cpp"):
+            continue
+        ex_src = os.path.join(ex_dir, name)
+        ex_bin = os.path.join(ex_dir, "_build", name[:-4])
+        if force or _stale(ex_bin, [ex_src, LIB] + headers):
+            os.makedirs(os.path.dirname(ex_bin), exist_ok=True)
+            log += _run(["g++", "-std=c++17", "-O2", f"-I{INC}", ex_src, "-o", ex_bin, f"-L{PKG}", "-lslosched_b200",
+                         f"-Wl,-rpath,{PKG}", "-Wl,-rpath,$ORIGIN/../../paper_2504_14966_b200"], verbose)
     return log
 
 

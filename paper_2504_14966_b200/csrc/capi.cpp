@@ -100,6 +100,8 @@ AnnealConfig config_of(const slosched_anneal_config* c) {
     a.engine.concurrent_instances = c->sequential_instances == 0;
     a.engine.max_blocks = c->max_blocks;
     a.engine.deadline_start = c->start_policy == 0;
+    if (c->n_devices > 0 && c->devices) a.engine.devices.assign(c->devices, c->devices + c->n_devices);
+    a.engine.comm_ctx = static_cast<slo_ctx*>(c->comm_ctx);
     return a;
 }
 
@@ -118,6 +120,8 @@ void stats_out(const AnnealStats& s, slosched_anneal_stats* o) {
     o->engine_t = s.engine_t;
     o->kernel_ms = s.kernel_ms;
     o->g_deadline_start = s.g_deadline_start;
+    o->exchange_ms = s.exchange_ms;
+    o->devices = s.devices;
 }
 
 }  // namespace

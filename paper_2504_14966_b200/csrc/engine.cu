@@ -286,6 +286,14 @@ int pick_upl(int n) {
     return units <= 32 ? 1 : (units <= 64 ? 2 : 4);
 }
 
+// exchange.cuh
+void comm_destroy(void* comm);
+int ex_reserve(slo_ctx* c, int nslots);
+int ex_pack(slo_ctx* c);
+int ex_allgather(slo_ctx* c);
+int ex_pick(slo_ctx* c, int nslots);
+int ex_local_counts(slo_ctx* c, unsigned long long out[3]);  // async D2H on the stream
+
 }  // namespace
 
 struct slo_ctx {
@@ -315,6 +323,16 @@ struct slo_ctx {
     int start_nb = 0;
     ChainParams kp{};
     ReplayParams rp{};
+    // cross-device exchange (exchange.cuh)
+    void* comm = nullptr;        // ncclComm_t: slo_ctx_comm_init (multi-process) or slo_group_create
+    bool own_comm = false;
+    int nranks = 1, rank = 0;
+    slo_group* group = nullptr;  // member of a single-process group (the group drives the exchange)
+    DevBuf ex_slot, ex_gather;
+    size_t ex_slot_bytes = 0;
+    bool exchanged = false;      // result / win_* hold the job-wide winner (global chain id)
+    bool empty_slice = false;    // this rank runs no chain (fewer chains than ranks)
+    cudaEvent_t ev2 = nullptr, ev_pack = nullptr;
 };
 
 extern "C" {
@@ -344,6 +362,8 @@ int slo_ctx_create(int device, slo_ctx** out) {
     cudaError_t e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev0);
     if (e == cudaSuccess) e = cudaEventCreate(&c->ev1);
+    if (e == cudaSuccess) e = cudaEventCreate(&c->ev2);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->ev_pack, cudaEventDisableTiming);
     if (e != cudaSuccess) {
         delete c;
         return fail(SLO_ERR_CUDA, std::string("slo_ctx_create: ") + cudaGetErrorString(e));
@@ -356,8 +376,11 @@ void slo_ctx_destroy(slo_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    if (c->comm && c->own_comm) comm_destroy(c->comm);
     cudaEventDestroy(c->ev0);
     cudaEventDestroy(c->ev1);
+    cudaEventDestroy(c->ev2);
+    cudaEventDestroy(c->ev_pack);
     cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -641,7 +664,10 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     if (!(prm->objective_scale >= 0.0)) return fail(SLO_ERR_DATA, "AnnealConfig: objective_scale must be >= 0");
     const int n = c->n;
     const int cb = prm->chain_begin, ce = prm->chain_end;
-    if (cb < 0 || ce <= cb || ce > prm->chains) return fail(SLO_ERR_ARG, "slo_chains_prepare: bad chain slice");
+    // a rank with a communicator may run no chain (fewer chains than ranks): it still takes part
+    // in the exchange with an empty slot
+    const bool empty = ce == cb && c->comm && prm->rng_mode == SLO_RNG_PHILOX;
+    if (cb < 0 || (ce <= cb && !empty) || ce > prm->chains) return fail(SLO_ERR_ARG, "slo_chains_prepare: bad chain slice");
     // validate the start schedule
     {
         std::vector<char> seen(n, 0);
@@ -663,6 +689,8 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     c->levels = count_levels(prm->t0, prm->t_thres, prm->tau);
     c->start_nb = start_nb;
     c->prepared = false;
+    c->exchanged = false;
+    c->empty_slice = empty;
 
     if (prm->rng_mode == SLO_RNG_XOSHIRO_REPLAY) {  // K2: one warp per chain, state in shared memory
         const int chains = c->chain_count;
@@ -718,6 +746,15 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     const int UPL = pick_upl(n);
     c->UPL = UPL;
     const size_t ent_words = 1024 * (size_t)UPL, bit_words = 32 * (size_t)UPL;
+    if (empty) {  // only the exchange buffers: the slot says "no chain"
+        CK(c->result.reserve(sizeof(ChainResult)));
+        CK(c->win_ent.reserve(ent_words * sizeof(uint16_t)));
+        CK(c->win_bits.reserve(bit_words * sizeof(uint32_t)));
+        CK(c->exact_count.reserve(sizeof(unsigned long long)));
+        if (int rc = ex_reserve(c, c->nranks)) return rc;
+        c->prepared = true;
+        return SLO_OK;
+    }
     // start state: linear entries (batch_size-1)*n + dense index, linear batch-end bitmask
     std::vector<uint16_t> ent(ent_words, 0);
     std::vector<uint32_t> bits(bit_words, 0);
@@ -776,14 +813,24 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
     kp.rec = c->rec.as<ChainRec>();
     CK(c->exact_count.reserve(sizeof(unsigned long long)));
     kp.exact_count = c->exact_count.as<unsigned long long>();
+    if (c->comm && !c->group)
+        if (int rc = ex_reserve(c, c->nranks)) return rc;
     c->prepared = true;
     return SLO_OK;
 }
 
-int slo_chains_launch(slo_ctx* c) {
-    if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_launch: not prepared");
-    CK(cudaSetDevice(c->device));
+}  // extern "C"
+
+namespace {
+// this device's chains and best-of-chains (no exchange)
+int launch_local(slo_ctx* c) {
     const size_t cc = c->chain_count;
+    c->exchanged = false;
+    if (c->empty_slice) {
+        CK(cudaEventRecord(c->ev0, c->stream));
+        CK(cudaEventRecord(c->ev1, c->stream));
+        return SLO_OK;
+    }
     CK(cudaMemsetAsync(c->rec.p, 0, cc * sizeof(ChainRec), c->stream));
     if (c->prm.rng_mode != SLO_RNG_XOSHIRO_REPLAY)
         CK(cudaMemsetAsync(c->exact_count.p, 0, sizeof(unsigned long long), c->stream));
@@ -807,6 +854,24 @@ int slo_chains_launch(slo_ctx* c) {
     CK(cudaGetLastError());
     return SLO_OK;
 }
+}  // namespace
+
+extern "C" {
+
+int slo_chains_launch(slo_ctx* c) {
+    if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_launch: not prepared");
+    if (c->group) return fail(SLO_ERR_STATE, "slo_chains_launch: the context belongs to a group (slo_group_anneal_chains)");
+    CK(cudaSetDevice(c->device));
+    if (int rc = launch_local(c)) return rc;
+    // multi-process: the job-wide winner on every rank, enqueued behind the local argmax
+    if (c->comm && c->prm.rng_mode == SLO_RNG_PHILOX) {
+        if (int rc = ex_pack(c)) return rc;
+        if (int rc = ex_allgather(c)) return rc;
+        if (int rc = ex_pick(c, c->nranks)) return rc;
+        CK(cudaEventRecord(c->ev2, c->stream));
+    }
+    return SLO_OK;
+}
 
 int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_t* best_nb, slo_chain_result* out) {
     if (!c || !c->prepared) return fail(SLO_ERR_STATE, "slo_chains_fetch: not prepared");
@@ -816,6 +881,10 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     CK(cudaMemcpyAsync(&r, c->result.p, sizeof r, cudaMemcpyDeviceToHost, c->stream));
     if (c->prm.rng_mode != SLO_RNG_XOSHIRO_REPLAY)
         CK(cudaMemcpyAsync(&exact, c->exact_count.p, sizeof exact, cudaMemcpyDeviceToHost, c->stream));
+    if (c->empty_slice && !c->exchanged) return fail(SLO_ERR_STATE, "slo_chains_fetch: this rank ran no chain");
+    unsigned long long local[3] = {0, 0, 0};
+    if (c->exchanged)
+        if (int rc = ex_local_counts(c, local)) return rc;
     const int n = c->n;
     std::vector<uint16_t> ent;
     std::vector<uint32_t> bits;
@@ -827,8 +896,9 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     CK(cudaMemcpyAsync(ent.data(), c->win_ent.p, ent.size() * sizeof(uint16_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaMemcpyAsync(bits.data(), c->win_bits.p, bits.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost, c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    float ms = 0.f;
+    float ms = 0.f, xms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev0, c->ev1));
+    if (c->exchanged) CK(cudaEventElapsedTime(&xms, c->ev1, c->ev2));
     if (r.chain < 0) return fail(SLO_ERR_STATE, "slo_chains_fetch: no chain ran (budget too small?)");
     {
         int nb = 0, run = 0;
@@ -841,13 +911,17 @@ int slo_chains_fetch(slo_ctx* c, int32_t* best_perm, int32_t* best_sizes, int32_
     }
     if (out) {
         out->g = r.g, out->t = r.t, out->n_met = r.n_met;
-        out->chain = c->prm.chain_begin + r.chain;
+        out->chain = c->exchanged ? r.chain : c->prm.chain_begin + r.chain;
         out->proposals = r.proposals, out->accepted = r.accepted;
         out->chains_run = r.chains_run, out->levels_run = r.levels_min;
         out->kernel_ms = ms;
         out->positions_pass1 = r.scan1;
         out->positions_pass2 = r.scan2;
         out->exact_walks = exact;
+        out->exchange_ms = xms;
+        if (c->exchanged) out->local_proposals = local[0], out->local_positions_pass1 = local[1], out->local_positions_pass2 = local[2];
+        else out->local_proposals = r.proposals, out->local_positions_pass1 = r.scan1, out->local_positions_pass2 = r.scan2;
+        out->nranks = c->exchanged ? (c->group ? (int)slo_group_size(c->group) : c->nranks) : 1;
     }
     return SLO_OK;
 }
@@ -962,3 +1036,11 @@ int slo_anneal_chains(slo_ctx* c, const slo_chain_params* prm, const int32_t* st
 }
 
 }  // extern "C"
+
+#include "exchange.cuh"
+
+namespace {
+void comm_destroy(void* comm) {
+    if (nccl_api().ok) nccl_api().CommDestroy((ncclComm_t)comm);
+}
+}  // namespace

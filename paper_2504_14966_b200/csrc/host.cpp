@@ -13,6 +13,7 @@
 #include <cstring>
 #include <future>
 #include <limits>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <numeric>
@@ -617,6 +618,106 @@ void engine_check(int rc) {
     throw EngineError("B200 engine: " + msg);
 }
 
+struct GroupDeleter {
+    void operator()(slo_group* g) const { slo_group_destroy(g); }
+};
+using GroupPtr = std::unique_ptr<slo_group, GroupDeleter>;
+
+// Device groups (one context per device + one NCCL communicator) keyed by their device list;
+// creating a communicator is expensive (tens of ms), so groups are kept for reuse.
+class GroupPool {
+public:
+    static GroupPool& get() {
+        static GroupPool* pool = new GroupPool();  // leaked on purpose, like CtxPool
+        return *pool;
+    }
+    GroupPtr acquire(const std::vector<int>& devs) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            auto& v = free_[devs];
+            if (!v.empty()) {
+                GroupPtr p(v.back());
+                v.pop_back();
+                return p;
+            }
+        }
+        slo_group* g = nullptr;
+        if (int rc = slo_group_create(static_cast<int32_t>(devs.size()), devs.data(), &g)) engine_check(rc);
+        return GroupPtr(g);
+    }
+    void release(const std::vector<int>& devs, GroupPtr g) {
+        std::lock_guard<std::mutex> l(mu_);
+        free_[devs].push_back(g.release());
+    }
+
+private:
+    std::mutex mu_;
+    std::map<std::vector<int>, std::vector<slo_group*>> free_;
+};
+
+// Where one anneal() runs: a pooled context on one device, the caller's rank context (one
+// process per GPU, NCCL communicator attached), or a pooled group of devices in this process.
+class EngineHandle {
+public:
+    explicit EngineHandle(const EngineOptions& eo) {
+        if (eo.comm_ctx) {
+            external_ = eo.comm_ctx;
+        } else if (eo.devices.size() > 1) {
+            devs_ = eo.devices;
+        } else {
+            device_ = eo.devices.size() == 1 ? eo.devices[0] : resolve_device(eo.device);
+        }
+    }
+    ~EngineHandle() {
+        if (!ok_) return;  // a failed call destroys its context / group instead of pooling it
+        if (ctx_) CtxPool::get().release(device_, std::move(ctx_));
+        if (group_) GroupPool::get().release(devs_, std::move(group_));
+    }
+    void problem_set(int n, int mb, const double* exec, const double* deadline) {
+        ok_ = false;
+        if (!devs_.empty()) {
+            group_ = GroupPool::get().acquire(devs_);
+            engine_check(slo_group_problem_set(group_.get(), n, mb, exec, deadline));
+        } else {
+            if (!external_) ctx_ = CtxPool::get().acquire(device_);
+            engine_check(slo_problem_set(ctx(), n, mb, exec, deadline));
+        }
+        ok_ = true;
+    }
+    bool ready() const { return group_ || ctx_ || external_; }
+    // the chain slice of this call: the caller's, else (rank context) this rank's share
+    void slice(const EngineOptions& eo, int chains, int* b, int* e) const {
+        *b = eo.chain_begin, *e = eo.chain_end < 0 ? chains : eo.chain_end;
+        if (external_ && eo.chain_end < 0) {
+            int32_t nr = 1, rk = 0;
+            engine_check(slo_ctx_comm_info(external_, &nr, &rk));
+            const int base = chains / nr, extra = chains % nr;
+            *b = rk * base + std::min<int>(rk, extra);
+            *e = *b + base + (rk < extra ? 1 : 0);
+        }
+    }
+    void anneal(const slo_chain_params& prm, const std::vector<int>& sp, const std::vector<int>& ss,
+                std::vector<int>& bp, std::vector<int>& bs, int* nb, slo_chain_result* cr) {
+        ok_ = false;
+        if (group_ && prm.rng_mode == SLO_RNG_PHILOX)
+            engine_check(slo_group_anneal_chains(group_.get(), &prm, sp.data(), ss.data(), static_cast<int>(ss.size()),
+                                                 bp.data(), bs.data(), nb, cr));
+        else
+            engine_check(slo_anneal_chains(ctx(), &prm, sp.data(), ss.data(), static_cast<int>(ss.size()), bp.data(),
+                                           bs.data(), nb, cr));
+        ok_ = true;
+    }
+
+private:
+    slo_ctx* ctx() const { return external_ ? external_ : (ctx_ ? ctx_.get() : slo_group_ctx(group_.get(), 0)); }
+    int device_ = 0;
+    std::vector<int> devs_;
+    slo_ctx* external_ = nullptr;
+    CtxPtr ctx_;
+    GroupPtr group_;
+    bool ok_ = true;
+};
+
 }  // namespace
 
 void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c, int max_batch,
@@ -830,27 +931,15 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     std::vector<int> dl_perm, dl_sizes;
     std::optional<double> g_dl;  // G of the deadline-first candidate (evaluated in full only if returned)
     const bool want_dl = cfg.engine.mode == SearchMode::Chains && cfg.engine.deadline_start;
-    // the engine context is acquired and the tables uploaded on the same thread, as soon as they exist
-    const int device = resolve_device(cfg.engine.device);
-    CtxPtr ctx;
-    bool ctx_ok = false;  // ctx holds this problem and may go back to the pool
-    struct PoolReturn {
-        CtxPtr& c;
-        int dev;
-        const bool& ok;
-        ~PoolReturn() {
-            if (c && ok) CtxPool::get().release(dev, std::move(c));
-        }
-    } pool_return{ctx, device, ctx_ok};
+    // the engine (context, rank context or device group) gets the tables on the same thread, as
+    // soon as they exist
+    EngineHandle eng(cfg.engine);
     auto tables = std::async(std::launch::async, [&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
         // the upload (context, tables, device-side tick tables) overlaps the deadline-first start
         auto upload = std::async(std::launch::async, [&] {
-            if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB) {
-                ctx = CtxPool::get().acquire(device);
-                engine_check(slo_problem_set(ctx.get(), n, max_batch, exec.data(), deadline.data()));
-                ctx_ok = true;
-            }
+            if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB)
+                eng.problem_set(n, max_batch, exec.data(), deadline.data());
         });
         if (want_dl) g_dl = best_deadline_first(n, max_batch, exec, deadline, dl_perm, dl_sizes);
         upload.get();
@@ -900,8 +989,8 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     prm.objective_scale = scale;
     prm.rng_mode = eo.mode == SearchMode::Replay ? SLO_RNG_XOSHIRO_REPLAY : SLO_RNG_PHILOX;
     prm.chains = eo.mode == SearchMode::Replay ? 1 : eo.chains;
-    prm.chain_begin = eo.mode == SearchMode::Replay ? 0 : eo.chain_begin;
-    prm.chain_end = eo.mode == SearchMode::Replay ? 1 : (eo.chain_end < 0 ? eo.chains : eo.chain_end);
+    prm.chain_begin = 0, prm.chain_end = 1;
+    if (eo.mode != SearchMode::Replay) eng.slice(eo, eo.chains, &prm.chain_begin, &prm.chain_end);
     prm.budget_ns = static_cast<int64_t>(eo.budget_ms * 1e6);
     prm.n_scale_mult = static_cast<int32_t>(eo.scale_ladder.size());
     prm.scale_mult = eo.scale_ladder.empty() ? nullptr : eo.scale_ladder.data();
@@ -910,12 +999,8 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     std::vector<int> best_perm(n), best_sizes(n);
     int best_nb = 0;
     slo_chain_result cr{};
-    if (!ctx) throw EngineError("B200 engine: no context for the problem");
-    ctx_ok = false;  // a failed launch destroys the context instead of pooling it
-    engine_check(slo_anneal_chains(ctx.get(), &prm, start_perm.data(), start_sizes.data(),
-                                   static_cast<int>(start_sizes.size()), best_perm.data(), best_sizes.data(), &best_nb,
-                                   &cr));
-    CtxPool::get().release(device, std::move(ctx));
+    if (!eng.ready()) throw EngineError("B200 engine: no context for the problem");
+    eng.anneal(prm, start_perm, start_sizes, best_perm, best_sizes, &best_nb, &cr);
 
     res.stats.proposals = cr.proposals;
     res.stats.accepted = cr.accepted;
@@ -925,6 +1010,8 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     res.stats.engine_g = cr.g;
     res.stats.engine_t = cr.t;
     res.stats.kernel_ms = cr.kernel_ms;
+    res.stats.exchange_ms = cr.exchange_ms;
+    res.stats.devices = cr.nranks;
 
     Schedule best;
     int pos = 0;
@@ -1057,8 +1144,23 @@ ScheduleAllResult schedule_all(const Workload& w, const std::vector<InstanceStat
     // stream, and a 1/k share of the SMs, so the k launches run side by side on the GPU.
     std::vector<AnnealConfig> per(k, cfg);
     const bool concurrent = k > 1 && cfg.engine.mode == SearchMode::Chains && cfg.engine.concurrent_instances;
-    if (concurrent && cfg.engine.max_blocks <= 0) {
-        const int device = resolve_device(cfg.engine.device);
+    const std::vector<int>& devs = cfg.engine.devices;
+    if (concurrent && devs.size() > 1) {
+        // instances are placed one per GPU (round robin); instances sharing a GPU split its SMs
+        std::map<int, int> on_dev;
+        for (std::size_t i = 0; i < k; ++i) ++on_dev[devs[i % devs.size()]];
+        for (std::size_t i = 0; i < k; ++i) {
+            const int d = devs[i % devs.size()];
+            per[i].engine.devices = {d};
+            if (cfg.engine.max_blocks <= 0 && on_dev[d] > 1) {
+                CtxPtr ctx = CtxPool::get().acquire(d);
+                const int sms = slo_ctx_sm_count(ctx.get());
+                CtxPool::get().release(d, std::move(ctx));
+                per[i].engine.max_blocks = std::max(1, sms / on_dev[d]);
+            }
+        }
+    } else if (concurrent && cfg.engine.max_blocks <= 0) {
+        const int device = devs.size() == 1 ? devs[0] : resolve_device(cfg.engine.device);
         CtxPtr ctx = CtxPool::get().acquire(device);
         const int sms = slo_ctx_sm_count(ctx.get());
         CtxPool::get().release(device, std::move(ctx));

@@ -137,3 +137,74 @@ class Engine:
         self.prepare(start_perm, start_sizes, **kw)
         self.launch()
         return self.fetch()
+
+    # ---- multi-process exchange (include/slosched_gpu.h, multi-GPU section)
+    @property
+    def handle(self) -> int:
+        """The slo_ctx pointer (AnnealConfig.comm_ctx of a rank context)."""
+        return int(self._ctx.value or 0)
+
+    def comm_init(self, nranks: int, rank: int, uid: bytes):
+        """Attach an NCCL communicator (collective over the nranks processes): launch() then also
+        enqueues the device-side exchange, fetch() returns the job-wide winner on every rank."""
+        buf = (ctypes.c_uint8 * _lib.SLO_COMM_ID_BYTES).from_buffer_copy(bytes(uid))
+        _check_engine(lib().slo_ctx_comm_init(self._ctx, nranks, rank, buf))
+
+    def comm_info(self):
+        nr, rk = c_int32(), c_int32()
+        _check_engine(lib().slo_ctx_comm_info(self._ctx, byref(nr), byref(rk)))
+        return nr.value, rk.value
+
+    def comm_check(self):
+        _check_engine(lib().slo_comm_check(self._ctx))
+
+
+def comm_unique_id() -> bytes:
+    """A fresh NCCL unique id (rank 0 creates it; the launcher distributes it)."""
+    buf = (ctypes.c_uint8 * _lib.SLO_COMM_ID_BYTES)()
+    _check_engine(lib().slo_comm_unique_id(buf))
+    return bytes(buf)
+
+
+class Group:
+    """Several devices driven by this process (slo_group): one context per device, one NCCL
+    communicator over them (transport "nccl"), or peer copies onto member 0 when a device is
+    listed twice (transport "peer")."""
+
+    def __init__(self, devices):
+        devs = _i32(list(devices))
+        self._g = c_void_p()
+        _check_engine(lib().slo_group_create(len(devs), _p(devs), byref(self._g)))
+        self.devices = [int(d) for d in devs]
+        self.n = 0
+
+    def close(self):
+        if self._g:
+            lib().slo_group_destroy(self._g)
+            self._g = c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def transport(self) -> str:
+        return lib().slo_group_transport(self._g).decode()
+
+    def set_problem(self, exec_tab: np.ndarray, deadline_tab: np.ndarray):
+        mb, n = exec_tab.shape
+        ex, dl = _f64(exec_tab).ravel(), _f64(deadline_tab).ravel()
+        _check_engine(lib().slo_group_problem_set(self._g, n, mb, _p(ex, c_double), _p(dl, c_double)))
+        self.n = n
+
+    def anneal_chains(self, start_perm, start_sizes, **kw):
+        prm, _ladder = Engine._params(None, **kw)
+        sp, ss = _i32(start_perm), _i32(start_sizes)
+        n = self.n
+        bp, bs, nb = np.zeros(n, dtype=np.int32), np.zeros(n, dtype=np.int32), c_int32()
+        res = SloChainResult()
+        _check_engine(lib().slo_group_anneal_chains(self._g, byref(prm), _p(sp), _p(ss), len(ss), _p(bp), _p(bs),
+                                                    byref(nb), byref(res)))
+        return bp, bs[:nb.value], res

@@ -310,17 +310,23 @@ class AnnealConfig:
     sequential_instances: bool = False  # schedule_all: anneal instances one after another
     max_blocks: int = 0                 # > 0: cap the chain grid (concurrent callers share the GPU)
     deadline_start: bool = True         # chains: the deadline-first candidate joins the two starts
+    # multi-GPU: devices of this process sharing the chains (slo_group), or this rank's engine
+    # context with an NCCL communicator (distributed.RankComm.handle) in a one-process-per-GPU job
+    devices: Sequence[int] = ()
+    comm_ctx: Optional[int] = None
 
     def _c(self):
         ladder = _f64(list(self.scale_ladder)) if len(self.scale_ladder) else None
+        devs = _i32(list(self.devices)) if len(self.devices) else None
         cfg = SloAnnealConfig(self.t0, self.t_thres, self.iter, self.tau, self.seed & (2**64 - 1),
                               0 if self.objective_scale is None else 1,
                               0.0 if self.objective_scale is None else self.objective_scale, int(self.mode),
                               self.chains, self.budget_ms, 0 if ladder is None else len(ladder),
                               None if ladder is None else _p(ladder, c_double), self.device, self.chain_begin,
                               self.chain_end, 1 if self.sequential_instances else 0, self.max_blocks,
-                              0 if self.deadline_start else 1)
-        return cfg, ladder
+                              0 if self.deadline_start else 1, 0 if devs is None else len(devs),
+                              None if devs is None else _p(devs), self.comm_ctx)
+        return cfg, (ladder, devs)
 
 
 @dataclass
@@ -338,12 +344,14 @@ class AnnealStats:
     engine_t: float = 0.0
     kernel_ms: float = 0.0
     g_deadline_start: float = 0.0
+    exchange_ms: float = 0.0  # multi-GPU: chain kernel end -> job-wide winner (device time)
+    devices: int = 1          # devices whose chains the result covers
 
     @staticmethod
     def _from(s: SloAnnealStats) -> "AnnealStats":
         return AnnealStats(int(s.proposals), int(s.accepted), bool(s.shortcut), s.g_sorted_start, s.g_input_start,
                            s.objective_scale_used, s.chains_run, s.levels_run, s.best_chain, s.engine_g, s.engine_t,
-                           s.kernel_ms, s.g_deadline_start)
+                           s.kernel_ms, s.g_deadline_start, s.exchange_ms, s.devices)
 
 
 @dataclass

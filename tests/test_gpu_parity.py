@@ -246,15 +246,16 @@ def test_cpp_example_runs_against_the_cpp_api(port):
 
 
 def test_distributed_path_over_nccl_single_rank():
-    """The multi-GPU exchange on real NCCL (one rank here: the box has one GPU per call): CUDA
-    tensors through all_gather / broadcast, and anneal_distributed == anneal over the same chains."""
+    """The multi-process path on real NCCL (one rank here: the box has one GPU per call): the rank
+    context's communicator (slo_ctx_comm_init, id shared over torch.distributed), the device-side
+    exchange enqueued behind the chains, and anneal_distributed == anneal over the same chains."""
     import os
     import socket
 
     import torch
     import torch.distributed as dist
 
-    from paper_2504_14966_b200.distributed import anneal_distributed
+    from paper_2504_14966_b200.distributed import RankComm, anneal_distributed
 
     with socket.socket() as s:
         s.bind(("127.0.0.1", 0))
@@ -265,12 +266,77 @@ def test_distributed_path_over_nccl_single_rank():
         c = S.table_coefficients()
         w = _three_class(96, 31)
         cfg = S.AnnealConfig(seed=2, chains=512, t0=80.0, iter=20, scale_ladder=(1.0, 1e3), device=0)
-        got = anneal_distributed(w, w.ids(), c, cfg, 4)
         want = S.anneal(w, w.ids(), c, cfg, 4)
-        assert got.best.schedule.batches == want.best.schedule.batches and got.best.g == want.best.g
-        assert got.stats.proposals == want.stats.proposals
+        comm = RankComm(0)
+        assert comm.engine.comm_info() == (1, 0)
+        for _ in range(2):  # the communicator is reused across calls
+            got = anneal_distributed(w, w.ids(), c, cfg, 4, comm=comm)
+            assert got.best.schedule.batches == want.best.schedule.batches and got.best.g == want.best.g
+            assert got.stats.proposals == want.stats.proposals and got.stats.best_chain == want.stats.best_chain
+            assert got.stats.devices == 1 and got.stats.exchange_ms > 0.0
+        comm.engine.comm_check()
+        comm.close()
+        got = anneal_distributed(w, w.ids(), c, cfg, 4)  # a communicator of its own
+        assert got.best.schedule.batches == want.best.schedule.batches
     finally:
         dist.destroy_process_group()
+
+
+def test_rank_with_empty_slice_takes_part_in_the_exchange():
+    """A rank given no chain (fewer chains than ranks) still contributes an empty slot; with no
+    chain anywhere the fetch reports it instead of returning garbage."""
+    w = _three_class(64, 5)
+    c = S.table_coefficients()
+    e = E.Engine(0)
+    e.comm_init(1, 0, E.comm_unique_id())
+    ex, dl = E.build_tables(w, w.ids(), c, 4)
+    e.set_problem(ex, dl)
+    s_sched, _ = S.initial_candidates(w, w.ids(), c, 4)
+    pos = {rid: k for k, rid in enumerate(sorted(w.ids()))}
+    sp, ss = [pos[x] for x in s_sched.flatten()], [len(b) for b in s_sched.batches]
+    e.prepare(sp, ss, t0=50.0, iter=5, chains=4, chain_begin=0, chain_end=0, objective_scale=1e6)
+    e.launch()
+    with pytest.raises(Exception, match="no chain"):
+        e.fetch()
+    e.prepare(sp, ss, t0=50.0, iter=5, chains=4, chain_begin=0, chain_end=4, objective_scale=1e6)
+    e.launch()
+    _, _, res = e.fetch()
+    assert res.nranks == 1 and res.chains_run == 4 and 0 <= res.chain < 4
+    e.close()
+
+
+def test_device_group_equals_one_context():
+    """anneal() over a device list (here two contexts on GPU 0: the peer-copy exchange) returns the
+    schedule one context returns over the same chain ids; Group{0} runs the NCCL transport."""
+    c = S.table_coefficients()
+    w = _three_class(300, 8)
+    base = dict(seed=4, chains=2049, t0=120.0, iter=25, scale_ladder=(1.0, 1e4))
+    one = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, device=0), 4)
+    two = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, devices=(0, 0)), 4)
+    assert two.best.schedule.batches == one.best.schedule.batches and two.best.g == one.best.g
+    assert two.stats.best_chain == one.stats.best_chain and two.stats.proposals == one.stats.proposals
+    assert two.stats.devices == 2
+    g = E.Group([0])
+    assert g.transport == "nccl"
+    g.close()
+    g = E.Group([0, 0])
+    assert g.transport == "peer"
+    g.close()
+
+
+def test_cpp_multi_gpu_example():
+    """examples/multi_gpu_example.cpp: the C++ entry point over device groups ({0}: NCCL with one
+    device, {0,0} / {0,0,0}: two / three contexts on one GPU) and schedule_all placement."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "examples", "_build", "multi_gpu_example")
+    if not os.path.exists(exe):
+        pytest.skip("example not built")
+    out = subprocess.run([exe, "400"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("PASS") >= 5 and "FAIL" not in out.stdout
 
 
 # ---------------------------------------------------------------- exhaustive oracle
