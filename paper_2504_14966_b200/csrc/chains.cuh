@@ -129,7 +129,10 @@ __device__ __forceinline__ int prev_end16(const uint32_t* bits, int q) {
     const int w = q >> 5;
     const uint32_t lo = bits[w - 1];
     const uint32_t hi = bits[w] & ((1u << (q & 31)) - 1u);
-    return hi ? (w << 5) + 31 - __clz(hi) : max((w << 5) - 1 - __clz(lo), -1);  // lo = 0 only when w = 0
+    // branch-free over the 64-bit window: clz(hi:lo) picks hi's top bit, else lo's (lo = 0 only
+    // when w = 0, where the max gives -1)
+    const unsigned long long x = (unsigned long long)hi << 32 | lo;
+    return max((w << 5) + 31 - __clzll(x), -1);
 }
 // first set bit at or after q (bit n-1 is always set; the word after the last one is never the
 // answer, so reading past it is harmless)
@@ -354,6 +357,9 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
 #ifndef SLO_RND_ROWS_WIDE
 #define SLO_RND_ROWS_WIDE 16
 #endif
+#ifndef SLO_RND_STRIDE1
+#define SLO_RND_STRIDE1 28  // 7 x 16 B: odd in 16-byte units, so the row stores stay conflict-free
+#endif
 #ifndef SLO_RND_STRIDE_WIDE
 #define SLO_RND_STRIDE_WIDE 32
 #endif
@@ -361,11 +367,11 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
 template <int UPL>
 __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : SLO_RND_ROWS_WIDE; }
 
-// row stride (words): 36 = 9 x 16 B puts the 32 lanes' row stores on distinct bank groups
-// (conflict-free uint4 stores); where shared memory bounds the resident warps (2-4 units per
-// lane) the dense stride keeps one more warp per SM
+// row stride (words): a row is 28 words (7 Philox blocks); an odd number of 16-byte units puts
+// the lanes' row stores on distinct bank groups (conflict-free uint4 stores); where shared memory
+// bounds the resident warps (2-4 units per lane) the dense stride keeps one more warp per SM
 template <int UPL>
-__host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? 36 : SLO_RND_STRIDE_WIDE; }
+__host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? SLO_RND_STRIDE1 : SLO_RND_STRIDE_WIDE; }
 
 // units at the head of the schedule whose per-position slacks are cached (UPL 1): the live
 // prefix at the bench shape is two to four units
@@ -377,9 +383,9 @@ template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
     // entries + a zero word (bits[-1]) and padding + batch-end bitmask + two move-flag bitmasks +
     // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + (UPL 1)
-    // the slack cache of the first kLiveCap units
+    // the slack and batch-start caches of the first kLiveCap units
     return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4 +
-           (UPL == 1 ? kLiveCap * 32 * 4 : 0) + 4 * kSwapRecWords * 4;
+           (UPL == 1 ? 2 * kLiveCap * 32 * 4 : 0) + 4 * kSwapRecWords * 4;
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -645,7 +651,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
         off = ((size_t)total * sizeof(uint32_t) + 15) & ~(size_t)15;
     }
     constexpr int kEnt = 1024 * UPL, kBits = 32 * UPL;
-    unsigned char* slot = smem + off + (size_t)wid * slot_bytes<UPL>();
+    // the slot's shared address is pinned in a register: otherwise the compiler, short of registers,
+    // re-derives it (S2R CgaCtaId, LEA, IMAD by the slot size...) before most shared accesses
+    uint32_t slot_s = (uint32_t)__cvta_generic_to_shared(smem + off + (size_t)wid * slot_bytes<UPL>());
+    if constexpr (UPL == 1) asm volatile("" : "+r"(slot_s));  // (UPL 2/4: measured slower pinned)
+    unsigned char* slot = reinterpret_cast<unsigned char*>(__cvta_shared_to_generic(slot_s));
     uint16_t* ent = reinterpret_cast<uint16_t*>(slot);
     uint32_t* bits = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16);
     uint32_t* sqb = bits + kBits;  // move flags (state: copied and parked with the bitmask)
@@ -659,7 +669,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     // per group of the current speculative pass: its swap decoded and scored (pa|pb, sa|sb, ea|eb,
     // na|nb, old entries, new makespans, makespan deltas, total delta, +inf delta), so a swap
     // that goes on to the general path is not decoded and gathered twice
-    uint32_t* prec = reinterpret_cast<uint32_t*>(sig + (UPL == 1 ? kLiveCap * 32 : 0));
+    // bst[q] (UPL 1, same positions): batch start of position q minus its unit's anchor E, in the
+    // committed state (the speculative stage's live-region bound reads it)
+    uint32_t* bst = reinterpret_cast<uint32_t*>(sig + (UPL == 1 ? kLiveCap * 32 : 0));
+    uint32_t* prec = bst + (UPL == 1 ? kLiveCap * 32 : 0);
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
     if (threadIdx.x == 0) s_xr = ExactRef{p.tab64, p.exact_count};
@@ -758,6 +771,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         }
                         const long long sl = D - (Eu + (long long)(sc - vv));
                         sig[q] = fin ? (int)max(min(sl, (long long)INT_MAX), (long long)INT_MIN + 1) : INT_MIN;
+                        bst[q] = sc - vv;
                     }
                     __syncwarp();
                 }
@@ -871,13 +885,51 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             if (sa == sb) dtot = 0, dA = 0;
                             const bool elig = g < G && n >= 2 && opw == 2u && (pa >> 5) >= u_live &&
                                               e_dead + (long long)min(0, min(da, da + db)) > dg;
-                            const double f_g = objective_fast(nm_cur + dA, (double)(tot + dtot) * p.tick);
-                            bool acc = f_g > f;
-                            if (!acc) {
-                                const float x = (float)((f - f_g) * sinv);
-                                const float u = (float)(rg[kAccWord] >> 8) * 0x1.0p-24f;
-                                acc = u < __expf(-x);
+                            int n_g = nm_cur + dA;
+                            // Live-region bound (UPL 1): a swap whose makespan changes shift no batch
+                            // earlier (da >= 0, da + db >= 0) leaves every other position's request,
+                            // table row and deadline in place and its batch start equal or later, so
+                            // none of them can gain an SLO: n_met <= nm_cur + the two moved requests'
+                            // change, decided from the cached batch starts (bst) and slacks (sig).
+                            // A proposal the Metropolis test rejects even at that bound is rejected
+                            // by the exact score too (the test is monotone in n_met; x >= 17 with a
+                            // nonzero uniform keeps __expf's rounding out of the decision).
+                            bool bnd = false;
+#ifndef SLO_NO_LIVE_BOUND
+                            if constexpr (UPL == 1) {
+                                const int nc = min(u_live, kLiveCap);
+                                const int ua = pa >> 5, ub = pb >> 5;
+                                const bool mine = act && (q == pa || q == pb);
+                                const bool live_q = (q >> 5) < nc;
+                                const long long Eq = __shfl_sync(FULL, cur.E[0], (q >> 5) & 31);
+                                bool m_old = (vo & kAlways) != 0u, m_new = (vn & kAlways) != 0u, amb = false;
+                                if (mine && live_q) {
+                                    const uint32_t mq = (uint32_t)cert_margin(q);
+                                    if (!m_old) {
+                                        const int sg = sig[q];
+                                        m_old = sg != INT_MIN && sg >= 0;
+                                        amb = sg != INT_MIN && (uint32_t)sg + mq <= 2u * mq;
+                                    }
+                                    if (!m_new) {
+                                        const long long D = __ldg(p.dt + en);
+                                        const long long sl = D - (Eq + (long long)bst[q] + (q == pb ? (long long)da : 0ll));
+                                        m_new = D >= 0 && sl >= 0;
+                                        amb = amb || (D >= 0 && (unsigned long long)(sl + mq) <= 2ull * mq);
+                                    }
+                                }
+                                const int up = __popc(__ballot_sync(FULL, mine && m_new) & gmask) -
+                                               __popc(__ballot_sync(FULL, mine && m_old) & gmask);
+                                const bool amb_g = (__ballot_sync(FULL, amb) & gmask) != 0u;
+                                bnd = !elig && g < G && n >= 2 && opw == 2u && sa != sb && da >= 0 && da + db >= 0 &&
+                                      ua < nc && (ub < nc || ub >= u_live) && !amb_g;
+                                if (bnd) n_g = nm_cur + up;
                             }
+#endif
+                            const double f_g = objective_fast(n_g, (double)(tot + dtot) * p.tick);
+                            const float x_g = (float)((f - f_g) * sinv);
+                            const uint32_t uw = rg[kAccWord] >> 8;
+                            const bool acc = f_g > f || (float)uw * 0x1.0p-24f < __expf(-x_g);
+                            const bool rej = (elig && !acc) || (bnd && !acc && x_g >= 17.0f && uw != 0u);
                             __syncwarp();  // the general path is done reading the previous pass's records
                             if (sub == 0) {
                                 uint4* rec = reinterpret_cast<uint4*>(prec + kSwapRecWords * g);
@@ -888,7 +940,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                                     (uint32_t)((unsigned long long)dtot >> 32), (uint32_t)dA);
                             }
                             // rejected groups as bits 0-3; positions scanned per group as nibbles
-                            const unsigned rj = __ballot_sync(FULL, sub == 0 && elig && !acc);
+                            const unsigned rj = __ballot_sync(FULL, sub == 0 && rej);
                             lead_c = (rj & 1u) | ((rj >> 7) & 2u) | ((rj >> 14) & 4u) | ((rj >> 21) & 8u);
                             span_c = __reduce_add_sync(FULL, sub == 0 ? (unsigned)(ea - sa + eb - sb + 2) << (4 * g) : 0u);
                             pass_it0 = it, pass_end = it + G;
