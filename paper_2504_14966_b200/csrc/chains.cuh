@@ -373,19 +373,17 @@ __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : SLO_RND_RO
 template <int UPL>
 __host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? SLO_RND_STRIDE1 : SLO_RND_STRIDE_WIDE; }
 
-// units at the head of the schedule whose per-position slacks are cached (UPL 1): the live
-// prefix at the bench shape is two to four units
+// units at the head of the schedule whose per-position slacks and batch starts are cached: the
+// live prefix at the bench shape is two to four units
 constexpr int kLiveCap = 3;
-// words of a speculative pass's per-group swap record (the general path reads it back)
-constexpr int kSwapRecWords = 12;
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
     // entries + a zero word (bits[-1]) and padding + batch-end bitmask + two move-flag bitmasks +
-    // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + (UPL 1)
-    // the slack and batch-start caches of the first kLiveCap units
+    // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + the
+    // slack and batch-start caches of the first kLiveCap units and their anchors
     return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4 +
-           (UPL == 1 ? 2 * kLiveCap * 32 * 4 : 0) + 4 * kSwapRecWords * 4;
+           2 * kLiveCap * 32 * 4 + 32;
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -661,18 +659,15 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     uint32_t* sqb = bits + kBits;  // move flags (state: copied and parked with the bitmask)
     uint32_t* dlb = bits + 2 * kBits;
     uint32_t* rnd = reinterpret_cast<uint32_t*>(slot + kEnt * 2 + 16 + 3 * kBits * 4);
-    // sig[q] (UPL 1, q < 32 * min(live units, kLiveCap)): deadline minus batch start of position q
-    // in the committed state, clamped to int32 (INT_MIN: +inf deadline or past the end). A unit
-    // whose contents and batch structure are unchanged and whose anchor moves by d meets
-    // exactly #{q : sig[q] >= d} finite-deadline SLOs (|d| < 2^28), so its walk is a ballot.
+    // sig[q] (q < 32 * min(live units, kLiveCap)): deadline minus batch start of position q in the
+    // committed state, clamped to int32 (INT_MIN: +inf deadline or past the end). A unit whose
+    // contents and batch structure are unchanged and whose anchor moves by d meets exactly
+    // #{q : sig[q] >= d} finite-deadline SLOs (|d| < 2^28), so its walk is a ballot (UPL 1).
     int* sig = reinterpret_cast<int*>(rnd + rnd_rows<UPL>() * rnd_stride<UPL>());
-    // per group of the current speculative pass: its swap decoded and scored (pa|pb, sa|sb, ea|eb,
-    // na|nb, old entries, new makespans, makespan deltas, total delta, +inf delta), so a swap
-    // that goes on to the general path is not decoded and gathered twice
-    // bst[q] (UPL 1, same positions): batch start of position q minus its unit's anchor E, in the
-    // committed state (the speculative stage's live-region bound reads it)
-    uint32_t* bst = reinterpret_cast<uint32_t*>(sig + (UPL == 1 ? kLiveCap * 32 : 0));
-    uint32_t* prec = bst + (UPL == 1 ? kLiveCap * 32 : 0);
+    // bst[q] (same positions): batch start of position q minus its unit's anchor cE[q >> 5], in the
+    // committed state (the speculative stage's live-region bound reads both)
+    uint32_t* bst = reinterpret_cast<uint32_t*>(sig + kLiveCap * 32);
+    long long* cE = reinterpret_cast<long long*>(bst + kLiveCap * 32);
     constexpr int kRows = rnd_rows<UPL>();
     if (lane == 0) bits[-1] = 0u;  // prev_end16 reads it for positions < 32 (never written again)
     if (threadIdx.x == 0) s_xr = ExactRef{p.tab64, p.exact_count};
@@ -743,46 +738,50 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 e_dead = cnt < 32 * UPL ? __shfl_sync(FULL, ed, (cnt / UPL) & 31) : kPadE;
             };
             auto refresh_sig = [&]() {
-                if constexpr (UPL == 1) {
-                    __syncwarp();
-                    const int nu = min(u_live, kLiveCap);
-                    for (int u = 0; u < nu; ++u) {
-                        const long long Eu = __shfl_sync(FULL, cur.E[0], u);
-                        const uint32_t Fu = __shfl_sync(FULL, cur.F[0], u);
-                        const int q = (u << 5) + lane;
-                        const uint32_t w = bits[u];
-                        uint32_t x = 0;
-                        long long D = 0;
-                        bool fin = false;
-                        if (q < n) {
-                            const uint32_t e = ent[q];
-                            const uint32_t v = xt_ld<SMEM>(tab, e);
-                            x = mkspan<NEG>(v & kTickMask, p.cofs);
-                            if (!(v & kAlways)) D = __ldg(p.dt + e), fin = D >= 0;
-                        }
-                        const uint32_t m = seg_max(x, w, lane, mb);
-                        const int f0 = w ? __ffs(w) - 1 : 32;
-                        const uint32_t vv = ((w >> lane) & 1u) ? (lane == f0 ? Fu : m) : 0u;
-                        uint32_t sc = vv;
+                __syncwarp();
+                const int nu = min(u_live, kLiveCap);
+                for (int u = 0; u < nu; ++u) {  // unit u: register u % UPL of lane u / UPL
+                    long long Es = cur.E[0];
+                    uint32_t Fs_ = cur.F[0];
 #pragma unroll
-                        for (int d = 1; d < 32; d <<= 1) {
-                            const uint32_t up = __shfl_up_sync(FULL, sc, d);
-                            if (lane >= d) sc += up;
-                        }
-                        const long long sl = D - (Eu + (long long)(sc - vv));
-                        sig[q] = fin ? (int)max(min(sl, (long long)INT_MAX), (long long)INT_MIN + 1) : INT_MIN;
-                        bst[q] = sc - vv;
+                    for (int kk = 1; kk < UPL; ++kk)
+                        if (u % UPL == kk) Es = cur.E[kk], Fs_ = cur.F[kk];
+                    const long long Eu = __shfl_sync(FULL, Es, u / UPL);
+                    const uint32_t Fu = __shfl_sync(FULL, Fs_, u / UPL);
+                    const int q = (u << 5) + lane;
+                    const uint32_t w = bits[u];
+                    uint32_t x = 0;
+                    long long D = 0;
+                    bool fin = false;
+                    if (q < n) {
+                        const uint32_t e = ent[q];
+                        const uint32_t v = xt_ld<SMEM>(tab, e);
+                        x = mkspan<NEG>(v & kTickMask, p.cofs);
+                        if (!(v & kAlways)) D = __ldg(p.dt + e), fin = D >= 0;
                     }
-                    __syncwarp();
+                    const uint32_t m = seg_max(x, w, lane, mb);
+                    const int f0 = w ? __ffs(w) - 1 : 32;
+                    const uint32_t vv = ((w >> lane) & 1u) ? (lane == f0 ? Fu : m) : 0u;
+                    uint32_t sc = vv;
+#pragma unroll
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const uint32_t up = __shfl_up_sync(FULL, sc, d);
+                        if (lane >= d) sc += up;
+                    }
+                    const long long sl = D - (Eu + (long long)(sc - vv));
+                    sig[q] = fin ? (int)max(min(sl, (long long)INT_MAX), (long long)INT_MIN + 1) : INT_MIN;
+                    bst[q] = sc - vv;
+                    if (lane == 0) cE[u] = Eu;
                 }
+                __syncwarp();
             };
             refresh_live();
             refresh_sig();
 
             int next_check = 8;
             int pass_it0 = 0, pass_end = 0;  // the speculative pass covering proposals [pass_it0, pass_end)
-            unsigned lead_c = 0, span_c = 0;
-            uint32_t pk_c = kNoMove;  // lane 8g: the move of the pass's proposal g
+            unsigned lead_c = 0, span_c = 0;  // rejected proposals of the pass (bit j); lane j's scanned positions
+            uint32_t pk_c = kNoMove;          // lane j: the move of the pass's proposal j
             for (int it = 0; it < p.iter; ++it) {
                 if (it >= next_check) {
                     // the device budget is checked every 8 proposals (warp-uniform), so a launch
@@ -809,168 +808,148 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     __syncwarp();
                 }
                 {
-                    if (mb <= 4) {
-                        // Speculative rejection (exact): the next G <= 4 proposals are scored at
-                        // once against the current state, one per 8-lane group. A proposal whose
-                        // move (first valid attempt of 8, else the forced swap) is a swap in the
-                        // dead region -- every unit it
-                        // touches or shifts is dead and stays dead -- changes n_met only through
-                        // its +inf-deadline count, so its score needs no walk. While such
-                        // proposals are rejected the state does not change, so each was scored
-                        // against exactly the state the sequential chain would see: the leading
-                        // run of rejected ones is consumed here; the first other proposal (an
-                        // accept, a squeeze/delay, a live-region swap) goes through the general
-                        // path below with the same random words.
-                        if (it >= pass_end) {  // score a new pass of G proposals
-                            const int G = min(4, min(p.iter - it, kRows - (it & (kRows - 1))));
-                            const int g = lane >> 3, sub = lane & 7;
-                            const uint32_t* rg = rnd + rnd_stride<UPL>() * ((it + g) & (kRows - 1));
-                            const uint32_t first = __umulhi(ent[0], magic) + 1u;
-                            const uint32_t r0 = rg[3 * sub], r1 = rg[3 * sub + 1], r2 = rg[3 * sub + 2];
-                            const uint32_t op = lemire32(r0, 3);
-                            const uint32_t a = lemire32(r1, nn);
-                            const uint32_t ps = first + lemire32(r1, nn - first);
-                            uint32_t b = lemire32(r2, nn - 1);
-                            b += b >= a ? 1u : 0u;
-                            const uint32_t pos = op == 0 ? ps : a;
-                            const uint32_t qf = min(pos, nn - 1);
-                            const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
-                            const bool ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
-                            const unsigned gm = (__ballot_sync(FULL, ok) >> (8 * g)) & 0xffu;
-                            const int src = (g << 3) + (gm ? __ffs(gm) - 1 : 0);
-                            // no valid attempt among the 8: the reference's forced swap (attempt 8)
-                            const uint32_t a8 = lemire32(rg[3 * (kAttempts - 1) + 1], nn);
-                            uint32_t b8 = lemire32(rg[3 * (kAttempts - 1) + 2], nn - 1);
-                            b8 += b8 >= a8 ? 1u : 0u;
-                            const uint32_t ops = __shfl_sync(FULL, op, src);
-                            const uint32_t as = __shfl_sync(FULL, a, src), bs = __shfl_sync(FULL, b, src);
-                            const uint32_t opw = gm ? ops : 2u, aw = gm ? as : a8, bw = gm ? bs : b8;
-                            // the group's move packed as draw_move returns it (the general path reuses it)
-                            const uint32_t pks = __shfl_sync(FULL, op << 30 | pos | (op == 2u ? b << 13 : 0u), src);
-                            pk_c = gm ? pks : (n >= 2 ? (2u << 30 | a8 | b8 << 13) : kNoMove);
-                            const int pa = (int)min(aw, bw), pb = (int)max(aw, bw);
+                    // Speculative rejection (exact), one proposal per lane: lane j scores proposal
+                    // it + j (up to the end of the Philox block) against the current state. A
+                    // proposal whose move (first valid attempt of 8, else the forced swap) is a swap
+                    // that provably cannot raise the score enough to pass its Metropolis test is
+                    // rejected without touching the state:
+                    //   dead-region swaps -- every unit the swap touches or shifts is dead and stays
+                    //     dead: n_met changes only through the +inf-deadline count (exact score);
+                    //   live-region swaps whose makespan changes shift no batch earlier -- no other
+                    //     request can gain an SLO, so n_met <= nm_cur + the two moved requests'
+                    //     change (cached batch starts / slacks of the first kLiveCap units): the test
+                    //     is monotone in n_met, so a rejection at this bound is the exact decision
+                    //     (x >= 17 with a nonzero uniform keeps __expf's rounding out of it).
+                    // While proposals are rejected the state does not change, so each was scored
+                    // against exactly the state the sequential chain sees: the leading run of
+                    // rejected ones is consumed; the first other proposal goes through the general
+                    // path below with the same random words. A general-path rejection leaves the
+                    // state bit-identical, so the rest of the pass stays valid; an accept ends it.
+                    if (it >= pass_end) {
+                        const int G = min(kRows - (it & (kRows - 1)), p.iter - it);
+                        const bool on = lane < G;
+                        const uint32_t* rl = rnd + rnd_stride<UPL>() * ((it + lane) & (kRows - 1));
+                        const uint32_t first = __umulhi(ent[0], magic) + 1u;  // size of the first batch
+                        uint32_t pk = kNoMove;
+                        if (on && n >= 2) {
+                            // the reference's proposal discipline (P:src/priority_mapper.cpp:184-198)
+                            for (int j = 0; j < kAttempts - 1; ++j) {
+                                const uint32_t r0 = rl[3 * j], r1 = rl[3 * j + 1], r2 = rl[3 * j + 2];
+                                const uint32_t op = lemire32(r0, 3);
+                                const uint32_t a = lemire32(r1, nn);
+                                const uint32_t ps = first + lemire32(r1, nn - first);
+                                uint32_t b = lemire32(r2, nn - 1);
+                                b += b >= a ? 1u : 0u;
+                                const uint32_t pos = op == 0 ? ps : a;
+                                const uint32_t qf = min(pos, nn - 1);
+                                const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
+                                if (op == 2u || (!fails && (op == 1u || first < nn))) {
+                                    pk = op << 30 | pos | (op == 2u ? b << 13 : 0u);
+                                    break;
+                                }
+                            }
+                            if (pk == kNoMove) {  // the forced swap (attempt 8)
+                                const uint32_t a8 = lemire32(rl[3 * (kAttempts - 1) + 1], nn);
+                                uint32_t b8 = lemire32(rl[3 * (kAttempts - 1) + 2], nn - 1);
+                                b8 += b8 >= a8 ? 1u : 0u;
+                                pk = 2u << 30 | a8 | b8 << 13;
+                            }
+                        }
+                        bool rej = false;
+                        unsigned span = 0;
+                        if (on && (pk >> 30) == 2u) {
+                            const int a0 = (int)(pk & 0x1fffu), b0 = (int)((pk >> 13) & 0x1fffu);
+                            const int pa = min(a0, b0), pb = max(a0, b0);
                             const uint32_t ea_ = ent[pa], eb_ = ent[pb];
-                            const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);
+                            const uint32_t za = __umulhi(ea_, magic), zb = __umulhi(eb_, magic);  // size - 1
                             const uint32_t ba = za * nn, bb = zb * nn;
                             const uint32_t na = ba + (eb_ - bb), nb = bb + (ea_ - ba);
                             const int sa = prev_end16(bits, pa) + 1, sb = prev_end16(bits, pb) + 1;
-                            const int ea = sa + (int)za, eb = sb + (int)zb;
-                            const bool firsth = sub < 4;
-                            const int q = firsth ? sa + sub : sb + sub - 4;
-                            const bool act = q <= (firsth ? ea : eb);
-                            uint32_t eo = 0, en = 0;
-                            if (act) {
-                                eo = ent[q];
-                                en = q == pa ? na : (q == pb ? nb : eo);
-                            }
-                            const uint32_t vo = act ? xt_ld<SMEM>(tab, eo) : 0u;
-                            const uint32_t vn = act ? xt_ld<SMEM>(tab, en) : 0u;
-                            const uint32_t xo = vo & kTickMask, xn = vn & kTickMask;
-                            // per-batch maxima over 4-lane halves, the exec delta over the 8 lanes
-                            uint32_t mo = max(xo, __shfl_xor_sync(FULL, xo, 1));
-                            uint32_t mn = max(xn, __shfl_xor_sync(FULL, xn, 1));
-                            mo = mkspan<NEG>(max(mo, __shfl_xor_sync(FULL, mo, 2)), p.cofs);
-                            mn = mkspan<NEG>(max(mn, __shfl_xor_sync(FULL, mn, 2)), p.cofs);
-                            const uint32_t mo_x = __shfl_xor_sync(FULL, mo, 4), mn_x = __shfl_xor_sync(FULL, mn, 4);
-                            int dx = (int)xn - (int)xo;
-                            dx += __shfl_xor_sync(FULL, dx, 1);
-                            dx += __shfl_xor_sync(FULL, dx, 2);
-                            dx += __shfl_xor_sync(FULL, dx, 4);
-                            const unsigned gmask = 0xffu << (8 * g);
-                            int dA = __popc(__ballot_sync(FULL, (vn & kAlways) != 0u) & gmask) -
-                                     __popc(__ballot_sync(FULL, (vo & kAlways) != 0u) & gmask);
-                            const int da = (int)(firsth ? mn : mn_x) - (int)(firsth ? mo : mo_x);
-                            const int db = (int)(firsth ? mn_x : mn) - (int)(firsth ? mo_x : mo);
-                            long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
-                            if (sa == sb) dtot = 0, dA = 0;
-                            const bool elig = g < G && n >= 2 && opw == 2u && (pa >> 5) >= u_live &&
-                                              e_dead + (long long)min(0, min(da, da + db)) > dg;
-                            int n_g = nm_cur + dA;
-                            // Live-region bound (UPL 1): a swap whose makespan changes shift no batch
-                            // earlier (da >= 0, da + db >= 0) leaves every other position's request,
-                            // table row and deadline in place and its batch start equal or later, so
-                            // none of them can gain an SLO: n_met <= nm_cur + the two moved requests'
-                            // change, decided from the cached batch starts (bst) and slacks (sig).
-                            // A proposal the Metropolis test rejects even at that bound is rejected
-                            // by the exact score too (the test is monotone in n_met; x >= 17 with a
-                            // nonzero uniform keeps __expf's rounding out of the decision).
-                            bool bnd = false;
-#ifndef SLO_NO_LIVE_BOUND
-                            if constexpr (UPL == 1) {
-                                const int nc = min(u_live, kLiveCap);
-                                const int ua = pa >> 5, ub = pb >> 5;
-                                const bool mine = act && (q == pa || q == pb);
-                                const bool live_q = (q >> 5) < nc;
-                                const long long Eq = __shfl_sync(FULL, cur.E[0], (q >> 5) & 31);
-                                bool m_old = (vo & kAlways) != 0u, m_new = (vn & kAlways) != 0u, amb = false;
-                                if (mine && live_q) {
-                                    const uint32_t mq = (uint32_t)cert_margin(q);
-                                    if (!m_old) {
-                                        const int sg = sig[q];
-                                        m_old = sg != INT_MIN && sg >= 0;
-                                        amb = sg != INT_MIN && (uint32_t)sg + mq <= 2u * mq;
-                                    }
-                                    if (!m_new) {
-                                        const long long D = __ldg(p.dt + en);
-                                        const long long sl = D - (Eq + (long long)bst[q] + (q == pb ? (long long)da : 0ll));
-                                        m_new = D >= 0 && sl >= 0;
-                                        amb = amb || (D >= 0 && (unsigned long long)(sl + mq) <= 2ull * mq);
-                                    }
+                            // same batch: nothing changes, the reference accepts (x = 0): general path
+                            if (sa != sb) {
+                                const int ea = sa + (int)za, eb = sb + (int)zb;
+                                // the two batches' makespans, and the maxima without the swapped positions
+                                uint32_t moa = 0, mxa = 0, mob = 0, mxb = 0;
+                                for (int qq = sa; qq <= ea; ++qq) {
+                                    const uint32_t x = xt_ld<SMEM>(tab, ent[qq]) & kTickMask;
+                                    moa = max(moa, x);
+                                    if (qq != pa) mxa = max(mxa, x);
                                 }
-                                const int up = __popc(__ballot_sync(FULL, mine && m_new) & gmask) -
-                                               __popc(__ballot_sync(FULL, mine && m_old) & gmask);
-                                const bool amb_g = (__ballot_sync(FULL, amb) & gmask) != 0u;
-                                bnd = !elig && g < G && n >= 2 && opw == 2u && sa != sb && da >= 0 && da + db >= 0 &&
-                                      ua < nc && (ub < nc || ub >= u_live) && !amb_g;
-                                if (bnd) n_g = nm_cur + up;
+                                for (int qq = sb; qq <= eb; ++qq) {
+                                    const uint32_t x = xt_ld<SMEM>(tab, ent[qq]) & kTickMask;
+                                    mob = max(mob, x);
+                                    if (qq != pb) mxb = max(mxb, x);
+                                }
+                                const uint32_t voa = xt_ld<SMEM>(tab, ea_), vob = xt_ld<SMEM>(tab, eb_);
+                                const uint32_t vna = xt_ld<SMEM>(tab, na), vnb = xt_ld<SMEM>(tab, nb);
+                                const int da = (int)mkspan<NEG>(max(mxa, vna & kTickMask), p.cofs) -
+                                               (int)mkspan<NEG>(moa, p.cofs);
+                                const int db = (int)mkspan<NEG>(max(mxb, vnb & kTickMask), p.cofs) -
+                                               (int)mkspan<NEG>(mob, p.cofs);
+                                const int dx = (int)(vna & kTickMask) + (int)(vnb & kTickMask) - (int)(voa & kTickMask) -
+                                               (int)(vob & kTickMask);
+                                const long long dtot = (long long)dx + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
+                                const int dA = (int)(vna >> 31) + (int)(vnb >> 31) - (int)(voa >> 31) - (int)(vob >> 31);
+                                const bool dead = (pa >> 5) >= u_live && e_dead + (long long)min(0, min(da, da + db)) > dg;
+                                int n_g = nm_cur + dA;
+                                bool bnd = false;
+                                const int nc = min(u_live, kLiveCap), ua = pa >> 5, ub = pb >> 5;
+                                if (!dead && da >= 0 && da + db >= 0 && ua < nc && (ub < nc || ub >= u_live)) {
+                                    // the moved requests' SLO tests before and after, certified on the grid
+                                    bool amb = false;
+                                    auto met_old = [&](int q, uint32_t v) {
+                                        if (v & kAlways) return 1;
+                                        const int sg = sig[q];
+                                        const uint32_t mq = (uint32_t)cert_margin(q);
+                                        amb = amb || (sg != INT_MIN && (uint32_t)sg + mq <= 2u * mq);
+                                        return sg != INT_MIN && sg >= 0 ? 1 : 0;
+                                    };
+                                    auto met_new = [&](int q, uint32_t v, uint32_t e, long long shift) {
+                                        if (v & kAlways) return 1;
+                                        const long long D = __ldg(p.dt + e);
+                                        const long long sl = D - (cE[q >> 5] + (long long)bst[q] + shift);
+                                        const uint32_t mq = (uint32_t)cert_margin(q);
+                                        amb = amb || (D >= 0 && (unsigned long long)(sl + mq) <= 2ull * mq);
+                                        return D >= 0 && sl >= 0 ? 1 : 0;
+                                    };
+                                    int up = met_new(pa, vna, na, 0) - met_old(pa, voa);
+                                    if (ub < nc) up += met_new(pb, vnb, nb, da) - met_old(pb, vob);
+                                    else up += (int)(vnb >> 31) - (int)(vob >> 31);  // dead region: only +inf deadlines
+                                    bnd = !amb;
+                                    n_g = nm_cur + up;
+                                }
+                                if (dead || bnd) {
+                                    const double f_g = objective_fast(n_g, (double)(tot + dtot) * p.tick);
+                                    const float x_g = (float)((f - f_g) * sinv);
+                                    const uint32_t uw = rl[kAccWord] >> 8;
+                                    const bool acc = f_g > f || (float)uw * 0x1.0p-24f < __expf(-x_g);
+                                    rej = !acc && (dead || (x_g >= 17.0f && uw != 0u));
+                                }
+                                span = (unsigned)(ea - sa + eb - sb + 2);
                             }
-#endif
-                            const double f_g = objective_fast(n_g, (double)(tot + dtot) * p.tick);
-                            const float x_g = (float)((f - f_g) * sinv);
-                            const uint32_t uw = rg[kAccWord] >> 8;
-                            const bool acc = f_g > f || (float)uw * 0x1.0p-24f < __expf(-x_g);
-                            const bool rej = (elig && !acc) || (bnd && !acc && x_g >= 17.0f && uw != 0u);
-                            __syncwarp();  // the general path is done reading the previous pass's records
-                            if (sub == 0) {
-                                uint4* rec = reinterpret_cast<uint4*>(prec + kSwapRecWords * g);
-                                rec[0] = make_uint4((uint32_t)pa | (uint32_t)pb << 16, (uint32_t)sa | (uint32_t)sb << 16,
-                                                    (uint32_t)ea | (uint32_t)eb << 16, na | nb << 16);
-                                rec[1] = make_uint4(ea_ | eb_ << 16, mn, mn_x, (uint32_t)da);
-                                rec[2] = make_uint4((uint32_t)db, (uint32_t)(unsigned long long)dtot,
-                                                    (uint32_t)((unsigned long long)dtot >> 32), (uint32_t)dA);
-                            }
-                            // rejected groups as bits 0-3; positions scanned per group as nibbles
-                            const unsigned rj = __ballot_sync(FULL, sub == 0 && rej);
-                            lead_c = (rj & 1u) | ((rj >> 7) & 2u) | ((rj >> 14) & 4u) | ((rj >> 21) & 8u);
-                            span_c = __reduce_add_sync(FULL, sub == 0 ? (unsigned)(ea - sa + eb - sb + 2) << (4 * g) : 0u);
-                            pass_it0 = it, pass_end = it + G;
                         }
-                        // consume the leading rejected run from proposal it; a pass stays valid
-                        // across general-path rejections (the state is unchanged by them)
-                        const int g0 = it - pass_it0, G = pass_end - pass_it0;
-                        // k = the run of rejected groups from g0 (trailing ones), sk their scan nibbles
-                        const int k = min(__ffs(~(lead_c >> g0)) - 1, G - g0);
-                        unsigned sk = (span_c >> (4 * g0)) & ((1u << (4 * k)) - 1u);
-                        sk = (sk & 0x0f0fu) + ((sk >> 4) & 0x0f0fu);
-                        sk = (sk & 0xffu) + (sk >> 8);
-                        props += (unsigned)k;
+                        lead_c = __ballot_sync(FULL, rej);
+                        span_c = span, pk_c = pk;
+                        pass_it0 = it, pass_end = it + G;
+                    }
+                    // consume the leading rejected run from proposal it
+                    const int g0 = it - pass_it0, G = pass_end - pass_it0;
+                    const int k = min(__ffsll(~(unsigned long long)(lead_c >> g0)) - 1, G - g0);
 #ifndef SLO_DIAG
-                        sc1 += sk;
+                    sc1 += __reduce_add_sync(FULL, lane >= g0 && lane < g0 + k ? span_c : 0u);
 #endif
+                    props += (unsigned)k;
 #ifdef SLO_SPEC_COUNT
-                        sc2 += (unsigned)k << 16;  // diagnostics: proposals consumed by this stage
+                    sc2 += (unsigned)k << 16;  // diagnostics: proposals consumed by this stage
 #endif
-                        it += k;
-                        __syncwarp();
-                        if (it == pass_end) {
-                            --it;  // the loop increment moves on to the next unconsumed proposal
-                            continue;
-                        }
+                    it += k;
+                    if (it == pass_end) {
+                        --it;  // the loop increment moves on to the next unconsumed proposal
+                        continue;
                     }
                 }
                 const uint32_t* rw = rnd + rnd_stride<UPL>() * (it & (kRows - 1));
-                const uint32_t pk = mb <= 4 ? __shfl_sync(FULL, pk_c, (it - pass_it0) << 3)
-                                            : draw_move(ent, sqb, dlb, n, magic, rw, lane);
+                const uint32_t pk = __shfl_sync(FULL, pk_c, it - pass_it0);  // the pass decoded it
                 const uint32_t op = pk >> 30;
                 const int kind = op == 3u ? 0 : (op == 2u ? 2 : 1);
 #ifdef SLO_DIAG
@@ -1090,18 +1069,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     // sizes; lanes 0-15 cover the first, 16-31 the second
                     int pa, pb, sa, sb, ea, eb, da, db;
                     uint32_t na, nb, mN0, mN1;
-                    if (mb <= 4) {  // the speculative pass decoded and scored this swap already
-                        const uint4* rec = reinterpret_cast<const uint4*>(prec + kSwapRecWords * (it - pass_it0));
-                        const uint4 r0 = rec[0], r1 = rec[1], r2 = rec[2];
-                        pa = (int)(r0.x & 0xffffu), pb = (int)(r0.x >> 16);
-                        sa = (int)(r0.y & 0xffffu), sb = (int)(r0.y >> 16);
-                        ea = (int)(r0.z & 0xffffu), eb = (int)(r0.z >> 16);
-                        na = r0.w & 0xffffu, nb = r0.w >> 16;
-                        ow0 = r1.x & 0xffffu, ow1 = r1.x >> 16;
-                        mN0 = r1.y, mN1 = r1.z, da = (int)r1.w, db = (int)r2.x;
-                        dtot = (long long)((unsigned long long)r2.y | (unsigned long long)r2.z << 32);
-                        dA = (int)r2.w;
-                    } else {
+                    {
                         const int sa0 = (int)(pk & 0x1fffu), sb0 = (int)((pk >> 13) & 0x1fffu);
                         pa = min(sa0, sb0), pb = max(sa0, sb0);
                         const uint32_t ea_ = ent[pa], eb_ = ent[pb];
