@@ -354,18 +354,21 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
     return tot > 0.0 ? (double)nm * r : 0.0;
 }
 
-#ifndef SLO_RND_ROWS_WIDE
-#define SLO_RND_ROWS_WIDE 16
+#ifndef SLO_RND_ROWS2
+#define SLO_RND_ROWS2 32
+#endif
+#ifndef SLO_RND_ROWS4
+#define SLO_RND_ROWS4 16
 #endif
 #ifndef SLO_RND_STRIDE1
 #define SLO_RND_STRIDE1 28  // 7 x 16 B: odd in 16-byte units, so the row stores stay conflict-free
 #endif
 #ifndef SLO_RND_STRIDE_WIDE
-#define SLO_RND_STRIDE_WIDE 32
+#define SLO_RND_STRIDE_WIDE 28
 #endif
 // Philox rows drawn per refill (one per lane): 32 proposals, 16 where shared memory is tight
 template <int UPL>
-__host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : SLO_RND_ROWS_WIDE; }
+__host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : (UPL == 2 ? SLO_RND_ROWS2 : SLO_RND_ROWS4); }
 
 // row stride (words): a row is 28 words (7 Philox blocks); an odd number of 16-byte units puts
 // the lanes' row stores on distinct bank groups (conflict-free uint4 stores); where shared memory
@@ -375,7 +378,14 @@ __host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? SLO_RND_STRID
 
 // units at the head of the schedule whose per-position slacks and batch starts are cached: the
 // live prefix at the bench shape is two to four units
-constexpr int kLiveCap = 3;
+#ifndef SLO_LIVE_CAP2
+#define SLO_LIVE_CAP2 6
+#endif
+#ifndef SLO_LIVE_CAP4
+#define SLO_LIVE_CAP4 10
+#endif
+template <int UPL>
+__host__ __device__ constexpr int live_cap() { return UPL == 1 ? 3 : (UPL == 2 ? SLO_LIVE_CAP2 : SLO_LIVE_CAP4); }
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {
@@ -383,7 +393,7 @@ __host__ __device__ constexpr int slot_bytes() {
     // Philox rows (next_end16 may read one word past the bitmask: the first flag word) + the
     // slack and batch-start caches of the first kLiveCap units and their anchors
     return 1024 * UPL * 2 + 16 + 3 * 32 * UPL * 4 + rnd_rows<UPL>() * rnd_stride<UPL>() * 4 +
-           2 * kLiveCap * 32 * 4 + 32;
+           ((2 * live_cap<UPL>() * 32 * 4 + 8 * live_cap<UPL>() + 15) & ~15);  // (slots stay 16-byte aligned)
 }
 
 // entries + BW words of bitmasks (the batch ends; with 3 * 32 * UPL also the move flags)
@@ -666,6 +676,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
     int* sig = reinterpret_cast<int*>(rnd + rnd_rows<UPL>() * rnd_stride<UPL>());
     // bst[q] (same positions): batch start of position q minus its unit's anchor cE[q >> 5], in the
     // committed state (the speculative stage's live-region bound reads both)
+    constexpr int kLiveCap = live_cap<UPL>();
     uint32_t* bst = reinterpret_cast<uint32_t*>(sig + kLiveCap * 32);
     long long* cE = reinterpret_cast<long long*>(bst + kLiveCap * 32);
     constexpr int kRows = rnd_rows<UPL>();
@@ -869,16 +880,19 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             if (sa != sb) {
                                 const int ea = sa + (int)za, eb = sb + (int)zb;
                                 // the two batches' makespans, and the maxima without the swapped positions
+                                // (4 positions per trip, predicated: the gathers of a trip issue back to back)
                                 uint32_t moa = 0, mxa = 0, mob = 0, mxb = 0;
-                                for (int qq = sa; qq <= ea; ++qq) {
-                                    const uint32_t x = xt_ld<SMEM>(tab, ent[qq]) & kTickMask;
-                                    moa = max(moa, x);
-                                    if (qq != pa) mxa = max(mxa, x);
-                                }
-                                for (int qq = sb; qq <= eb; ++qq) {
-                                    const uint32_t x = xt_ld<SMEM>(tab, ent[qq]) & kTickMask;
-                                    mob = max(mob, x);
-                                    if (qq != pb) mxb = max(mxb, x);
+                                for (int q0 = 0; q0 <= (int)max(za, zb); q0 += 4) {
+#pragma unroll
+                                    for (int j = 0; j < 4; ++j) {
+                                        const int qa = sa + q0 + j, qb = sb + q0 + j;
+                                        const bool ina = q0 + j <= (int)za, inb = q0 + j <= (int)zb;
+                                        const uint32_t xa = ina ? xt_ld<SMEM>(tab, ent[qa]) & kTickMask : 0u;
+                                        const uint32_t xb = inb ? xt_ld<SMEM>(tab, ent[qb]) & kTickMask : 0u;
+                                        moa = max(moa, xa), mob = max(mob, xb);
+                                        if (qa != pa) mxa = max(mxa, xa);
+                                        if (qb != pb) mxb = max(mxb, xb);
+                                    }
                                 }
                                 const uint32_t voa = xt_ld<SMEM>(tab, ea_), vob = xt_ld<SMEM>(tab, eb_);
                                 const uint32_t vna = xt_ld<SMEM>(tab, na), vnb = xt_ld<SMEM>(tab, nb);
