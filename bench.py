@@ -53,7 +53,7 @@ def parse():
     ap.add_argument("--t0", type=float, default=500.0)
     ap.add_argument("--t-thres", type=float, default=20.0)
     ap.add_argument("--tau", type=float, default=0.7)
-    ap.add_argument("--iter", type=int, default=300)  # the device budget, not the ladder, ends a decision
+    ap.add_argument("--iter", type=int, default=1000)  # the device budget, not the ladder, ends a decision
     ap.add_argument("--e2e-steps", type=int, default=20)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-sample-s", type=float, default=10.0)
