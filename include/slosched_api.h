@@ -112,6 +112,81 @@ int slosched_schedule_all(const slosched_workload* w, const double* coeffs8, int
 int slosched_build_tables(const slosched_workload* w, const double* coeffs8, const int32_t* ids, int32_t n,
                           int32_t max_batch, double* exec, double* deadline);
 
+/* ---------------------------------------------------------------- evaluation harness
+ * (include/slosched_b200.hpp "evaluation harness"; reference P:src/simulator.cpp:17-220,
+ *  P:src/output_estimator.cpp:10-78, P:tools/slosched.cpp:297-448) */
+typedef struct {
+    int32_t n;
+    const int32_t* id;
+    const double *total_mem, *remaining_mem, *mu, *sigma;
+    const int32_t* max_batch;
+} slosched_fleet;
+
+typedef struct {
+    double noise_pct, dispatch_gap_ms;
+    uint64_t seed;
+} slosched_sim_config;
+
+typedef struct {
+    int32_t request_id;
+    double wait_ms, exec_ms, e2e_ms, ttft_ms, tpot_ms;
+    int32_t slo_met, extrapolated;
+} slosched_record;
+
+typedef struct {
+    double slo_attainment, avg_latency_ms, g, scheduling_overhead_ms;
+    int32_t n_met;
+    double total_latency_ms;
+} slosched_report;
+
+typedef struct {
+    int32_t policy; /* 0 sa, 1 exhaustive, 2 fcfs (Policy) */
+    uint64_t seed;
+    int32_t n_requests, max_batch;
+    double attainment, avg_latency_ms, g_req_per_ms, overhead_ms;
+} slosched_row;
+
+/* run() P:src/simulator.cpp:49-74: per-instance schedules concatenated (inst_nb[i] batches each);
+ * records in the report's order (instance by instance). */
+int slosched_run(const slosched_workload* w, const double* coeffs8, const slosched_fleet* fleet, const int32_t* ids,
+                 const int32_t* sizes, const int32_t* inst_nb, const slosched_sim_config* sim, double overhead_ms,
+                 slosched_record* records, slosched_report* report);
+/* run_fcfs() P:src/simulator.cpp:76-123: the FCFS plans (per instance, concatenated) and the report. */
+int slosched_run_fcfs(const slosched_workload* w, const double* coeffs8, const slosched_fleet* fleet,
+                      const slosched_sim_config* sim, int32_t* out_ids, int32_t* out_sizes, int32_t* inst_nb,
+                      slosched_record* records, slosched_report* report);
+/* One instance clock of the replay (realize_batches): records appended in dispatch order. */
+int slosched_realize_batches(const slosched_workload* w, const double* coeffs8, const int32_t* ids,
+                             const int32_t* sizes, int32_t nb, double clock0, double first_gap, double gap,
+                             double until, double noise_pct, uint64_t seed, int32_t from_arrival,
+                             slosched_record* records, double* clock, int32_t* batches_started);
+/* Estimator P:src/output_estimator.cpp: classes with priors (kind 0 none, 1 Gaussian (a = mean,
+ * b = std), 2 range (a = low, b = high)); observe n_obs (class, length) pairs in order, then predict
+ * n_pred lengths with Rng(seed); the models' (count, mean, m2) after the observations. */
+int slosched_estimator(int32_t n_classes, const int32_t* class_id, const int32_t* prior_kind, const double* prior_a,
+                       const double* prior_b, int32_t n_obs, const int32_t* obs_cls, const int32_t* obs_len,
+                       int32_t n_pred, const int32_t* pred_cls, uint64_t seed, int32_t* pred_out,
+                       int64_t* model_count, double* model_mean, double* model_m2);
+/* compare() P:src/simulator.cpp:148-220: rows (n_pol x n_seeds, policy-major) and medians (n_pol). */
+int slosched_compare(const slosched_workload* w, const double* coeffs8, const slosched_fleet* fleet, int32_t n_pol,
+                     const int32_t* policies, int32_t n_seeds, const uint64_t* seeds, const slosched_anneal_config* cfg,
+                     const slosched_sim_config* sim, int32_t exhaustive_cap, slosched_row* rows, slosched_row* medians);
+/* sweep / perturb drivers (P:tools/slosched.cpp:335-448) over the CLI's synthetic workload per seed
+ * (generate_mixed(n, seed) + estimator priors when predict_mode = 1). sweep rows: (t0-major,
+ * iter, seed); perturb rows: (param-major, factor, seed). */
+int slosched_sweep(int32_t n_requests, int32_t predict_mode, int32_t n_seeds, const uint64_t* seeds,
+                   const slosched_fleet* fleet, const double* coeffs8, const slosched_anneal_config* cfg, int32_t n_t0,
+                   const double* t0_grid, int32_t n_iter, const int32_t* iter_grid, double* g_out);
+int slosched_perturb(int32_t n_requests, int32_t predict_mode, int32_t n_seeds, const uint64_t* seeds,
+                     const slosched_fleet* fleet, const double* truth8, const slosched_anneal_config* cfg,
+                     const slosched_sim_config* sim, int32_t n_params, const char* const* params, int32_t n_factors,
+                     const double* factors, double* g_out, double* baseline_out, double* degradation_out);
+/* n / t / g of n_sched schedules over the same requests (ids: n_sched x n; inst-style batch counts
+ * nb[s]; sizes concatenated) in one launch of the bit-exact evaluator (K1). */
+int slosched_evaluate_batch(const slosched_workload* w, const double* coeffs8, int32_t n_sched, int32_t n,
+                            const int32_t* ids, const int32_t* sizes, const int32_t* nb, int32_t max_batch,
+                            int32_t* n_met, double* t, double* g);
+
 #ifdef __cplusplus
 }
 #endif

@@ -306,6 +306,140 @@ struct ScheduleAllResult {
 ScheduleAllResult schedule_all(const Workload&, const std::vector<InstanceState>&, const LatencyCoefficients&,
                                const AnnealConfig&, Policy policy = Policy::SA, int exhaustive_cap = 10);
 
+// ---------------------------------------------------------------- output-length estimator
+// (P:include/slosched/output_estimator.hpp:10-56) Welford running Gaussian per task class; the
+// scheduler consumes its predictions as Request::predicted_output_len.
+constexpr int kDefaultOutputLen = 256;
+
+struct LengthModel {
+    int task_class_id = 0;
+    long long count = 0;
+    double mean = 0.0;
+    double m2 = 0.0;  // sum of squared deviations from the running mean
+    OutputPrior prior;
+    double sample_variance() const;
+    double sample_std() const;
+};
+void observe(LengthModel& model, int actual_len);
+int predict_len(const LengthModel& model, Rng& rng);
+int simulate_predictor_error(int true_len, double error_pct, Rng& rng);
+
+class Estimator {
+public:
+    explicit Estimator(const std::vector<TaskClass>& classes);
+    LengthModel& model_for(int task_class_id);
+    const std::vector<LengthModel>& models() const { return models_; }
+    void observe_output(int task_class_id, int actual_len);
+    int predict(int task_class_id, Rng& rng);
+
+private:
+    std::vector<LengthModel> models_;
+};
+void assign_predicted_lengths(std::vector<Request>& requests, Estimator& estimator, Rng& rng);
+
+// ---------------------------------------------------------------- evaluation harness
+// (P:include/slosched/core.hpp:139-150, P:include/slosched/simulator.hpp:13-72,
+//  P:tools/slosched.cpp:297-448) The realized-attainment replay, the FCFS baseline and the
+// compare / sweep / perturb drivers, with the annealing on the GPU (schedule_all) and the
+// sweep's scoring batched through the bit-exact evaluator (K1).
+struct MetricsReport {
+    double slo_attainment = 0.0;
+    double avg_latency_ms = 0.0;
+    double g = 0.0;
+    double scheduling_overhead_ms = 0.0;
+    std::vector<RequestMetrics> per_request;
+    int n_met = 0;
+    double total_latency_ms = 0.0;
+    static MetricsReport from_records(std::vector<RequestMetrics> records, double overhead_ms);
+};
+
+struct SimConfig {
+    double noise_pct = 0.0;        // uniform multiplicative execution noise
+    double dispatch_gap_ms = 0.1;  // interval between consecutive batch dispatches
+    std::uint64_t seed = 0;
+};
+
+MetricsReport run(const std::vector<Schedule>& schedules, const Workload& workload,
+                  const std::vector<InstanceState>& instances, const LatencyCoefficients& coeffs,
+                  const SimConfig& sim_cfg, double scheduling_overhead_ms = 0.0);
+
+struct FcfsResult {
+    MetricsReport report;
+    std::vector<Schedule> schedules;
+};
+FcfsResult run_fcfs(const Workload& workload, const std::vector<InstanceState>& instances,
+                    const LatencyCoefficients& coeffs, const SimConfig& sim_cfg);
+
+struct ComparisonRow {
+    std::string policy;
+    std::uint64_t seed = 0;
+    int n_requests = 0;
+    int max_batch = 0;
+    double attainment = 0.0;
+    double avg_latency_ms = 0.0;
+    double g_req_per_ms = 0.0;
+    double overhead_ms = 0.0;
+};
+struct ComparisonTable {
+    std::vector<ComparisonRow> rows;
+    std::vector<ComparisonRow> medians;
+};
+double median(std::vector<double> values);
+std::string policy_name(Policy p);
+Policy parse_policy(const std::string& name);
+ComparisonTable compare(const Workload& workload, const std::vector<InstanceState>& instances,
+                        const LatencyCoefficients& coeffs, const std::vector<Policy>& policies,
+                        const std::vector<std::uint64_t>& seeds, const AnnealConfig& anneal_cfg,
+                        const SimConfig& sim_cfg, int exhaustive_cap = 10);
+
+// One instance clock of the replay: batch 0 starts at clock0 + first_gap, batch j > 0 at the
+// previous batch's end + gap; no batch starts once the clock (before its gap) has reached `until`.
+// Records (wait = start - arrival when from_arrival, else start) are appended; returns the clock
+// and the number of batches started. run() is this from clock 0 with no first gap and no bound;
+// the online driver replays each window with it.
+struct ReplayResult {
+    double clock = 0.0;
+    int batches_started = 0;
+};
+ReplayResult realize_batches(const std::vector<Batch>& batches, const Workload& workload,
+                             const LatencyCoefficients& coeffs, double clock0, double first_gap, double gap,
+                             double until,
+                             double noise_pct, Rng& rng, std::vector<RequestMetrics>& records,
+                             bool from_arrival = false);
+
+// Engine extension: n / t / g of many schedules over the same request set in one launch of the
+// bit-exact evaluator (K1; == evaluate() bit for bit).
+struct ScheduleScore {
+    int n = 0;
+    double t_ms = 0.0, g = 0.0;
+};
+std::vector<ScheduleScore> evaluate_batch(const std::vector<Schedule>& schedules, const LatencyCoefficients& coeffs,
+                                          const Workload& workload, int max_batch, int device = -1);
+
+// sweep / perturb drivers (P:tools/slosched.cpp:335-448): one workload per seed. Every cell's
+// schedule_all runs concurrently on the GPU (a share of the SMs each; chain results do not depend
+// on the grid, so the rows equal one-after-another runs).
+struct SweepRow {
+    double t0 = 0.0;
+    int iter = 0;
+    std::uint64_t seed = 0;
+    double g_req_per_ms = 0.0;
+};
+std::vector<SweepRow> sweep(const std::vector<Workload>& per_seed, const std::vector<std::uint64_t>& seeds,
+                            const std::vector<InstanceState>& instances, const LatencyCoefficients& coeffs,
+                            const AnnealConfig& base_cfg, const std::vector<double>& t0_grid,
+                            const std::vector<int>& iter_grid);
+struct PerturbRow {
+    std::string param;
+    double factor = 1.0;
+    std::uint64_t seed = 0;
+    double g_req_per_ms = 0.0, baseline_g = 0.0, degradation_pct = 0.0;
+};
+std::vector<PerturbRow> perturb(const std::vector<Workload>& per_seed, const std::vector<std::uint64_t>& seeds,
+                                const std::vector<InstanceState>& instances, const LatencyCoefficients& truth,
+                                const AnnealConfig& base_cfg, const SimConfig& sim_cfg,
+                                const std::vector<std::string>& params, const std::vector<double>& factors);
+
 // ---------------------------------------------------------------- synthetic inputs
 struct LengthDists {
     double code_input_median = 300.0, code_input_sigma = 0.5;

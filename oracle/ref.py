@@ -209,4 +209,88 @@ def schedule_all(w: FlatWorkload, coeffs, instances, seed=0, **cfg):
     return out, epochs.value
 
 
+def _fleet(instances):
+    col = lambda key, f: f([inst[key] for inst in instances])  # noqa: E731
+    return (col("id", _i32), col("total_mem", _f64), col("remaining_mem", _f64), col("mu", _f64), col("sigma", _f64),
+            col("max_batch", _i32))
+
+
+def _fleet_args(fl):
+    iid, tm, rm, mu, sg, mb = fl
+    return (c_int(len(iid)), ptr(iid, c_int), ptr(tm, c_double), ptr(rm, c_double), ptr(mu, c_double),
+            ptr(sg, c_double), ptr(mb, c_int))
+
+
+def _unpack_records(rec, n):
+    r = rec[:8 * n].reshape(n, 8)
+    return [dict(request_id=int(x[0]), wait_ms=x[1], exec_ms=x[2], e2e_ms=x[3], ttft_ms=x[4], tpot_ms=x[5],
+                 slo_met=bool(x[6]), extrapolated=bool(x[7])) for x in r]
+
+
+def _unpack_report(rep):
+    return dict(slo_attainment=rep[0], avg_latency_ms=rep[1], g=rep[2], scheduling_overhead_ms=rep[3],
+                n_met=int(rep[4]), total_latency_ms=rep[5])
+
+
+def run(w: FlatWorkload, coeffs, instances, plans, noise=0.0, gap=0.1, seed=0, overhead=0.0):
+    """run() (P:src/simulator.cpp:49-74); plans: per instance a list of batches (request ids)."""
+    fl = _fleet(instances)
+    ids = _i32([i for p in plans for b in p for i in b] or [0])
+    sizes = _i32([len(b) for p in plans for b in p] or [0])
+    nb = _i32([len(p) for p in plans])
+    n = sum(len(b) for p in plans for b in p)
+    rec, rep = np.zeros(8 * max(n, 1)), np.zeros(6)
+    _check(lib().ref_run(*_wargs(w), ptr(_f64(coeffs), c_double), *_fleet_args(fl), ptr(ids, c_int),
+                         ptr(sizes, c_int), ptr(nb, c_int), c_double(noise), c_double(gap), c_uint64(seed),
+                         c_double(overhead), ptr(rec, c_double), ptr(rep, c_double)))
+    return _unpack_records(rec, n), _unpack_report(rep)
+
+
+def run_fcfs(w: FlatWorkload, coeffs, instances, noise=0.0, gap=0.1, seed=0):
+    fl = _fleet(instances)
+    n = w.n
+    oi, osz = np.zeros(max(n, 1), dtype=np.int32), np.zeros(max(n, 1), dtype=np.int32)
+    inb = np.zeros(len(instances), dtype=np.int32)
+    rec, rep = np.zeros(8 * max(n, 1)), np.zeros(6)
+    _check(lib().ref_run_fcfs(*_wargs(w), ptr(_f64(coeffs), c_double), *_fleet_args(fl), c_double(noise),
+                              c_double(gap), c_uint64(seed), ptr(oi, c_int), ptr(osz, c_int), ptr(inb, c_int),
+                              ptr(rec, c_double), ptr(rep, c_double)))
+    plans, pos, kb = [], 0, 0
+    for i in range(len(instances)):
+        sizes = osz[kb:kb + inb[i]]
+        cnt = int(sizes.sum())
+        plans.append(unflatten(oi[pos:pos + cnt], sizes))
+        pos += cnt
+        kb += int(inb[i])
+    return plans, _unpack_records(rec, n), _unpack_report(rep)
+
+
+def estimator(class_ids, priors, observations, predict_classes, seed):
+    """Estimator (P:src/output_estimator.cpp): priors per class None / ("gaussian", m, s) / ("range", lo, hi)."""
+    kinds = [0 if p is None else (1 if p[0] == "gaussian" else 2) for p in priors]
+    pa = [0.0 if p is None else float(p[1]) for p in priors]
+    pb = [0.0 if p is None else float(p[2]) for p in priors]
+    k = len(class_ids)
+    oc, ol = _i32([o[0] for o in observations] or [0]), _i32([o[1] for o in observations] or [0])
+    pc = _i32(list(predict_classes) or [0])
+    out = np.zeros(max(len(predict_classes), 1), dtype=np.int32)
+    cnt, mean, m2 = np.zeros(k, dtype=np.int64), np.zeros(k), np.zeros(k)
+    _check(lib().ref_estimator(c_int(k), ptr(_i32(class_ids), c_int), ptr(_i32(kinds), c_int), ptr(_f64(pa), c_double),
+                               ptr(_f64(pb), c_double), c_int(len(observations)), ptr(oc, c_int), ptr(ol, c_int),
+                               c_int(len(predict_classes)), ptr(pc, c_int), c_uint64(seed), ptr(out, c_int),
+                               ptr(cnt, ctypes.c_longlong), ptr(mean, c_double), ptr(m2, c_double)))
+    return [int(x) for x in out[:len(predict_classes)]], [(int(cnt[i]), float(mean[i]), float(m2[i])) for i in range(k)]
+
+
+def compare(w: FlatWorkload, coeffs, instances, policies, seeds, noise=0.0, gap=0.1, n_cap=10, **cfg):
+    """compare() (P:src/simulator.cpp:148-220); policies as codes (0 sa, 1 exhaustive, 2 fcfs)."""
+    fl = _fleet(instances)
+    sd = np.asarray(list(seeds), dtype=np.uint64)
+    rows, med = np.zeros(6 * len(policies) * len(sd)), np.zeros(6 * len(policies))
+    _check(lib().ref_compare(*_wargs(w), ptr(_f64(coeffs), c_double), *_fleet_args(fl), c_int(len(policies)),
+                             ptr(_i32(policies), c_int), c_int(len(sd)), ptr(sd, c_uint64), ptr(_cfg(**cfg), c_double),
+                             c_double(noise), c_double(gap), c_int(n_cap), ptr(rows, c_double), ptr(med, c_double)))
+    return rows.reshape(-1, 6), med.reshape(-1, 6)
+
+
 __all__ = [n for n in dir() if not n.startswith("_")] + ["POINTER"]

@@ -14,6 +14,8 @@
 //   anneal                       P:src/priority_mapper.cpp:340-411
 //   exhaustive                   P:src/priority_mapper.cpp:440-517
 //   schedule_all                 P:src/scheduler.cpp:92-129
+//   run / run_fcfs               P:src/simulator.cpp:49-123
+//   Estimator                    P:src/output_estimator.cpp:10-78
 // Errors map to codes: 1 DataError, 2 CapacityError, 6 std::invalid_argument,
 // 9 anything else; the message is kept in ref_last_error().
 #include <chrono>
@@ -31,6 +33,7 @@
 #include "slosched/priority_mapper.hpp"
 #include "slosched/rng.hpp"
 #include "slosched/scheduler.hpp"
+#include "slosched/simulator.hpp"
 #include "slosched/workload.hpp"
 
 using namespace slosched;
@@ -368,6 +371,131 @@ int ref_schedule_all(FLAT_ARGS, const double* c, int n_inst, const int* inst_id,
             }
         }
         *epochs = res.assignment.epochs;
+    });
+}
+
+}  // extern "C"
+
+namespace {
+std::vector<InstanceState> fleet_of(int n_inst, const int* inst_id, const double* total_mem,
+                                    const double* remaining_mem, const double* mu, const double* sigma,
+                                    const int* inst_mb) {
+    std::vector<InstanceState> fleet;
+    for (int i = 0; i < n_inst; ++i) {
+        InstanceState s;
+        s.id = inst_id[i];
+        s.total_mem = static_cast<std::uint64_t>(total_mem[i]);
+        s.remaining_mem = static_cast<std::uint64_t>(remaining_mem[i]);
+        s.mem_utility = mu[i];
+        s.bytes_per_token = sigma[i];
+        s.max_batch_size = inst_mb[i];
+        fleet.push_back(s);
+    }
+    return fleet;
+}
+// records as 8 doubles each: id, wait, exec, e2e, ttft, tpot, met, extrapolated; report as 6
+void dump(const MetricsReport& r, double* rec, double* rep) {
+    for (std::size_t i = 0; i < r.per_request.size(); ++i) {
+        const auto& m = r.per_request[i];
+        double* o = rec + 8 * i;
+        o[0] = m.request_id, o[1] = m.wait_ms, o[2] = m.exec_ms, o[3] = m.e2e_ms, o[4] = m.ttft_ms, o[5] = m.tpot_ms;
+        o[6] = m.slo_met ? 1.0 : 0.0, o[7] = m.extrapolated ? 1.0 : 0.0;
+    }
+    rep[0] = r.slo_attainment, rep[1] = r.avg_latency_ms, rep[2] = r.g, rep[3] = r.scheduling_overhead_ms;
+    rep[4] = r.n_met, rep[5] = r.total_latency_ms;
+}
+}  // namespace
+
+extern "C" {
+
+// run() over per-instance schedules (inst_nb[i] batches each, concatenated)
+int ref_run(FLAT_ARGS, const double* c, int n_inst, const int* inst_id, const double* total_mem,
+            const double* remaining_mem, const double* mu, const double* sigma, const int* inst_mb,
+            const int* s_ids, const int* s_sizes, const int* inst_nb, double noise, double gap,
+            std::uint64_t seed, double overhead, double* rec, double* rep) {
+    return guarded([&] {
+        Workload w = build(FLAT_PASS);
+        const auto fleet = fleet_of(n_inst, inst_id, total_mem, remaining_mem, mu, sigma, inst_mb);
+        std::vector<Schedule> plans;
+        int pos = 0, kb = 0;
+        for (int i = 0; i < n_inst; ++i) {
+            plans.push_back(schedule_of(s_ids + pos, s_sizes + kb, inst_nb[i]));
+            pos += static_cast<int>(plans.back().request_count());
+            kb += inst_nb[i];
+        }
+        SimConfig sim;
+        sim.noise_pct = noise, sim.dispatch_gap_ms = gap, sim.seed = seed;
+        dump(run(plans, w, fleet, coeffs_of(c), sim, overhead), rec, rep);
+    });
+}
+
+int ref_run_fcfs(FLAT_ARGS, const double* c, int n_inst, const int* inst_id, const double* total_mem,
+                 const double* remaining_mem, const double* mu, const double* sigma, const int* inst_mb,
+                 double noise, double gap, std::uint64_t seed, int* out_ids, int* out_sizes, int* inst_nb,
+                 double* rec, double* rep) {
+    return guarded([&] {
+        Workload w = build(FLAT_PASS);
+        SimConfig sim;
+        sim.noise_pct = noise, sim.dispatch_gap_ms = gap, sim.seed = seed;
+        const FcfsResult r = run_fcfs(w, fleet_of(n_inst, inst_id, total_mem, remaining_mem, mu, sigma, inst_mb),
+                                      coeffs_of(c), sim);
+        int pos = 0, kb = 0;
+        for (int i = 0; i < n_inst; ++i) {
+            int nb = 0;
+            emit(r.schedules[i], out_ids + pos, out_sizes + kb, &nb);
+            inst_nb[i] = nb;
+            pos += static_cast<int>(r.schedules[i].request_count());
+            kb += nb;
+        }
+        dump(r.report, rec, rep);
+    });
+}
+
+// Estimator: observe (class, len) pairs in order, then predict with Rng(seed)
+int ref_estimator(int n_classes, const int* class_id, const int* prior_kind, const double* prior_a,
+                  const double* prior_b, int n_obs, const int* obs_cls, const int* obs_len, int n_pred,
+                  const int* pred_cls, std::uint64_t seed, int* pred_out, long long* model_count,
+                  double* model_mean, double* model_m2) {
+    return guarded([&] {
+        std::vector<TaskClass> classes(n_classes);
+        for (int k = 0; k < n_classes; ++k) {
+            classes[k].id = class_id[k];
+            classes[k].slo = SloSpec::e2e(1.0);
+            if (prior_kind[k] == 1) classes[k].output_prior = GaussianPrior{prior_a[k], prior_b[k]};
+            else if (prior_kind[k] == 2)
+                classes[k].output_prior = RangePrior{static_cast<int>(prior_a[k]), static_cast<int>(prior_b[k])};
+        }
+        Estimator est(classes);
+        for (int i = 0; i < n_obs; ++i) est.observe_output(obs_cls[i], obs_len[i]);
+        for (int k = 0; k < n_classes; ++k) {
+            const LengthModel& m = est.model_for(class_id[k]);
+            model_count[k] = m.count, model_mean[k] = m.mean, model_m2[k] = m.m2;
+        }
+        Rng rng(seed);
+        for (int i = 0; i < n_pred; ++i) pred_out[i] = est.predict(pred_cls[i], rng);
+    });
+}
+
+// compare(): rows as 6 doubles (policy code, seed, attainment, avg latency, g, overhead), medians too
+int ref_compare(FLAT_ARGS, const double* c, int n_inst, const int* inst_id, const double* total_mem,
+                const double* remaining_mem, const double* mu, const double* sigma, const int* inst_mb,
+                int n_pol, const int* policies, int n_seeds, const std::uint64_t* seeds, const double* cfg,
+                double noise, double gap, int n_cap, double* rows, double* medians) {
+    return guarded([&] {
+        Workload w = build(FLAT_PASS);
+        std::vector<Policy> pol;
+        for (int i = 0; i < n_pol; ++i) pol.push_back(static_cast<Policy>(policies[i]));
+        SimConfig sim;
+        sim.noise_pct = noise, sim.dispatch_gap_ms = gap;
+        const auto t = compare(w, fleet_of(n_inst, inst_id, total_mem, remaining_mem, mu, sigma, inst_mb),
+                               coeffs_of(c), pol, std::vector<std::uint64_t>(seeds, seeds + n_seeds),
+                               config_of(cfg, 0), sim, n_cap);
+        auto put = [](const ComparisonRow& r, double* o) {
+            o[0] = static_cast<double>(parse_policy(r.policy)), o[1] = static_cast<double>(r.seed);
+            o[2] = r.attainment, o[3] = r.avg_latency_ms, o[4] = r.g_req_per_ms, o[5] = r.overhead_ms;
+        };
+        for (std::size_t i = 0; i < t.rows.size(); ++i) put(t.rows[i], rows + 6 * i);
+        for (std::size_t i = 0; i < t.medians.size(); ++i) put(t.medians[i], medians + 6 * i);
     });
 }
 

@@ -59,6 +59,32 @@ class SloChainResult(Structure):
                 ("local_positions_pass2", c_uint64)]
 
 
+class SloFleet(Structure):
+    _fields_ = [("n", c_int32), ("id", POINTER(c_int32)), ("total_mem", POINTER(c_double)),
+                ("remaining_mem", POINTER(c_double)), ("mu", POINTER(c_double)), ("sigma", POINTER(c_double)),
+                ("max_batch", POINTER(c_int32))]
+
+
+class SloSimConfig(Structure):
+    _fields_ = [("noise_pct", c_double), ("dispatch_gap_ms", c_double), ("seed", c_uint64)]
+
+
+class SloRecord(Structure):
+    _fields_ = [("request_id", c_int32), ("wait_ms", c_double), ("exec_ms", c_double), ("e2e_ms", c_double),
+                ("ttft_ms", c_double), ("tpot_ms", c_double), ("slo_met", c_int32), ("extrapolated", c_int32)]
+
+
+class SloReport(Structure):
+    _fields_ = [("slo_attainment", c_double), ("avg_latency_ms", c_double), ("g", c_double),
+                ("scheduling_overhead_ms", c_double), ("n_met", c_int32), ("total_latency_ms", c_double)]
+
+
+class SloRow(Structure):
+    _fields_ = [("policy", c_int32), ("seed", c_uint64), ("n_requests", c_int32), ("max_batch", c_int32),
+                ("attainment", c_double), ("avg_latency_ms", c_double), ("g_req_per_ms", c_double),
+                ("overhead_ms", c_double)]
+
+
 _I = POINTER(c_int32)
 _D = POINTER(c_double)
 
@@ -113,6 +139,24 @@ _SIGNATURES = [
     ("slosched_exhaustive", c_int32, [POINTER(SloWorkload), _D, _I, c_int32, c_int32, c_int32, _I, _I, _I, _I, _D,
                                       _D, POINTER(c_uint64)]),
     ("slo_exhaustive", c_int32, [c_void_p, c_int32, _I, _I, _I, _D, _D, POINTER(c_uint64)]),
+    ("slosched_run", c_int32, [POINTER(SloWorkload), _D, POINTER(SloFleet), _I, _I, _I, POINTER(SloSimConfig),
+                               c_double, POINTER(SloRecord), POINTER(SloReport)]),
+    ("slosched_run_fcfs", c_int32, [POINTER(SloWorkload), _D, POINTER(SloFleet), POINTER(SloSimConfig), _I, _I, _I,
+                                    POINTER(SloRecord), POINTER(SloReport)]),
+    ("slosched_realize_batches", c_int32, [POINTER(SloWorkload), _D, _I, _I, c_int32, c_double, c_double, c_double,
+                                           c_double, c_double, c_uint64, c_int32, POINTER(SloRecord), _D, _I]),
+    ("slosched_estimator", c_int32, [c_int32, _I, _I, _D, _D, c_int32, _I, _I, c_int32, _I, c_uint64, _I,
+                                     POINTER(c_int64), _D, _D]),
+    ("slosched_compare", c_int32, [POINTER(SloWorkload), _D, POINTER(SloFleet), c_int32, _I, c_int32,
+                                   POINTER(c_uint64), POINTER(SloAnnealConfig), POINTER(SloSimConfig), c_int32,
+                                   POINTER(SloRow), POINTER(SloRow)]),
+    ("slosched_sweep", c_int32, [c_int32, c_int32, c_int32, POINTER(c_uint64), POINTER(SloFleet), _D,
+                                 POINTER(SloAnnealConfig), c_int32, _D, c_int32, _I, _D]),
+    ("slosched_perturb", c_int32, [c_int32, c_int32, c_int32, POINTER(c_uint64), POINTER(SloFleet), _D,
+                                   POINTER(SloAnnealConfig), POINTER(SloSimConfig), c_int32, POINTER(c_char_p),
+                                   c_int32, _D, _D, _D, _D]),
+    ("slosched_evaluate_batch", c_int32, [POINTER(SloWorkload), _D, c_int32, c_int32, _I, _I, _I, c_int32, _I, _D,
+                                          _D]),
 ]
 
 EXPORTED = [name for name, _, _ in _SIGNATURES]

@@ -81,6 +81,54 @@ int emit(const Schedule& s, int32_t* ids, int32_t* sizes) {
     return nb;
 }
 
+std::vector<InstanceState> fleet_of(const slosched_fleet* f) {
+    if (!f) throw std::invalid_argument("null fleet");
+    std::vector<InstanceState> fleet(f->n);
+    for (int i = 0; i < f->n; ++i) {
+        fleet[i].id = f->id[i];
+        fleet[i].total_mem = static_cast<std::uint64_t>(f->total_mem[i]);
+        fleet[i].remaining_mem = static_cast<std::uint64_t>(f->remaining_mem[i]);
+        fleet[i].mem_utility = f->mu[i];
+        fleet[i].bytes_per_token = f->sigma[i];
+        fleet[i].max_batch_size = f->max_batch[i];
+    }
+    return fleet;
+}
+
+SimConfig sim_of(const slosched_sim_config* s) {
+    SimConfig c;
+    if (s) c.noise_pct = s->noise_pct, c.dispatch_gap_ms = s->dispatch_gap_ms, c.seed = s->seed;
+    return c;
+}
+
+void records_out(const std::vector<RequestMetrics>& v, slosched_record* out) {
+    if (!out) return;
+    for (std::size_t i = 0; i < v.size(); ++i) {
+        const auto& m = v[i];
+        out[i] = slosched_record{m.request_id, m.wait_ms, m.exec_ms, m.e2e_ms, m.ttft_ms, m.tpot_ms, m.slo_met ? 1 : 0,
+                                 m.extrapolated ? 1 : 0};
+    }
+}
+
+void report_out(const MetricsReport& r, slosched_report* out) {
+    if (out)
+        *out = slosched_report{r.slo_attainment, r.avg_latency_ms, r.g, r.scheduling_overhead_ms, r.n_met,
+                               r.total_latency_ms};
+}
+
+// the reference CLI's synthetic workload for a seed (P:tools/slosched.cpp:119-142)
+Workload synth_workload(int n, std::uint64_t seed, int predict_mode) {
+    auto [code, chat] = default_synth_classes();
+    auto reqs = generate_mixed(n, seed, code, chat);
+    if (predict_mode == 1) {
+        Rng rng(Rng::derive(seed, 0x9e37));
+        assign_predicted_lengths_from_priors(reqs, {code, chat}, rng);
+    } else {
+        for (auto& r : reqs) r.predicted_output_len = r.true_output_len;
+    }
+    return validate_workload(std::move(reqs), {code, chat});
+}
+
 AnnealConfig config_of(const slosched_anneal_config* c) {
     AnnealConfig a;
     if (!c) return a;
@@ -289,6 +337,152 @@ int slosched_build_tables(const slosched_workload* w, const double* c, const int
         cost_tables(wl, std::vector<int>(ids, ids + n), coeffs_of(c), max_batch, e, d);
         std::memcpy(exec, e.data(), e.size() * sizeof(double));
         std::memcpy(deadline, d.data(), d.size() * sizeof(double));
+    });
+}
+
+int slosched_run(const slosched_workload* w, const double* c, const slosched_fleet* f, const int32_t* ids,
+                 const int32_t* sizes, const int32_t* inst_nb, const slosched_sim_config* sim, double overhead_ms,
+                 slosched_record* records, slosched_report* report) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        const auto fleet = fleet_of(f);
+        std::vector<Schedule> plans(fleet.size());
+        int pos = 0, kb = 0;
+        for (std::size_t i = 0; i < fleet.size(); ++i) {
+            plans[i] = schedule_of(ids + pos, sizes + kb, inst_nb[i]);
+            pos += static_cast<int>(plans[i].request_count());
+            kb += inst_nb[i];
+        }
+        const MetricsReport r = run(plans, wl, fleet, coeffs_of(c), sim_of(sim), overhead_ms);
+        records_out(r.per_request, records);
+        report_out(r, report);
+    });
+}
+
+int slosched_run_fcfs(const slosched_workload* w, const double* c, const slosched_fleet* f,
+                      const slosched_sim_config* sim, int32_t* out_ids, int32_t* out_sizes, int32_t* inst_nb,
+                      slosched_record* records, slosched_report* report) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        const FcfsResult r = run_fcfs(wl, fleet_of(f), coeffs_of(c), sim_of(sim));
+        int pos = 0, kb = 0;
+        for (std::size_t i = 0; i < r.schedules.size(); ++i) {
+            inst_nb[i] = emit(r.schedules[i], out_ids + pos, out_sizes + kb);
+            pos += static_cast<int>(r.schedules[i].request_count());
+            kb += inst_nb[i];
+        }
+        records_out(r.report.per_request, records);
+        report_out(r.report, report);
+    });
+}
+
+int slosched_realize_batches(const slosched_workload* w, const double* c, const int32_t* ids, const int32_t* sizes,
+                             int32_t nb, double clock0, double first_gap, double gap, double until, double noise_pct,
+                             uint64_t seed, int32_t from_arrival, slosched_record* records, double* clock,
+                             int32_t* started) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        Rng rng(seed);
+        std::vector<RequestMetrics> rec;
+        const ReplayResult r = realize_batches(schedule_of(ids, sizes, nb).batches, wl, coeffs_of(c), clock0, first_gap,
+                                               gap, until, noise_pct, rng, rec, from_arrival != 0);
+        records_out(rec, records);
+        *clock = r.clock;
+        *started = r.batches_started;
+    });
+}
+
+int slosched_estimator(int32_t n_classes, const int32_t* class_id, const int32_t* prior_kind, const double* prior_a,
+                       const double* prior_b, int32_t n_obs, const int32_t* obs_cls, const int32_t* obs_len,
+                       int32_t n_pred, const int32_t* pred_cls, uint64_t seed, int32_t* pred_out, int64_t* model_count,
+                       double* model_mean, double* model_m2) {
+    return guarded([&] {
+        std::vector<TaskClass> classes(n_classes);
+        for (int k = 0; k < n_classes; ++k) {
+            classes[k].id = class_id[k];
+            classes[k].slo = SloSpec::e2e(1.0);
+            if (prior_kind[k] == 1) classes[k].output_prior = GaussianPrior{prior_a[k], prior_b[k]};
+            else if (prior_kind[k] == 2)
+                classes[k].output_prior = RangePrior{static_cast<int>(prior_a[k]), static_cast<int>(prior_b[k])};
+        }
+        Estimator est(classes);
+        for (int i = 0; i < n_obs; ++i) est.observe_output(obs_cls[i], obs_len[i]);
+        for (int k = 0; k < n_classes; ++k) {
+            const LengthModel& m = est.model_for(class_id[k]);
+            if (model_count) model_count[k] = m.count;
+            if (model_mean) model_mean[k] = m.mean;
+            if (model_m2) model_m2[k] = m.m2;
+        }
+        Rng rng(seed);
+        for (int i = 0; i < n_pred; ++i) pred_out[i] = est.predict(pred_cls[i], rng);
+    });
+}
+
+int slosched_compare(const slosched_workload* w, const double* c, const slosched_fleet* f, int32_t n_pol,
+                     const int32_t* policies, int32_t n_seeds, const uint64_t* seeds, const slosched_anneal_config* cfg,
+                     const slosched_sim_config* sim, int32_t exhaustive_cap, slosched_row* rows, slosched_row* medians) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        std::vector<Policy> pol;
+        for (int i = 0; i < n_pol; ++i) {
+            if (policies[i] < 0 || policies[i] > 2) throw DataError("compare: unknown policy code");
+            pol.push_back(static_cast<Policy>(policies[i]));
+        }
+        const ComparisonTable t = compare(wl, fleet_of(f), coeffs_of(c), pol, std::vector<std::uint64_t>(seeds, seeds + n_seeds),
+                                          config_of(cfg), sim_of(sim), exhaustive_cap);
+        auto row_out = [&](const ComparisonRow& r) {
+            return slosched_row{static_cast<int32_t>(parse_policy(r.policy)), r.seed, r.n_requests, r.max_batch,
+                                r.attainment, r.avg_latency_ms, r.g_req_per_ms, r.overhead_ms};
+        };
+        for (std::size_t i = 0; i < t.rows.size(); ++i) rows[i] = row_out(t.rows[i]);
+        for (std::size_t i = 0; i < t.medians.size(); ++i) medians[i] = row_out(t.medians[i]);
+    });
+}
+
+int slosched_sweep(int32_t n_requests, int32_t predict_mode, int32_t n_seeds, const uint64_t* seeds,
+                   const slosched_fleet* f, const double* c, const slosched_anneal_config* cfg, int32_t n_t0,
+                   const double* t0_grid, int32_t n_iter, const int32_t* iter_grid, double* g_out) {
+    return guarded([&] {
+        std::vector<Workload> per;
+        for (int s = 0; s < n_seeds; ++s) per.push_back(synth_workload(n_requests, seeds[s], predict_mode));
+        const auto rows = sweep(per, std::vector<std::uint64_t>(seeds, seeds + n_seeds), fleet_of(f), coeffs_of(c),
+                                config_of(cfg), std::vector<double>(t0_grid, t0_grid + n_t0),
+                                std::vector<int>(iter_grid, iter_grid + n_iter));
+        for (std::size_t i = 0; i < rows.size(); ++i) g_out[i] = rows[i].g_req_per_ms;
+    });
+}
+
+int slosched_perturb(int32_t n_requests, int32_t predict_mode, int32_t n_seeds, const uint64_t* seeds,
+                     const slosched_fleet* f, const double* truth, const slosched_anneal_config* cfg,
+                     const slosched_sim_config* sim, int32_t n_params, const char* const* params, int32_t n_factors,
+                     const double* factors, double* g_out, double* baseline_out, double* degradation_out) {
+    return guarded([&] {
+        std::vector<Workload> per;
+        for (int s = 0; s < n_seeds; ++s) per.push_back(synth_workload(n_requests, seeds[s], predict_mode));
+        std::vector<std::string> ps(params, params + n_params);
+        const auto rows = perturb(per, std::vector<std::uint64_t>(seeds, seeds + n_seeds), fleet_of(f), coeffs_of(truth),
+                                  config_of(cfg), sim_of(sim), ps, std::vector<double>(factors, factors + n_factors));
+        for (std::size_t i = 0; i < rows.size(); ++i) {
+            g_out[i] = rows[i].g_req_per_ms;
+            baseline_out[i] = rows[i].baseline_g;
+            degradation_out[i] = rows[i].degradation_pct;
+        }
+    });
+}
+
+int slosched_evaluate_batch(const slosched_workload* w, const double* c, int32_t n_sched, int32_t n, const int32_t* ids,
+                            const int32_t* sizes, const int32_t* nb, int32_t max_batch, int32_t* n_met, double* t,
+                            double* g) {
+    return guarded([&] {
+        const Workload wl = workload_of(w);
+        std::vector<Schedule> sch(n_sched);
+        int kb = 0;
+        for (int s = 0; s < n_sched; ++s) {
+            sch[s] = schedule_of(ids + static_cast<std::size_t>(s) * n, sizes + kb, nb[s]);
+            kb += nb[s];
+        }
+        const auto sc = evaluate_batch(sch, coeffs_of(c), wl, max_batch);
+        for (int s = 0; s < n_sched; ++s) n_met[s] = sc[s].n, t[s] = sc[s].t_ms, g[s] = sc[s].g;
     });
 }
 

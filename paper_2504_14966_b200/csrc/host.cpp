@@ -21,6 +21,7 @@
 
 #include "slosched_b200.hpp"
 #include "slosched_gpu.h"
+#include "internal.hpp"
 
 namespace slosched {
 
@@ -905,6 +906,13 @@ double best_deadline_first(int n, int mb, const std::vector<double>& exec, const
 }
 
 }  // namespace
+
+namespace detail {
+slo_ctx* acquire_ctx(int device) { return CtxPool::get().acquire(device).release(); }
+void release_ctx(int device, slo_ctx* ctx) { CtxPool::get().release(device, CtxPtr(ctx)); }
+int resolve_device(int requested) { return ::slosched::resolve_device(requested); }
+void check(int rc) { engine_check(rc); }
+}  // namespace detail
 
 Schedule deadline_first_candidate(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c,
                                   int max_batch) {

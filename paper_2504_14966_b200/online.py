@@ -5,30 +5,36 @@ is the §8(f) row 2 extension, built on the public entry points:
 
 * stream    -- request lengths from the reference's synthetic generator (generate_mixed, with
               estimator-predicted output lengths), Poisson arrivals at a stated rate;
-* instances -- k serving instances (one per GPU in production; here they share the visible
-              GPUs), requests assigned on arrival to the least-loaded instance;
+* instances -- k serving instances placed round-robin on `devices` (one per GPU on an 8-GPU box;
+              instances sharing a GPU split its SMs), requests assigned on arrival to the
+              least-loaded instance;
 * windows   -- every window_ms of simulated time each instance's queue (arrived, not yet
               started) is re-planned with anneal() under a per-window device budget; the plan's
               batches are dispatched until the next window boundary, the rest is re-planned;
 * planning  -- the objective sees each request's remaining slack: its SLO minus the time it has
               already waited (a per-request SLO class), exactly the reference objective otherwise;
-* execution -- realized times from the latency model with the TRUE output lengths plus the
-              reference simulator's 0.1 ms dispatch gap (P:src/simulator.cpp:49-74, noise 0).
+* execution -- the library's replay (harness.realize_batches, csrc/harness.cpp): the reference
+              simulator's ground truth -- latency model over the TRUE output lengths, 0.1 ms
+              dispatch gap, noise 0 (P:src/simulator.cpp:17-74) -- on each instance's clock, every
+              window; run() is the same routine and is pinned bit-for-bit to the reference's run()
+              (tests/test_harness.py).
 
 Policies: "sa" (GPU chains), "fcfs" (arrival order, greedy batches -- the reference's FCFS
-baseline, P:src/simulator.cpp:76-123).
+baseline, P:src/simulator.cpp:76-123), "custom" (a caller's planner(stream, queue, start_ms) ->
+batches; tools/online_bench.py plugs the reference's own CPU anneal() in per window).
 """
 from __future__ import annotations
 
 import time
 from concurrent.futures import ThreadPoolExecutor
 from dataclasses import dataclass, field
-from typing import Dict, List, Optional
+from typing import Callable, Dict, List, Optional, Sequence
 
 import numpy as np
 
-from .slosched import (AnnealConfig, LatencyCoefficients, Request, SloKind, SloSpec, TaskClass, Workload,
-                       anneal_flat, generate_mixed, table_coefficients)
+from .harness import realize_batches
+from .slosched import (AnnealConfig, LatencyCoefficients, Request, SloSpec, TaskClass, Workload, anneal_flat,
+                       generate_mixed, table_coefficients)
 
 _IMPOSSIBLE_MS = 1e-9  # an SLO whose slack is already gone: positive (valid) but unreachable
 
@@ -124,6 +130,23 @@ def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
     return out, st.proposals
 
 
+_CLASSES = [TaskClass(0, "code", SloSpec.e2e(30000.0)), TaskClass(1, "chat", SloSpec.ttft_tpot(10000.0, 50.0))]
+
+
+def _execute(stream, batches, c, clock0, gap, until):
+    """Replay a plan on one instance clock until the window ends: (met, summed e2e, started ids, clock)."""
+    ids = [i for b in batches for i in b]
+    reqs = [Request(int(i), int(stream.cls[i]), int(stream.input_len[i]), int(stream.true_out[i]),
+                    int(stream.pred_out[i]), float(stream.arrival_ms[i])) for i in ids]
+    recs, clock, started = realize_batches(batches, Workload(reqs, _CLASSES), c, clock0, gap, gap, until,
+                                           from_arrival=True)
+    met = sum(1 for r in recs if r.slo_met)
+    lat = 0.0
+    for r in recs:
+        lat += r.e2e_ms
+    return met, lat, [i for b in batches[:started] for i in b], clock
+
+
 def _plan_fcfs(stream, ids, max_batch):
     order = sorted(ids, key=lambda i: (stream.arrival_ms[i], i))
     return [order[k:k + max_batch] for k in range(0, len(order), max_batch)], 0
@@ -133,7 +156,8 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
                max_batch: int = 4, budget_ms: float = 10.0, chains: int = 4096, seed: int = 0,
                coeffs: Optional[LatencyCoefficients] = None, dispatch_gap_ms: float = 0.1,
                max_windows: Optional[int] = None, scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4, 1e5),
-               t0: float = 500.0, tau: float = 0.7, iter: int = 30) -> OnlineResult:
+               t0: float = 500.0, tau: float = 0.7, iter: int = 30, devices: Sequence[int] = (0,),
+               planner: Optional[Callable] = None) -> OnlineResult:
     c = coeffs or table_coefficients()
     n = stream.n
     queue: List[List[int]] = [[] for _ in range(n_instances)]
@@ -143,15 +167,23 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
     done = 0
     n_met, total_lat, proposals, decisions = 0, 0.0, 0, 0
     overhead: List[float] = []
-    share = 0
+    # instance k runs on devices[k % len]; instances sharing a device split its SMs
+    dev_of = [int(devices[k % len(devices)]) for k in range(n_instances)]
+    share = [0] * n_instances
     if policy == "sa":
         import ctypes
         from ._lib import lib
-        ctx = ctypes.c_void_p()
-        if lib().slo_ctx_create(0, ctypes.byref(ctx)) == 0:
-            share = max(1, int(lib().slo_ctx_sm_count(ctx)) // n_instances)
-            lib().slo_ctx_destroy(ctx)
-    pool = ThreadPoolExecutor(n_instances) if policy == "sa" else None
+        for d in set(dev_of):
+            ctx = ctypes.c_void_p()
+            if lib().slo_ctx_create(d, ctypes.byref(ctx)) == 0:
+                sms = int(lib().slo_ctx_sm_count(ctx))
+                lib().slo_ctx_destroy(ctx)
+                for k in range(n_instances):
+                    if dev_of[k] == d:
+                        share[k] = max(1, sms // dev_of.count(d))
+    if policy == "custom" and planner is None:
+        raise ValueError("run_online: policy 'custom' needs a planner")
+    pool = ThreadPoolExecutor(n_instances) if policy in ("sa", "custom") else None
     t_win = 0.0
     windows = 0
     while done < n and (max_windows is None or windows < max_windows):
@@ -177,44 +209,30 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
             def plan(k):
                 cfg = AnnealConfig(t0=t0, tau=tau, iter=iter, seed=seed * 1_000_003 + windows * 131 + k,
                                    chains=chains, budget_ms=kernel_budget, scale_ladder=scale_ladder,
-                                   max_blocks=share)
+                                   max_blocks=share[k], device=dev_of[k])
                 return _plan_sa(stream, queue[k], max(busy_until[k], t_win), c, max_batch, cfg)
             plans = dict(zip(active, pool.map(plan, active)))
+        elif policy == "custom":
+            starts = [max(busy_until[k], t_win) for k in active]
+            plans = {k: (b, 0) for k, b in zip(active, pool.map(planner, [stream] * len(active),
+                                                                 [queue[k] for k in active], starts))}
         else:
             plans = {k: _plan_fcfs(stream, queue[k], max_batch) for k in active}
         overhead.append((time.perf_counter() - t0_wall) * 1e3)
         decisions += len(active)
-        # execute each plan until the next window boundary
+        # execute each plan until the next window boundary (the library's replay)
         for k, (batches, props) in plans.items():
             proposals += props
-            t = max(busy_until[k], t_win)
-            started = []
-            for b in batches:
-                if t >= t_next:
-                    break
-                start = t + dispatch_gap_ms
-                bs = len(b)
-                li = stream.input_len[b].astype(np.float64)
-                lo = stream.true_out[b].astype(np.float64)
-                pf = prefill_ms(c, bs, li)
-                dec = decode_total_ms(c, bs, li, lo)
-                ex = pf + dec
-                for j, i in enumerate(b):
-                    e2e = start + ex[j] - stream.arrival_ms[i]
-                    if stream.cls[i] == 0:
-                        ok = e2e <= 30000.0
-                    else:
-                        ok = (start + pf[j] - stream.arrival_ms[i] <= 10000.0) and (dec[j] / lo[j] <= 50.0)
-                    n_met += int(ok)
-                    total_lat += e2e
-                    load[k] -= prefill_ms(c, 1, stream.input_len[i]) + decode_total_ms(
-                        c, 1, stream.input_len[i], stream.pred_out[i])
-                started.extend(b)
-                t = start + ex.max()
-            busy_until[k] = t
+            met, lat, started, clock = _execute(stream, batches, c, max(busy_until[k], t_win), dispatch_gap_ms, t_next)
+            n_met += met
+            total_lat += lat
+            busy_until[k] = clock
             if started:
-                s = set(started)
-                queue[k] = [i for i in queue[k] if i not in s]
+                for i in started:
+                    load[k] -= prefill_ms(c, 1, stream.input_len[i]) + decode_total_ms(c, 1, stream.input_len[i],
+                                                                                       stream.pred_out[i])
+                s_ = set(started)
+                queue[k] = [i for i in queue[k] if i not in s_]
                 done += len(started)
         t_win = t_next
     if pool:

@@ -36,3 +36,12 @@ def ref():
     if not r.available():
         pytest.skip("oracle/_ref not built (needs /root/reference at build time)")
     return r
+
+
+def _ref_available():
+    from oracle import ref as r
+    return r.available()
+
+
+# tests that compare with the unmodified reference library (oracle/_ref)
+requires_ref = pytest.mark.skipif(not _ref_available(), reason="oracle/_ref not built (needs /root/reference at build time)")

@@ -41,6 +41,18 @@ def test_fcfs_completes_every_request_and_matches_a_direct_simulation():
     assert r1.n_met == n_met
 
 
+def test_custom_planner_and_devices():
+    """A caller's planner plugs in per window (here the FCFS rule itself: identical result)."""
+    s = O.make_stream(400, rate_per_s=0.6, seed=5)
+    ref = O.run_online(s, "fcfs", n_instances=3, window_ms=4000.0)
+    fcfs_rule = lambda st, ids, start: O._plan_fcfs(st, ids, 4)[0]  # noqa: E731
+    got = O.run_online(s, "custom", n_instances=3, window_ms=4000.0, planner=fcfs_rule, devices=(0, 1))
+    assert (got.n, got.n_met, got.total_latency_ms, got.windows) == (ref.n, ref.n_met, ref.total_latency_ms,
+                                                                      ref.windows)
+    with pytest.raises(ValueError):
+        O.run_online(s, "custom", n_instances=2)
+
+
 @pytest.mark.gpu
 def test_online_sa_beats_fcfs():
     mu = O.service_rate_per_s()
