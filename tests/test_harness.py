@@ -162,11 +162,11 @@ def _replay_cfg(**kw):
 def test_compare_replay_mode_matches_reference_compare():
     """With the exact-replay mapper, compare() is the reference's compare() row for row."""
     c = S.table_coefficients()
-    w = S.generate_mixed(60, 4)
+    w = S.generate_mixed(18, 4)  # 6 requests per instance: the exhaustive oracle stays small
     insts = _fleet(3, mb=4)
     t = H.compare(w, insts, c, ["sa", "fcfs", "exhaustive"], [1, 2], _replay_cfg(), H.SimConfig(noise_pct=0.1),
-                  exhaustive_cap=25)
-    rows, med = ref.compare(_flat(w), TABLE_COEFFS, _ref_fleet(insts), [0, 2, 1], [1, 2], noise=0.1, n_cap=25,
+                  exhaustive_cap=10)
+    rows, med = ref.compare(_flat(w), TABLE_COEFFS, _ref_fleet(insts), [0, 2, 1], [1, 2], noise=0.1, n_cap=10,
                             t0=80.0, iter=15)
     assert len(t.rows) == 6
     for got, want in zip(t.rows, rows):

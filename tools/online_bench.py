@@ -7,6 +7,7 @@ Prints one JSON object: the stream (rate = load x instances x per-instance servi
 per policy realized attainment, average latency, G and the per-window scheduling overhead (wall ms
 for planning all instances of a window concurrently). Policies:
   sa    the GPU chains, instances placed round-robin on --devices (default: every visible GPU)
+  sa-dlstart  the same, with the deadline-first candidate among the chains' starts
   fcfs  arrival order, greedy batches (the reference's FCFS baseline)
   ref   the UNMODIFIED reference's CPU anneal() (oracle/_ref, default AnnealConfig) per window and
         instance, with the same remaining-slack SLOs the GPU arm plans with -- the reference
@@ -75,7 +76,12 @@ def main():
     out["devices"] = devices
     for pol in args.policies.split(","):
         t = time.perf_counter()
-        kw = dict(policy="custom", planner=reference_planner(seed=args.seed)) if pol == "ref" else dict(policy=pol)
+        if pol == "ref":
+            kw = dict(policy="custom", planner=reference_planner(seed=args.seed))
+        elif pol == "sa-dlstart":  # the chains also start from the deadline-first candidate
+            kw = dict(policy="sa", anneal_kw=dict(deadline_start=True))
+        else:
+            kw = dict(policy=pol)
         r = O.run_online(stream, n_instances=args.instances, window_ms=args.window_ms, budget_ms=args.budget_ms,
                          chains=args.chains, seed=args.seed, devices=devices, **kw)
         s = r.summary()
