@@ -384,8 +384,11 @@ __host__ __device__ constexpr int rnd_stride() { return UPL == 1 ? SLO_RND_STRID
 #ifndef SLO_LIVE_CAP4
 #define SLO_LIVE_CAP4 10
 #endif
+#ifndef SLO_LIVE_CAP1
+#define SLO_LIVE_CAP1 5  // mb = 8 at N = 1024: the live prefix is 4 units (3: 6.2e9, 5: 9.1e9 proposals/s)
+#endif
 template <int UPL>
-__host__ __device__ constexpr int live_cap() { return UPL == 1 ? 3 : (UPL == 2 ? SLO_LIVE_CAP2 : SLO_LIVE_CAP4); }
+__host__ __device__ constexpr int live_cap() { return UPL == 1 ? SLO_LIVE_CAP1 : (UPL == 2 ? SLO_LIVE_CAP2 : SLO_LIVE_CAP4); }
 
 template <int UPL>
 __host__ __device__ constexpr int slot_bytes() {

@@ -10,12 +10,13 @@ import numpy as np
 import paper_2504_14966_b200 as S
 from paper_2504_14966_b200 import engine as E
 c = S.table_coefficients()
+MB = int(os.environ.get("MB", "4"))
 for n in (1024, 4096):
     w = S.generate_mixed(n, 0); ids = sorted(w.ids())
-    s, i = S.initial_candidates(w, ids, c, 4); d = S.deadline_first_candidate(w, ids, c, 4)
+    s, i = S.initial_candidates(w, ids, c, MB); d = S.deadline_first_candidate(w, ids, c, MB)
     ev = max([S.evaluate(x, c, w) for x in (s, i, d)], key=lambda e: e.g)
     pos = {r: k for k, r in enumerate(ids)}
-    eng = E.Engine(0); ex, dl = E.build_tables(w, ids, c, 4); eng.set_problem(ex, dl)
+    eng = E.Engine(0); ex, dl = E.build_tables(w, ids, c, MB); eng.set_problem(ex, dl)
     for lev in (3, 7):
         t0, tau = 500.0, 0.7
         eng.prepare([pos[x] for x in ev.schedule.flatten()], [len(b) for b in ev.schedule.batches], t0=t0, tau=tau, iter=100,
