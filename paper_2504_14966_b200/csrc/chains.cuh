@@ -31,7 +31,7 @@
 #define SLO_CHAIN_THREADS 896  // k_chains<1> block size (28 warps, 72 registers; 768 and 1024 measured slower)
 #endif
 #ifndef SLO_CHAIN_THREADS2
-#define SLO_CHAIN_THREADS2 896
+#define SLO_CHAIN_THREADS2 768  // 20-word rows let 25 warps fit; 24 balance 16384 chains better (8.8e9 vs 6.1e9)
 #endif
 #ifndef SLO_CHAIN_THREADS4
 #define SLO_CHAIN_THREADS4 512
@@ -44,11 +44,17 @@ template <int UPL>
 __host__ __device__ constexpr int chain_threads() {
     return UPL == 1 ? SLO_CHAIN_THREADS : (UPL == 2 ? SLO_CHAIN_THREADS2 : SLO_CHAIN_THREADS4);
 }
+// A proposal's row of Philox words: word 0 holds the ops of the 8 random attempts (U[0, 3^8) by
+// one multiply-high, op j = its base-3 digit j: each op exactly uniform); attempt j reads its
+// positions from words 1 + 2j (squeeze / delay position, first swap position) and 2 + 2j (second
+// swap position); words 17, 18 are the forced swap's (attempt 8), word 19 the acceptance uniform.
 constexpr int kAttempts = 9;                         // 8 random move attempts + the forced swap
-constexpr int kAccWord = 3 * kAttempts;              // 3 words per attempt, then the acceptance uniform
-constexpr int kRndWords = 32;                        // words of a proposal's row (stride: rnd_stride)
-constexpr int kRndBlocks = (kAccWord + 1 + 3) / 4;   // Philox blocks a row needs (7: words 0..27)
-static_assert(4 * kRndBlocks <= kRndWords, "Philox row too small");
+constexpr int kOpsWord = 0;
+constexpr int kAccWord = 1 + 2 * kAttempts;          // 19
+constexpr int kRndWords = kAccWord + 1;              // 20 words = 5 Philox blocks
+constexpr int kRndBlocks = kRndWords / 4;
+static_assert(4 * kRndBlocks == kRndWords, "Philox row");
+__device__ __forceinline__ uint32_t pos_word(int j) { return 1 + 2 * j; }
 constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
 constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
 constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
@@ -268,36 +274,7 @@ struct Move {         // also the move record of K2 (replay.cuh)
     int a, b;        // swap positions
 };
 
-// The reference's proposal discipline (P:src/priority_mapper.cpp:184-198) over the entry /
-// bitmask representation: up to 8 attempts of op = U[0,3) (squeeze / delay / swap), the first
-// that applies wins, else a forced swap. Lane j < 9 tests attempt j from its three Philox words
-// (attempt 8 is the forced swap) with one move-flag bit -- branch-free, all attempts at once --
-// and the warp takes the first valid one: the same move the sequential loop would pick.
-// Returns op << 30 | pos | b << 13 (squeeze / delay: pos; swap: a = pos, b), or kNoMove.
-constexpr uint32_t kNoMove = 0xffffffffu;
-__device__ __forceinline__ uint32_t draw_move(const uint16_t* ent, const uint32_t* sqb, const uint32_t* dlb, int n,
-                                              uint32_t magic, const uint32_t* rw, int lane) {
-    const uint32_t nn = (uint32_t)n;
-    const uint32_t first = __umulhi(ent[0], magic) + 1u;  // size of the first batch
-    bool ok = false;
-    uint32_t pk = 0;
-    if (lane < kAttempts && n > 0) {
-        const uint32_t r0 = rw[3 * lane], r1 = rw[3 * lane + 1], r2 = rw[3 * lane + 2];
-        const uint32_t op = lane < kAttempts - 1 ? lemire32(r0, 3) : 2u;
-        const uint32_t a = lemire32(r1, nn);                   // delay position / first swap position
-        const uint32_t ps = first + lemire32(r1, nn - first);  // squeeze position (:141-153)
-        uint32_t b = lemire32(r2, nn - 1);                     // swap (:172-180)
-        b += b >= a ? 1u : 0u;
-        const uint32_t pos = op == 0 ? ps : a;
-        const uint32_t qf = min(pos, nn - 1);
-        // squeeze fails if the batch before pos's batch is full; delay if the next one is full
-        const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
-        ok = op == 2 ? n >= 2 : (!fails && (op == 1 || first < nn));
-        pk = op << 30 | pos | (op == 2 ? b << 13 : 0u);
-    }
-    const unsigned vm = __ballot_sync(FULL, ok);
-    return vm ? __shfl_sync(FULL, pk, __ffs(vm) - 1) : kNoMove;
-}
+constexpr uint32_t kNoMove = 0xffffffffu;  // packed move: op << 30 | pos | b << 13
 
 // the batch rebuild of a squeeze (op 0) or delay (op 1) of position pos: batch bounds from one
 // bit search, sizes from the entries
@@ -361,16 +338,16 @@ __device__ __forceinline__ double objective_fast(int nm, double tot) {
 #define SLO_RND_ROWS4 16
 #endif
 #ifndef SLO_RND_STRIDE1
-#define SLO_RND_STRIDE1 28  // 7 x 16 B: odd in 16-byte units, so the row stores stay conflict-free
+#define SLO_RND_STRIDE1 20  // 5 x 16 B: odd in 16-byte units, so the row stores stay conflict-free
 #endif
 #ifndef SLO_RND_STRIDE_WIDE
-#define SLO_RND_STRIDE_WIDE 28
+#define SLO_RND_STRIDE_WIDE 20
 #endif
 // Philox rows drawn per refill (one per lane): 32 proposals, 16 where shared memory is tight
 template <int UPL>
 __host__ __device__ constexpr int rnd_rows() { return UPL == 1 ? 32 : (UPL == 2 ? SLO_RND_ROWS2 : SLO_RND_ROWS4); }
 
-// row stride (words): a row is 28 words (7 Philox blocks); an odd number of 16-byte units puts
+// row stride (words): a row is 20 words (5 Philox blocks); an odd number of 16-byte units puts
 // the lanes' row stores on distinct bank groups (conflict-free uint4 stores); where shared memory
 // bounds the resident warps (2-4 units per lane) the dense stride keeps one more warp per SM
 template <int UPL>
@@ -811,12 +788,17 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     __syncwarp();                // every lane is done reading the previous rows
                     if (lane < kRows) {
                         // Philox block b of a row = counter (proposal, chain, b, tag)
-                        uint4* dst = reinterpret_cast<uint4*>(rnd + rnd_stride<UPL>() * lane);
+                        uint32_t* dst = rnd + rnd_stride<UPL>() * lane;
 #pragma unroll
                         for (int b = 0; b < kRndBlocks; ++b) {
                             uint32_t r[4] = {prop0 + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
                             philox10(r, p.key0, p.key1);
-                            dst[b] = make_uint4(r[0], r[1], r[2], r[3]);
+                            if constexpr (rnd_stride<UPL>() % 4 == 0) {
+                                reinterpret_cast<uint4*>(dst)[b] = make_uint4(r[0], r[1], r[2], r[3]);
+                            } else {
+#pragma unroll
+                                for (int i = 0; i < 4; ++i) dst[4 * b + i] = r[i];
+                            }
                         }
                     }
                     __syncwarp();
@@ -847,9 +829,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         uint32_t pk = kNoMove;
                         if (on && n >= 2) {
                             // the reference's proposal discipline (P:src/priority_mapper.cpp:184-198)
+                            uint32_t ops = lemire32(rl[kOpsWord], 6561u);  // 3^8: the 8 ops as base-3 digits
                             for (int j = 0; j < kAttempts - 1; ++j) {
-                                const uint32_t r0 = rl[3 * j], r1 = rl[3 * j + 1], r2 = rl[3 * j + 2];
-                                const uint32_t op = lemire32(r0, 3);
+                                const uint32_t r1 = rl[pos_word(j)], r2 = rl[pos_word(j) + 1];
+                                const uint32_t op = ops % 3u;
+                                ops /= 3u;
                                 const uint32_t a = lemire32(r1, nn);
                                 const uint32_t ps = first + lemire32(r1, nn - first);
                                 uint32_t b = lemire32(r2, nn - 1);
@@ -863,8 +847,8 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 }
                             }
                             if (pk == kNoMove) {  // the forced swap (attempt 8)
-                                const uint32_t a8 = lemire32(rl[3 * (kAttempts - 1) + 1], nn);
-                                uint32_t b8 = lemire32(rl[3 * (kAttempts - 1) + 2], nn - 1);
+                                const uint32_t a8 = lemire32(rl[pos_word(kAttempts - 1)], nn);
+                                uint32_t b8 = lemire32(rl[pos_word(kAttempts - 1) + 1], nn - 1);
                                 b8 += b8 >= a8 ? 1u : 0u;
                                 pk = 2u << 30 | a8 | b8 << 13;
                             }

@@ -6,8 +6,10 @@ Semantics modelled:
   list of batches: up to 8 attempts of op = U[0,3) -- squeeze / delay / swap -- the first valid one
   wins, else a forced swap (attempt 8);
 * draws from Philox4x32-10 (Random123 constants): the row of proposal `prop` of chain `cid` is
-  32 words, block b = philox(ctr = (prop, cid, b, 0x5105c4ed), key = (seed lo, seed hi)); attempt a
-  uses words 3a, 3a+1, 3a+2; U[0, m) = (word * m) >> 32; the acceptance uniform is word 27;
+  20 words, block b = philox(ctr = (prop, cid, b, 0x5105c4ed), key = (seed lo, seed hi)); the ops of
+  attempts 0-7 are the base-3 digits of U[0, 3^8) from word 0, attempt a's positions come from words
+  1 + 2a and 2 + 2a (attempt 8, the forced swap: words 17, 18); U[0, m) = (word * m) >> 32; the
+  acceptance uniform is word 19;
 * objective: the total latency on the tick grid (exec rounded half-even to multiples of `tick`,
   every sum an integer); n_met exactly the reference's -- the batch-start elapsed time summed in
   fp64 makespan by makespan (P:src/priority_mapper.cpp:264-276) against the fp64 latest-start
@@ -27,7 +29,7 @@ import numpy as np
 M32 = 0xFFFFFFFF
 TAG_MOVE = 0x5105C4ED
 ATTEMPTS = 9
-ACC_WORD = 27
+ACC_WORD = 19
 
 
 def philox4x32_10(ctr, key):
@@ -43,7 +45,7 @@ def philox4x32_10(ctr, key):
 
 def row(prop, cid, seed):
     words = []
-    for b in range(8):
+    for b in range(5):
         words += philox4x32_10([prop, cid, b, TAG_MOVE], [seed & M32, (seed >> 32) & M32])
     return words
 
@@ -96,9 +98,10 @@ def _locate(batches, pos):
 
 def propose(batches, n, mb, words):
     """Apply the first valid attempt to a copy of batches; returns the new batches (or None)."""
+    ops = mulhi(words[0], 3 ** 8)
     for a in range(ATTEMPTS):
-        r0, r1, r2 = words[3 * a], words[3 * a + 1], words[3 * a + 2]
-        op = mulhi(r0, 3) if a < ATTEMPTS - 1 else 2
+        r1, r2 = words[1 + 2 * a], words[2 + 2 * a]
+        op = (ops // 3 ** a) % 3 if a < ATTEMPTS - 1 else 2
         if op == 0:  # squeeze: move pos to the end of the previous batch (:141-153)
             first = len(batches[0])
             if first >= n:
