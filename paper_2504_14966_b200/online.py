@@ -130,7 +130,7 @@ def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
     for s in sizes:
         out.append([int(x) for x in seq[pos:pos + s]])
         pos += int(s)
-    return out, st.proposals
+    return out, st.proposals, st.kernel_ms
 
 
 _CLASSES = [TaskClass(0, "code", SloSpec.e2e(30000.0)), TaskClass(1, "chat", SloSpec.ttft_tpot(10000.0, 50.0))]

@@ -60,8 +60,8 @@ def eng():
 
 
 # ---------------------------------------------------------------- K1
-@pytest.mark.parametrize("n,mb,count", [(1, 1, 4), (8, 2, 500), (64, 4, 2000), (256, 8, 20000), (1024, 4, 2000),
-                                        (300, 16, 500), (4096, 4, 64)])
+@pytest.mark.parametrize("n,mb,count", [(1, 1, 4), (8, 2, 500), (64, 4, 2000), (256, 4, 100000), (256, 8, 20000),
+                                        (1024, 4, 2000), (300, 16, 500), (4096, 4, 64)])
 def test_evaluate_batch_bit_exact(eng, port, n, mb, count):
     w = _three_class(n, 1000 + n)
     c = S.table_coefficients()
@@ -416,6 +416,30 @@ def test_chains_valid_and_dominant(n, mb, chains):
         # the grid's rounding of the exact evaluation of its winner
         if res.best.g > max(res.stats.g_sorted_start, res.stats.g_input_start, res.stats.g_deadline_start):
             assert abs(res.stats.engine_g - res.best.g) <= 2.0 ** -26 * res.best.g
+
+
+@pytest.mark.parametrize("n,mb", [(256, 4), (1024, 4), (1024, 8), (3000, 4)])
+def test_chain_winner_objective_matches_exact_evaluation(n, mb):
+    """Whichever start wins the final floor, the engine's own winner -- fetched through the engine
+    C ABI -- has the n_met of the reference's evaluate() exactly and t within 2^-26."""
+    c = S.table_coefficients()
+    w = _three_class(n, 77 + n)
+    ids = sorted(w.ids())
+    s_sched, i_sched = S.initial_candidates(w, ids, c, mb)
+    ev = max([S.evaluate(x, c, w) for x in (s_sched, i_sched, S.deadline_first_candidate(w, ids, c, mb))],
+             key=lambda e: e.g)
+    pos = {r: k for k, r in enumerate(ids)}
+    eng = E.Engine(0)
+    ex, dl = E.build_tables(w, ids, c, mb)
+    eng.set_problem(ex, dl)
+    bp, bs, res = eng.anneal_chains([pos[x] for x in ev.schedule.flatten()], [len(b) for b in ev.schedule.batches],
+                                    t0=200.0, iter=40, seed=9, objective_scale=1e6 * 200.0 / ev.g, chains=2048,
+                                    scale_ladder=(1.0, 100.0))
+    eng.close()
+    sched = S.Schedule([[ids[k] for k in bp[p0:p0 + z]] for p0, z in zip(np.cumsum([0] + list(bs[:-1])), bs)])
+    exact = S.evaluate(sched, c, w)
+    assert res.n_met == exact.n
+    assert abs(res.t - exact.t_ms) <= 2.0 ** -26 * exact.t_ms
 
 
 def tick_objective(ex, dl, tick, perm, sizes):

@@ -29,6 +29,14 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --c
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
 timeout 300 python bench.py --impl reference --steps 5 --warmup 3 > gpurun_out/bench_ref.json 2> gpurun_out/bench_ref.err
 timeout 600 python bench.py --n 4096 > gpurun_out/bench_n4096.json 2> gpurun_out/bench_n4096.err
+timeout 600 python bench.py --mb 8 > gpurun_out/bench_mb8.json 2> gpurun_out/bench_mb8.err
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_chains -c 1 \
+    -o gpurun_out/k_chains_mb8 python tools/prof_chains.py --bench --mb 8 > gpurun_out/ncu_mb8.log 2>&1
+python tools/ncu_summary.py gpurun_out/k_chains_mb8.ncu-rep --proposals 39321600 --tag ${TAG:-r2} --n 1024 --mb 8 \
+    --out k_chains_summary_n1024_mb8.json --desc "k_chains<1> (N=1024, mb=8, 16384 chains, prof_chains.py --bench --mb 8)" \
+    > /dev/null 2>&1 && cp profiles/${TAG:-r2}/k_chains_summary_n1024_mb8.json gpurun_out/
+[ -n "$ONLINE" ] && timeout 1500 python tools/online_bench.py --n 100000 --policies sa,fcfs,ref \
+    --out gpurun_out/online_config5.json > gpurun_out/online.log 2>&1
 for t in memcheck racecheck synccheck initcheck; do
   timeout 900 compute-sanitizer --tool $t python tools/sanitize_run.py > gpurun_out/san_$t.log 2>&1
 done
