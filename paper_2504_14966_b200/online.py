@@ -112,8 +112,9 @@ class OnlineResult:
                 "overhead_ms_max": float(ov.max())}
 
 
-def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
-    """Plan one instance's queue with the GPU annealer; SLOs shrunk by the time already waited."""
+def window_workload(stream, ids, start_ms):
+    """The planning view of one instance queue at start_ms: each request in a class of its own whose
+    SLO is shrunk by the time it has already waited (the objective every planner optimises)."""
     classes, reqs = [], []
     for k, i in enumerate(ids):
         waited = start_ms - stream.arrival_ms[i]
@@ -124,7 +125,12 @@ def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
         classes.append(TaskClass(k, f"r{i}", slo))
         reqs.append(Request(int(i), k, int(stream.input_len[i]), int(stream.true_out[i]), int(stream.pred_out[i]),
                             float(stream.arrival_ms[i])))
-    w = Workload(reqs, classes)
+    return Workload(reqs, classes)
+
+
+def _plan_sa(stream, ids, start_ms, coeffs, max_batch, cfg: AnnealConfig):
+    """Plan one instance's queue with the GPU annealer; SLOs shrunk by the time already waited."""
+    w = window_workload(stream, ids, start_ms)
     seq, sizes, _, _, _, st = anneal_flat(w, [int(i) for i in ids], coeffs, cfg, max_batch)
     out, pos = [], 0
     for s in sizes:
@@ -160,7 +166,8 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
                coeffs: Optional[LatencyCoefficients] = None, dispatch_gap_ms: float = 0.1,
                max_windows: Optional[int] = None, scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4, 1e5),
                t0: float = 500.0, tau: float = 0.7, iter: int = 30, devices: Sequence[int] = (0,),
-               planner: Optional[Callable] = None, anneal_kw: Optional[Dict] = None) -> OnlineResult:
+               planner: Optional[Callable] = None, anneal_kw: Optional[Dict] = None,
+               snapshots: Optional[List] = None, snapshot_every: int = 50) -> OnlineResult:
     c = coeffs or table_coefficients()
     n = stream.n
     queue: List[List[int]] = [[] for _ in range(n_instances)]
@@ -206,6 +213,8 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
         windows += 1
         # plan every non-empty instance queue (concurrently, one engine context each)
         active = [k for k in range(n_instances) if queue[k]]
+        if snapshots is not None and windows % snapshot_every == 0:  # planning inputs, for offline study
+            snapshots.extend((list(queue[k]), max(busy_until[k], t_win)) for k in active)
         t0_wall = time.perf_counter()
         if policy == "sa":
             # the window's planning (host setup of every instance, kernels, copies) fits the budget:
