@@ -32,12 +32,17 @@ def main():
     ap.add_argument("--n", type=int, default=1024)
     ap.add_argument("--seeds", type=int, default=2)
     ap.add_argument("--ladders", default="1e3..1e7,1e4..1e8,1e5..1e9")
+    ap.add_argument("--schedules", default=None, help="t0:tau:iter,... (default: the built-in list)")
+    ap.add_argument("--workload-seed", type=int, default=0)
+    ap.add_argument("--out", default=None, help="append the rows (JSONL)")
     args = ap.parse_args()
+    scheds = SCHEDULES if not args.schedules else [tuple(float(x) if i < 2 else int(x) for i, x in enumerate(s.split(":")))
+                                                   for s in args.schedules.split(",")]
     c = S.table_coefficients()
-    w = S.generate_mixed(args.n, 0)
+    w = S.generate_mixed(args.n, args.workload_seed)
     ids = w.ids()
     rows = []
-    grid = itertools.product([(k, LADDERS[k]) for k in args.ladders.split(",")], SCHEDULES)
+    grid = itertools.product([(k, LADDERS[k]) for k in args.ladders.split(",")], scheds)
     for (lname, ladder), (t0, tau, it) in grid:
         for chains in (args.chains, args.chains // 4):
             ns, gs = [], []
@@ -48,9 +53,12 @@ def main():
                 ns.append(n_met)
                 gs.append(g)
             row = dict(ladder=lname, t0=t0, tau=tau, iter=it, chains=chains, n_met=ns, g=[f"{x:.5e}" for x in gs],
-                       levels=st.levels_run, g_mean=sum(gs) / len(gs))
+                       levels=st.levels_run, g_mean=sum(gs) / len(gs), n=args.n, workload_seed=args.workload_seed)
             rows.append(row)
             print(json.dumps(row), flush=True)
+            if args.out:
+                with open(args.out, "a") as f:
+                    f.write(json.dumps(row) + "\n")
     best = max(rows, key=lambda r: r["g_mean"])
     print("BEST", json.dumps(best))
 
