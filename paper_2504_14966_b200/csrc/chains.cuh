@@ -278,7 +278,10 @@ constexpr uint32_t kNoMove = 0xffffffffu;  // packed move: op << 30 | pos | b <<
 
 // the batch rebuild of a squeeze (op 0) or delay (op 1) of position pos: batch bounds from one
 // bit search, sizes from the entries
-__device__ __forceinline__ Move range_move(const uint16_t* ent, const uint32_t* bits, int n, uint32_t magic,
+#ifndef SLO_COLD
+#define SLO_COLD __forceinline__  // code only the general path runs (tuning runs: __noinline__)
+#endif
+__device__ SLO_COLD Move range_move(const uint16_t* ent, const uint32_t* bits, int n, uint32_t magic,
                                            uint32_t op, int pos) {
     auto size_at = [&](int q) { return (int)__umulhi(ent[q], magic) + 1; };
     Move mv;
@@ -389,7 +392,7 @@ __device__ __forceinline__ void copy_state(uint16_t* de, uint32_t* db, const uin
 // batch before q's batch is full), of dlb iff a delay of q fails (q's batch is not the last and
 // the next one is full). They change only when an accepted squeeze/delay rebuilds batches, so the
 // draw tests an attempt with one bit instead of a batch-bound search.
-__device__ __forceinline__ void rebuild_flags(const uint16_t* ent, const uint32_t* bits, uint32_t* sqb, uint32_t* dlb,
+__device__ SLO_COLD void rebuild_flags(const uint16_t* ent, const uint32_t* bits, uint32_t* sqb, uint32_t* dlb,
                                               int n, int mb, uint32_t magic, int w0, int w1, int lane) {
     for (int w = w0; w <= w1; ++w) {
         const int q = (w << 5) + lane;
