@@ -55,6 +55,14 @@ constexpr int kRndWords = kAccWord + 1;              // 20 words = 5 Philox bloc
 constexpr int kRndBlocks = kRndWords / 4;
 static_assert(4 * kRndBlocks == kRndWords, "Philox row");
 __device__ __forceinline__ uint32_t pos_word(int j) { return 1 + 2 * j; }
+#ifndef SLO_PHILOX_UNROLL
+#define SLO_PHILOX_UNROLL 1  // rolled: the kernel is instruction-fetch bound (N=1024: 1.31e10 unrolled, 1.47e10 rolled)
+#endif
+constexpr int kPhiloxUnroll = SLO_PHILOX_UNROLL;  // Philox blocks unrolled per row refill
+#ifndef SLO_DECODE_UNROLL
+#define SLO_DECODE_UNROLL 2  // code size: N=1024 1.48e10 at 8, 1.53e10 at 2
+#endif
+constexpr int kDecodeUnroll = SLO_DECODE_UNROLL;  // move attempts unrolled in the speculative decode
 constexpr uint32_t kAlways = 0x80000000u;            // exec-tick flag: deadline +inf at this batch size
 constexpr uint32_t kTickMask = 0x07ffffffu;          // exec ticks < 2^27: 32 of them sum in a u32
 constexpr long long kPadE = 1ll << 62;               // anchor of units past the end (never live)
@@ -769,8 +777,10 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 }
                 __syncwarp();
             };
-            refresh_live();
-            refresh_sig();
+            // the live-prefix summary and caches are refreshed at the start of the next speculative
+            // pass (one inlined copy: the kernel is instruction-fetch bound); every general-path
+            // proposal follows a pass, so it always reads them fresh
+            bool need_refresh = true;
 
             int next_check = 8;
             int pass_it0 = 0, pass_end = 0;  // the speculative pass covering proposals [pass_it0, pass_end)
@@ -792,7 +802,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     if (lane < kRows) {
                         // Philox block b of a row = counter (proposal, chain, b, tag)
                         uint32_t* dst = rnd + rnd_stride<UPL>() * lane;
-#pragma unroll
+#pragma unroll kPhiloxUnroll
                         for (int b = 0; b < kRndBlocks; ++b) {
                             uint32_t r[4] = {prop0 + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
                             philox10(r, p.key0, p.key1);
@@ -825,6 +835,11 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     // path below with the same random words. A general-path rejection leaves the
                     // state bit-identical, so the rest of the pass stays valid; an accept ends it.
                     if (it >= pass_end) {
+                        if (need_refresh) {
+                            refresh_live();
+                            refresh_sig();
+                            need_refresh = false;
+                        }
                         const int G = min(kRows - (it & (kRows - 1)), p.iter - it);
                         const bool on = lane < G;
                         const uint32_t* rl = rnd + rnd_stride<UPL>() * ((it + lane) & (kRows - 1));
@@ -833,6 +848,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         if (on && n >= 2) {
                             // the reference's proposal discipline (P:src/priority_mapper.cpp:184-198)
                             uint32_t ops = lemire32(rl[kOpsWord], 6561u);  // 3^8: the 8 ops as base-3 digits
+#pragma unroll kDecodeUnroll
                             for (int j = 0; j < kAttempts - 1; ++j) {
                                 const uint32_t r1 = rl[pos_word(j)], r2 = rl[pos_word(j) + 1];
                                 const uint32_t op = ops % 3u;
@@ -1167,8 +1183,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     }
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
-                    refresh_live();
-                    refresh_sig();
+                    need_refresh = true;
                     pass_end = 0;  // the state changed: later speculative scores are stale
                     if (f > best_f) {
                         best_f = f;

@@ -68,8 +68,12 @@ __device__ __forceinline__ uint64_t gtimer() {
 }
 
 // Philox4x32-10, Random123 constants.
+#ifndef SLO_PHILOX_ROUNDS_UNROLL
+#define SLO_PHILOX_ROUNDS_UNROLL 10
+#endif
+constexpr int kPhiloxRoundsUnroll = SLO_PHILOX_ROUNDS_UNROLL;
 __host__ __device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
-#pragma unroll
+#pragma unroll kPhiloxRoundsUnroll
     for (int r = 0; r < 10; ++r) {
 #if defined(__CUDA_ARCH__)
         const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), hi1 = __umulhi(0xCD9E8D57u, c[2]);
