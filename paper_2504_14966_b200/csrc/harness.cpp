@@ -17,6 +17,7 @@
 // engine context with a share of the SMs) and the sweep scores every cell's per-instance
 // schedules with one launch of the bit-exact evaluator (evaluate_batch, K1) per instance.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <exception>
@@ -340,19 +341,28 @@ std::vector<ScheduleScore> evaluate_batch(const std::vector<Schedule>& schedules
 // ================================================================ sweep / perturb
 namespace {
 
-// Run jobs(i) for i in [0, count) on concurrent host threads (each job anneals on its own engine
-// context), `slots` of SMs per job; exceptions are rethrown in job order after all finished.
+// At most this many driver cells anneal at once (each on its own engine contexts with a share of
+// the SMs): enough to fill the GPU with the small queues of a sweep, few enough that a large grid
+// neither starves every cell of SMs nor holds hundreds of contexts' buffers.
+constexpr std::size_t kMaxInflightCells = 8;
+
+// Run job(i) for i in [0, count) on up to kMaxInflightCells host threads pulling job indices;
+// exceptions are rethrown in job order after all finished.
 template <typename F>
 void run_concurrent(std::size_t count, F&& job) {
     std::vector<std::exception_ptr> errs(count);
+    std::atomic<std::size_t> next{0};
     std::vector<std::thread> th;
-    th.reserve(count);
-    for (std::size_t i = 0; i < count; ++i)
-        th.emplace_back([&, i] {
-            try {
-                job(i);
-            } catch (...) {
-                errs[i] = std::current_exception();
+    const std::size_t workers = std::min(count, kMaxInflightCells);
+    th.reserve(workers);
+    for (std::size_t w = 0; w < workers; ++w)
+        th.emplace_back([&] {
+            for (std::size_t i; (i = next.fetch_add(1)) < count;) {
+                try {
+                    job(i);
+                } catch (...) {
+                    errs[i] = std::current_exception();
+                }
             }
         });
     for (auto& t : th) t.join();
@@ -360,8 +370,10 @@ void run_concurrent(std::size_t count, F&& job) {
         if (e) std::rethrow_exception(e);
 }
 
-// SMs per anneal when `jobs` schedule_all calls over `k` instances run at once (Chains mode)
+// SMs per anneal when `jobs` schedule_all calls over `k` instances run (at most
+// kMaxInflightCells at once; Chains mode)
 int sm_share(const AnnealConfig& cfg, std::size_t jobs, std::size_t k) {
+    jobs = std::min(jobs, kMaxInflightCells);
     const int dev = detail::resolve_device(cfg.engine.device);
     slo_ctx* ctx = detail::acquire_ctx(dev);
     const int sms = slo_ctx_sm_count(ctx);
