@@ -840,19 +840,26 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                             refresh_sig();
                             need_refresh = false;
                         }
+                        // kLanesPer lanes per proposal (2 where a refill holds 16 rows: the pair splits
+                        // the move attempts and the two batches' gathers); g = the proposal, h = the half
+                        constexpr int kLanesPer = 32 / kRows;
+                        const int g = lane & (kRows - 1), h = lane / kRows;
+                        const unsigned pair = kLanesPer == 1 ? FULL : (1u << g) | (1u << (g + kRows));
                         const int G = min(kRows - (it & (kRows - 1)), p.iter - it);
-                        const bool on = lane < G;
-                        const uint32_t* rl = rnd + rnd_stride<UPL>() * ((it + lane) & (kRows - 1));
+                        const bool on = g < G;
+                        const uint32_t* rl = rnd + rnd_stride<UPL>() * ((it + g) & (kRows - 1));
                         const uint32_t first = __umulhi(ent[0], magic) + 1u;  // size of the first batch
                         uint32_t pk = kNoMove;
+                        int jv = kAttempts - 1;  // the first valid attempt this lane found (8: none)
                         if (on && n >= 2) {
                             // the reference's proposal discipline (P:src/priority_mapper.cpp:184-198)
                             uint32_t ops = lemire32(rl[kOpsWord], 6561u);  // 3^8: the 8 ops as base-3 digits
+                            if (h) ops /= 3u;
 #pragma unroll kDecodeUnroll
-                            for (int j = 0; j < kAttempts - 1; ++j) {
+                            for (int j = h; j < kAttempts - 1; j += kLanesPer) {
                                 const uint32_t r1 = rl[pos_word(j)], r2 = rl[pos_word(j) + 1];
                                 const uint32_t op = ops % 3u;
-                                ops /= 3u;
+                                ops /= kLanesPer == 1 ? 3u : 9u;
                                 const uint32_t a = lemire32(r1, nn);
                                 const uint32_t ps = first + lemire32(r1, nn - first);
                                 uint32_t b = lemire32(r2, nn - 1);
@@ -862,9 +869,17 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 const bool fails = ((op == 0 ? sqb : dlb)[qf >> 5] >> (qf & 31)) & 1u;
                                 if (op == 2u || (!fails && (op == 1u || first < nn))) {
                                     pk = op << 30 | pos | (op == 2u ? b << 13 : 0u);
+                                    jv = j;
                                     break;
                                 }
                             }
+                        }
+                        if constexpr (kLanesPer == 2) {  // the pair's first valid attempt
+                            const int jo = __shfl_xor_sync(FULL, jv, kRows);
+                            const uint32_t po = __shfl_xor_sync(FULL, pk, kRows);
+                            if (jo < jv) pk = po;
+                        }
+                        if (on && n >= 2) {
                             if (pk == kNoMove) {  // the forced swap (attempt 8)
                                 const uint32_t a8 = lemire32(rl[pos_word(kAttempts - 1)], nn);
                                 uint32_t b8 = lemire32(rl[pos_word(kAttempts - 1) + 1], nn - 1);
@@ -888,17 +903,25 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 // the two batches' makespans, and the maxima without the swapped positions
                                 // (4 positions per trip, predicated: the gathers of a trip issue back to back)
                                 uint32_t moa = 0, mxa = 0, mob = 0, mxb = 0;
-                                for (int q0 = 0; q0 <= (int)max(za, zb); q0 += 4) {
+                                // (a lane pair: batch a on the first half, batch b on the second)
+                                const int za_ = kLanesPer == 2 && h ? -1 : (int)za, zb_ = kLanesPer == 2 && !h ? -1 : (int)zb;
+                                for (int q0 = 0; q0 <= max(za_, zb_); q0 += 4) {
 #pragma unroll
                                     for (int j = 0; j < 4; ++j) {
                                         const int qa = sa + q0 + j, qb = sb + q0 + j;
-                                        const bool ina = q0 + j <= (int)za, inb = q0 + j <= (int)zb;
+                                        const bool ina = q0 + j <= za_, inb = q0 + j <= zb_;
                                         const uint32_t xa = ina ? xt_ld<SMEM>(tab, ent[qa]) & kTickMask : 0u;
                                         const uint32_t xb = inb ? xt_ld<SMEM>(tab, ent[qb]) & kTickMask : 0u;
                                         moa = max(moa, xa), mob = max(mob, xb);
                                         if (qa != pa) mxa = max(mxa, xa);
                                         if (qb != pb) mxb = max(mxb, xb);
                                     }
+                                }
+                                if constexpr (kLanesPer == 2) {  // the other half's maxima (0 where not gathered)
+                                    moa = max(moa, __shfl_xor_sync(pair, moa, kRows));
+                                    mxa = max(mxa, __shfl_xor_sync(pair, mxa, kRows));
+                                    mob = max(mob, __shfl_xor_sync(pair, mob, kRows));
+                                    mxb = max(mxb, __shfl_xor_sync(pair, mxb, kRows));
                                 }
                                 const uint32_t voa = xt_ld<SMEM>(tab, ea_), vob = xt_ld<SMEM>(tab, eb_);
                                 const uint32_t vna = xt_ld<SMEM>(tab, na), vnb = xt_ld<SMEM>(tab, nb);
@@ -948,7 +971,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                                 span = (unsigned)(ea - sa + eb - sb + 2);
                             }
                         }
-                        lead_c = __ballot_sync(FULL, rej);
+                        lead_c = __ballot_sync(FULL, rej && h == 0);
                         span_c = span, pk_c = pk;
                         pass_it0 = it, pass_end = it + G;
                     }
