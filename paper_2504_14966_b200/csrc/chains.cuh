@@ -805,7 +805,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
 #pragma unroll kPhiloxUnroll
                         for (int b = 0; b < kRndBlocks; ++b) {
                             uint32_t r[4] = {prop0 + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
-                            philox10(r, p.key0, p.key1);
+                            philox_rounds<SLO_PHILOX_ROUNDS>(r, p.key0, p.key1);
                             if constexpr (rnd_stride<UPL>() % 4 == 0) {
                                 reinterpret_cast<uint4*>(dst)[b] = make_uint4(r[0], r[1], r[2], r[3]);
                             } else {
