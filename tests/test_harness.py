@@ -238,3 +238,19 @@ def test_evaluate_batch_equals_evaluate():
         assert (int(nm[k]), float(t[k]), float(g[k])) == (ev.n, ev.t_ms, ev.g)
     with pytest.raises(S.DataError):
         H.evaluate_batch([plans[0], S.Schedule([w.ids()[:5]])], c, w, 6)
+
+
+@pytest.mark.gpu
+def test_cpp_harness_example():
+    """examples/harness_example.cpp: the harness through the C++ API (Estimator, run_fcfs, compare
+    with GPU chains, evaluate_batch, run)."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "examples", "_build", "harness_example")
+    if not os.path.exists(exe):
+        pytest.skip("example not built")
+    out = subprocess.run([exe, "150"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("PASS") == 5 and "FAIL" not in out.stdout
