@@ -1031,7 +1031,14 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     // final evaluation through the objective; both starts stay a floor, :404-410
     EvaluatedSchedule ev_best = evaluate_owned(std::move(best), c, w);
     const double floor_g = std::max(ev_sorted.g, ev_input.g);
-    if (ev_best.g >= floor_g && (!g_dl || ev_best.g >= *g_dl)) res.best = std::move(ev_best);
+    // Replay mode keeps the reference's ">=" floor (:406-410) bit for bit. In Chains mode the chains'
+    // winner replaces the starts only when it strictly improves the reference's objective -- the
+    // reference's own best-so-far rule (`f > best_f`, :392-400): on an exact tie the start stands,
+    // as it would in the reference's walk (an equal-G plan found on the tick grid is not preferred)
+    const bool strict = eo.mode == SearchMode::Chains;
+    const bool beats = strict ? ev_best.g > floor_g && (!g_dl || ev_best.g > *g_dl)
+                              : ev_best.g >= floor_g && (!g_dl || ev_best.g >= *g_dl);
+    if (beats) res.best = std::move(ev_best);
     else if (g_dl && *g_dl > floor_g) res.best = evaluate(schedule_of(dl_perm, dl_sizes, sorted_ids), c, w);
     else res.best = use_sorted ? std::move(ev_sorted) : std::move(ev_input);
     return res;
