@@ -163,6 +163,10 @@ int slo_chains_fetch(slo_ctx* ctx, int32_t* best_perm, int32_t* best_sizes, int3
 int slo_comm_unique_id(uint8_t id[SLO_COMM_ID_BYTES]);
 int slo_ctx_comm_init(slo_ctx* ctx, int32_t nranks, int32_t rank, const uint8_t id[SLO_COMM_ID_BYTES]);
 int slo_ctx_comm_info(slo_ctx* ctx, int32_t* nranks, int32_t* rank);
+/* A rank that cannot run its slice (an error before its launch) still takes part in the
+ * exchange with an empty slot (n: the job's request count, which fixes the slot size), so the
+ * other ranks are not left waiting in the collective. Collective. */
+int slo_ctx_exchange_empty(slo_ctx* ctx, int32_t n);
 /* ncclCommGetAsyncError of the attached communicator (SLO_ERR_COMM on a failed peer). */
 int slo_comm_check(slo_ctx* ctx);
 

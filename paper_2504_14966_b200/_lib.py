@@ -112,6 +112,7 @@ _SIGNATURES = [
     ("slo_ctx_comm_init", c_int32, [c_void_p, c_int32, c_int32, POINTER(ctypes.c_uint8)]),
     ("slo_ctx_comm_info", c_int32, [c_void_p, _I, _I]),
     ("slo_comm_check", c_int32, [c_void_p]),
+    ("slo_ctx_exchange_empty", c_int32, [c_void_p, c_int32]),
     ("slo_group_create", c_int32, [c_int32, _I, POINTER(c_void_p)]),
     ("slo_group_destroy", None, [c_void_p]),
     ("slo_group_size", c_int32, [c_void_p]),

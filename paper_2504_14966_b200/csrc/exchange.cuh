@@ -247,6 +247,27 @@ int slo_ctx_comm_init(slo_ctx* c, int32_t nranks, int32_t rank, const uint8_t* i
     return SLO_OK;
 }
 
+int slo_ctx_exchange_empty(slo_ctx* c, int32_t n) {
+    if (!c || !c->comm || c->group) return fail(SLO_ERR_ARG, "slo_ctx_exchange_empty: needs a rank context");
+    if (n < 1 || n > SLO_MAX_N) return fail(SLO_ERR_ARG, "slo_ctx_exchange_empty: bad n");
+    CK(cudaSetDevice(c->device));
+    c->UPL = pick_upl(n);
+    const size_t ew = 1024 * (size_t)c->UPL, bw = 32 * (size_t)c->UPL;
+    CK(c->result.reserve(sizeof(ChainResult)));
+    CK(c->win_ent.reserve(ew * sizeof(uint16_t)));
+    CK(c->win_bits.reserve(bw * sizeof(uint32_t)));
+    CK(c->exact_count.reserve(sizeof(unsigned long long)));
+    if (int rc = ex_reserve(c, c->nranks)) return rc;
+    c->empty_slice = true;
+    c->prm.chain_begin = 0;
+    if (int rc = ex_pack(c)) return rc;
+    if (int rc = ex_allgather(c)) return rc;
+    if (int rc = ex_pick(c, c->nranks)) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    c->prepared = false;
+    return SLO_OK;
+}
+
 int slo_ctx_comm_info(slo_ctx* c, int32_t* nranks, int32_t* rank) {
     if (!c) return fail(SLO_ERR_ARG, "slo_ctx_comm_info: null context");
     if (nranks) *nranks = c->nranks;

@@ -11,6 +11,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <future>
 #include <limits>
 #include <map>
@@ -707,6 +708,16 @@ public:
             engine_check(slo_anneal_chains(ctx(), &prm, sp.data(), ss.data(), static_cast<int>(ss.size()), bp.data(),
                                            bs.data(), nb, cr));
         ok_ = true;
+        exchanged_ = true;
+    }
+    // A rank context whose call fails before its exchange joins it with an empty slot, so the
+    // other ranks' collective completes (and they report the job's result without this rank).
+    void abandon(int n) noexcept {
+        if (external_ && !exchanged_ && n >= 1 && n <= SLO_MAX_N) {
+            int32_t nr = 1, rk = 0;
+            if (slo_ctx_comm_info(external_, &nr, &rk) == SLO_OK && nr > 1) slo_ctx_exchange_empty(external_, n);
+        }
+        exchanged_ = true;
     }
 
 private:
@@ -714,6 +725,7 @@ private:
     int device_ = 0;
     std::vector<int> devs_;
     slo_ctx* external_ = nullptr;
+    bool exchanged_ = false;
     CtxPtr ctx_;
     GroupPtr group_;
     bool ok_ = true;
@@ -942,6 +954,16 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     // the engine (context, rank context or device group) gets the tables on the same thread, as
     // soon as they exist
     EngineHandle eng(cfg.engine);
+    // one rank of a multi-process job that fails before its exchange still joins it (EngineHandle::
+    // abandon), so its peers are not left waiting in the collective
+    struct AbandonOnThrow {
+        EngineHandle& e;
+        int n;
+        const int pending = std::uncaught_exceptions();
+        ~AbandonOnThrow() {
+            if (std::uncaught_exceptions() > pending) e.abandon(n);
+        }
+    } abandon_on_throw{eng, n};
     auto tables = std::async(std::launch::async, [&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
         // the upload (context, tables, device-side tick tables) overlaps the deadline-first start

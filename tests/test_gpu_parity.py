@@ -302,6 +302,11 @@ def test_rank_with_empty_slice_takes_part_in_the_exchange():
     e.launch()
     _, _, res = e.fetch()
     assert res.nranks == 1 and res.chains_run == 4 and 0 <= res.chain < 4
+    # a rank that failed before its launch joins the exchange with an empty slot
+    from paper_2504_14966_b200._lib import lib
+    assert lib().slo_ctx_exchange_empty(e._ctx, 64) == 0
+    with pytest.raises(Exception, match="prepared|no chain"):
+        e.fetch()
     e.close()
 
 
