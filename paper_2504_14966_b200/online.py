@@ -167,6 +167,7 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
                max_windows: Optional[int] = None, scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4, 1e5),
                t0: float = 500.0, tau: float = 0.7, iter: int = 30, devices: Sequence[int] = (0,),
                planner: Optional[Callable] = None, anneal_kw: Optional[Dict] = None,
+               chains_per_request: int = 64, chains_min: int = 256,
                snapshots: Optional[List] = None, snapshot_every: int = 50) -> OnlineResult:
     c = coeffs or table_coefficients()
     n = stream.n
@@ -222,8 +223,12 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
             kernel_budget = max(0.5, budget_ms - host_ms - 0.3)
 
             def plan(k):
+                # chains in proportion to the queue (a short queue's search space is tiny: the
+                # ladder then finishes well inside the budget instead of filling it)
+                nq = len(queue[k])
+                ch = min(chains, max(chains_min, chains_per_request * nq))
                 cfg = AnnealConfig(t0=t0, tau=tau, iter=iter, seed=seed * 1_000_003 + windows * 131 + k,
-                                   chains=chains, budget_ms=kernel_budget, scale_ladder=scale_ladder,
+                                   chains=ch, budget_ms=kernel_budget, scale_ladder=scale_ladder,
                                    max_blocks=share[k], device=dev_of[k],
                                    **{"deadline_start": False, **(anneal_kw or {})})
                 return _plan_sa(stream, queue[k], max(busy_until[k], t_win), c, max_batch, cfg)

@@ -8,6 +8,8 @@ per policy realized attainment, average latency, G and the per-window scheduling
 for planning all instances of a window concurrently). Policies:
   sa    the GPU chains, instances placed round-robin on --devices (default: every visible GPU)
   sa-dlstart  the same, with the deadline-first candidate among the chains' starts
+  sa-full     every plan gets all --chains chains (the default sa arm scales them with the queue:
+              64 per request, at least 256, so a short queue's plan ends well inside the budget)
   fcfs  arrival order, greedy batches (the reference's FCFS baseline)
   ref   the UNMODIFIED reference's CPU anneal() (oracle/_ref, default AnnealConfig) per window and
         instance, with the same remaining-slack SLOs the GPU arm plans with -- the reference
@@ -80,6 +82,8 @@ def main():
             kw = dict(policy="custom", planner=reference_planner(seed=args.seed))
         elif pol == "sa-dlstart":  # the chains also start from the deadline-first candidate
             kw = dict(policy="sa", anneal_kw=dict(deadline_start=True))
+        elif pol == "sa-full":  # every window's plan gets all --chains chains (fills the budget)
+            kw = dict(policy="sa", chains_per_request=1 << 30)
         else:
             kw = dict(policy=pol)
         r = O.run_online(stream, n_instances=args.instances, window_ms=args.window_ms, budget_ms=args.budget_ms,
