@@ -139,7 +139,10 @@ def bench_config(args, world):
     return {"workload": f"{cfg_name}: generate_mixed({n}, seed {SEED}) ShareGPT-shaped lengths + estimator "
                         f"predictions, max_batch {mb}, {args.budget_ms} ms scheduling budget per decision, "
                         f"{world} GPU(s)",
-            "n_requests": n, "max_batch": mb, "budget_ms": args.budget_ms, "seed": SEED, "n_gpus": world}
+            "n_requests": n, "max_batch": mb, "budget_ms": args.budget_ms, "seed": SEED, "n_gpus": world,
+            "chains_per_gpu": args.chains,
+            "l2": "GPU arm: L2 flushed between timed steps (512 MiB write on the engine stream); "
+                  "CPU arm: not applicable"}
 
 
 def flat_of(w):
