@@ -274,7 +274,7 @@ def test_bench_reference_arm_line():
     import argparse
     sys.path.insert(0, ROOT)
     import bench
-    assert line["config"] == bench.bench_config(argparse.Namespace(n=256, mb=4, budget_ms=10.0), 1)
+    assert line["config"] == bench.bench_config(argparse.Namespace(n=256, mb=4, budget_ms=10.0, chains=16384), 1)
 
 
 def test_bench_reference_arm_never_loads_the_product():
