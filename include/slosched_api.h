@@ -187,6 +187,36 @@ int slosched_evaluate_batch(const slosched_workload* w, const double* coeffs8, i
                             const int32_t* ids, const int32_t* sizes, const int32_t* nb, int32_t max_batch,
                             int32_t* n_met, double* t, double* g);
 
+/* run_online (include/slosched_b200.hpp "online rescheduling"): the stream as arrays (arrival
+ * order), the result and up to overhead_cap per-window planning times (ms). policy: 0 SA, 2 FCFS. */
+typedef struct {
+    int32_t policy, n_instances;
+    double window_ms;
+    int32_t max_batch;
+    double budget_ms;
+    int32_t chains, chains_per_request, chains_min;
+    uint64_t seed;
+    double dispatch_gap_ms;
+    int32_t n_devices;
+    const int32_t* devices;
+    int32_t n_scale_ladder;
+    const double* scale_ladder;
+    double t0, tau;
+    int32_t iter, deadline_start, max_windows;
+} slosched_online_config;
+
+typedef struct {
+    int32_t n, n_met;
+    double total_latency_ms;
+    int32_t windows, decisions;
+    uint64_t proposals;
+} slosched_online_result;
+
+int slosched_run_online(int32_t n, const double* arrival_ms, const int32_t* cls, const int32_t* input_len,
+                        const int32_t* true_out, const int32_t* pred_out, const double* coeffs8,
+                        const slosched_online_config* cfg, slosched_online_result* out, double* overhead_ms,
+                        int32_t overhead_cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -440,6 +440,42 @@ std::vector<PerturbRow> perturb(const std::vector<Workload>& per_seed, const std
                                 const AnnealConfig& base_cfg, const SimConfig& sim_cfg,
                                 const std::vector<std::string>& params, const std::vector<double>& factors);
 
+// ---------------------------------------------------------------- online rescheduling
+// (engine extension, BASELINE configs[4]; the reference has no online mode) A request
+// stream (arrival order) served by n_instances instances: arrivals join the least-loaded
+// instance, every window_ms each instance's queue is re-planned -- GPU chains under the window's
+// budget (SLOs less the time already waited), or FCFS -- and run on the replay until the next
+// window boundary. Stream classes: 0 = code (E2E 30 s), 1 = chat (TTFT 10 s + TPOT 50 ms).
+struct OnlineStream {
+    std::vector<double> arrival_ms;
+    std::vector<int> cls, input_len, true_out, pred_out;
+};
+struct OnlineConfig {
+    Policy policy = Policy::SA;          // SA (GPU chains) or FCFS
+    int n_instances = 8;
+    double window_ms = 5000.0;
+    int max_batch = 4;
+    double budget_ms = 10.0;             // per window, all instances' planning together
+    int chains = 4096;                   // per plan at most; in proportion to the queue:
+    int chains_per_request = 64, chains_min = 256;
+    std::uint64_t seed = 0;
+    double dispatch_gap_ms = 0.1;
+    std::vector<int> devices;            // instance i on devices[i % size] (empty: the default device)
+    std::vector<double> scale_ladder = {1.0, 10.0, 100.0, 1000.0, 1e4, 1e5};
+    double t0 = 500.0, tau = 0.7;
+    int iter = 30;
+    bool deadline_start = false;
+    int max_windows = -1;                // < 0: until every request has started
+};
+struct OnlineResult {
+    int n = 0, n_met = 0;
+    double total_latency_ms = 0.0;
+    int windows = 0, decisions = 0;
+    std::uint64_t proposals = 0;
+    std::vector<double> overhead_ms;     // wall time of each window's planning
+};
+OnlineResult run_online(const OnlineStream& stream, const LatencyCoefficients& coeffs, const OnlineConfig& cfg);
+
 // ---------------------------------------------------------------- synthetic inputs
 struct LengthDists {
     double code_input_median = 300.0, code_input_sigma = 0.5;

@@ -85,6 +85,20 @@ class SloRow(Structure):
                 ("overhead_ms", c_double)]
 
 
+class SloOnlineConfig(Structure):
+    _fields_ = [("policy", c_int32), ("n_instances", c_int32), ("window_ms", c_double), ("max_batch", c_int32),
+                ("budget_ms", c_double), ("chains", c_int32), ("chains_per_request", c_int32),
+                ("chains_min", c_int32), ("seed", c_uint64), ("dispatch_gap_ms", c_double),
+                ("n_devices", c_int32), ("devices", POINTER(c_int32)), ("n_scale_ladder", c_int32),
+                ("scale_ladder", POINTER(c_double)), ("t0", c_double), ("tau", c_double), ("iter", c_int32),
+                ("deadline_start", c_int32), ("max_windows", c_int32)]
+
+
+class SloOnlineResult(Structure):
+    _fields_ = [("n", c_int32), ("n_met", c_int32), ("total_latency_ms", c_double), ("windows", c_int32),
+                ("decisions", c_int32), ("proposals", c_uint64)]
+
+
 _I = POINTER(c_int32)
 _D = POINTER(c_double)
 
@@ -156,6 +170,8 @@ _SIGNATURES = [
     ("slosched_perturb", c_int32, [c_int32, c_int32, c_int32, POINTER(c_uint64), POINTER(SloFleet), _D,
                                    POINTER(SloAnnealConfig), POINTER(SloSimConfig), c_int32, POINTER(c_char_p),
                                    c_int32, _D, _D, _D, _D]),
+    ("slosched_run_online", c_int32, [c_int32, _D, _I, _I, _I, _I, _D, POINTER(SloOnlineConfig),
+                                      POINTER(SloOnlineResult), _D, c_int32]),
     ("slosched_evaluate_batch", c_int32, [POINTER(SloWorkload), _D, c_int32, c_int32, _I, _I, _I, c_int32, _I, _D,
                                           _D]),
 ]

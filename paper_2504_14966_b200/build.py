@@ -26,7 +26,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-fmad=false", "-std=c++17", "-Xcompile
 NVCC_FLAGS += os.environ.get("SLO_EXTRA_NVCC", "").split()  # e.g. -DSLO_CHAIN_THREADS=640 (tuning runs)
 CXX_FLAGS = ["-std=c++17", "-O2", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra", f"-I{INC}"]
 
-HOST_SRCS = ["host.cpp", "capi.cpp", "harness.cpp"]
+HOST_SRCS = ["host.cpp", "capi.cpp", "harness.cpp", "online.cpp"]
 CUDA_SRCS = ["engine.cu"]
 
 

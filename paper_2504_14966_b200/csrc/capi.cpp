@@ -1,4 +1,5 @@
 // Flat C ABI (include/slosched_api.h) over the C++ scheduler API.
+#include <algorithm>
 #include <cstring>
 #include <exception>
 #include <string>
@@ -483,6 +484,33 @@ int slosched_evaluate_batch(const slosched_workload* w, const double* c, int32_t
         }
         const auto sc = evaluate_batch(sch, coeffs_of(c), wl, max_batch);
         for (int s = 0; s < n_sched; ++s) n_met[s] = sc[s].n, t[s] = sc[s].t_ms, g[s] = sc[s].g;
+    });
+}
+
+int slosched_run_online(int32_t n, const double* arrival_ms, const int32_t* cls, const int32_t* input_len,
+                        const int32_t* true_out, const int32_t* pred_out, const double* c,
+                        const slosched_online_config* cfg, slosched_online_result* out, double* overhead_ms,
+                        int32_t overhead_cap) {
+    return guarded([&] {
+        if (!cfg || !out) throw std::invalid_argument("run_online: null argument");
+        OnlineStream st;
+        st.arrival_ms.assign(arrival_ms, arrival_ms + n);
+        st.cls.assign(cls, cls + n), st.input_len.assign(input_len, input_len + n);
+        st.true_out.assign(true_out, true_out + n), st.pred_out.assign(pred_out, pred_out + n);
+        OnlineConfig oc;
+        if (cfg->policy != 0 && cfg->policy != 2) throw DataError("run_online: policy must be 0 (SA) or 2 (FCFS)");
+        oc.policy = static_cast<Policy>(cfg->policy);
+        oc.n_instances = cfg->n_instances, oc.window_ms = cfg->window_ms, oc.max_batch = cfg->max_batch;
+        oc.budget_ms = cfg->budget_ms, oc.chains = cfg->chains, oc.chains_per_request = cfg->chains_per_request;
+        oc.chains_min = cfg->chains_min, oc.seed = cfg->seed, oc.dispatch_gap_ms = cfg->dispatch_gap_ms;
+        if (cfg->n_devices > 0) oc.devices.assign(cfg->devices, cfg->devices + cfg->n_devices);
+        if (cfg->n_scale_ladder > 0) oc.scale_ladder.assign(cfg->scale_ladder, cfg->scale_ladder + cfg->n_scale_ladder);
+        oc.t0 = cfg->t0, oc.tau = cfg->tau, oc.iter = cfg->iter, oc.deadline_start = cfg->deadline_start != 0;
+        oc.max_windows = cfg->max_windows;
+        const OnlineResult r = run_online(st, coeffs_of(c), oc);
+        *out = slosched_online_result{r.n, r.n_met, r.total_latency_ms, r.windows, r.decisions, r.proposals};
+        for (int i = 0; i < std::min<int>(overhead_cap, static_cast<int>(r.overhead_ms.size())); ++i)
+            overhead_ms[i] = r.overhead_ms[i];
     });
 }
 

@@ -169,6 +169,46 @@ def run_online(stream: Stream, policy: str = "sa", n_instances: int = 8, window_
                planner: Optional[Callable] = None, anneal_kw: Optional[Dict] = None,
                chains_per_request: int = 64, chains_min: int = 256,
                snapshots: Optional[List] = None, snapshot_every: int = 50) -> OnlineResult:
+    """The online driver. "sa" and "fcfs" run in the library (csrc/online.cpp, slosched_run_online);
+    a caller's planner ("custom"), snapshot capture or engine options other than deadline_start run
+    the same loop in Python (_run_online_py; identical results on the same inputs)."""
+    kw = dict(anneal_kw or {})
+    native = (policy in ("sa", "fcfs") and planner is None and snapshots is None and set(kw) <= {"deadline_start"})
+    if not native:
+        return _run_online_py(stream, policy, n_instances, window_ms, max_batch, budget_ms, chains, seed, coeffs,
+                              dispatch_gap_ms, max_windows, scale_ladder, t0, tau, iter, devices, planner, anneal_kw,
+                              chains_per_request, chains_min, snapshots, snapshot_every)
+    import ctypes
+
+    from ._lib import SloOnlineConfig, SloOnlineResult, lib
+    from .slosched import _check_api, _f64, _i32, _p
+    c = coeffs or table_coefficients()
+    devs = _i32(list(devices) or [0])
+    lad = _f64(list(scale_ladder) or [1.0])
+    cfg = SloOnlineConfig(0 if policy == "sa" else 2, n_instances, window_ms, max_batch, budget_ms, chains,
+                          chains_per_request, chains_min, seed & (2**64 - 1), dispatch_gap_ms, len(devs), _p(devs),
+                          len(lad), _p(lad, ctypes.c_double), t0, tau, iter, 1 if kw.get("deadline_start") else 0,
+                          -1 if max_windows is None else max_windows)
+    arr = _f64(stream.arrival_ms)
+    cap = int(np.ceil((arr[-1] if len(arr) else 0.0) / window_ms)) + stream.n + 16
+    ovh = np.zeros(cap)
+    out = SloOnlineResult()
+    _check_api(lib().slosched_run_online(stream.n, _p(arr, ctypes.c_double), _p(_i32(stream.cls)),
+                                         _p(_i32(stream.input_len)), _p(_i32(stream.true_out)),
+                                         _p(_i32(stream.pred_out)), _p(c.as_array(), ctypes.c_double),
+                                         ctypes.byref(cfg), ctypes.byref(out), _p(ovh, ctypes.c_double), cap))
+    return OnlineResult(policy, out.n, out.n_met, out.total_latency_ms, out.windows, out.decisions, int(out.proposals),
+                        list(ovh[:min(out.windows, cap)]))
+
+
+def _run_online_py(stream: Stream, policy: str = "sa", n_instances: int = 8, window_ms: float = 5000.0,
+               max_batch: int = 4, budget_ms: float = 10.0, chains: int = 4096, seed: int = 0,
+               coeffs: Optional[LatencyCoefficients] = None, dispatch_gap_ms: float = 0.1,
+               max_windows: Optional[int] = None, scale_ladder=(1.0, 10.0, 100.0, 1000.0, 1e4, 1e5),
+               t0: float = 500.0, tau: float = 0.7, iter: int = 30, devices: Sequence[int] = (0,),
+               planner: Optional[Callable] = None, anneal_kw: Optional[Dict] = None,
+               chains_per_request: int = 64, chains_min: int = 256,
+               snapshots: Optional[List] = None, snapshot_every: int = 50) -> OnlineResult:
     c = coeffs or table_coefficients()
     n = stream.n
     queue: List[List[int]] = [[] for _ in range(n_instances)]

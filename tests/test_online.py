@@ -53,6 +53,19 @@ def test_custom_planner_and_devices():
         O.run_online(s, "custom", n_instances=2)
 
 
+@pytest.mark.parametrize("n_inst,window,mb,gap,maxw", [(3, 4000.0, 4, 0.1, None), (2, 1500.0, 8, 0.0, None),
+                                                       (5, 7000.0, 2, 0.5, 6)])
+def test_native_driver_matches_the_python_loop(n_inst, window, mb, gap, maxw):
+    """slosched_run_online (csrc/online.cpp) and the Python loop agree on FCFS, request for request."""
+    s = O.make_stream(600, rate_per_s=0.8 * n_inst * O.service_rate_per_s(), seed=11)
+    kw = dict(n_instances=n_inst, window_ms=window, max_batch=mb, dispatch_gap_ms=gap, max_windows=maxw)
+    nat = O.run_online(s, "fcfs", **kw)
+    py = O._run_online_py(s, "fcfs", **kw)
+    assert (nat.n, nat.n_met, nat.windows, nat.decisions) == (py.n, py.n_met, py.windows, py.decisions)
+    assert nat.total_latency_ms == pytest.approx(py.total_latency_ms, rel=1e-12)
+    assert len(nat.overhead_ms) == nat.windows
+
+
 @pytest.mark.gpu
 def test_online_sa_beats_fcfs():
     mu = O.service_rate_per_s()
@@ -62,3 +75,5 @@ def test_online_sa_beats_fcfs():
     assert sa.n == fc.n == 1500
     assert sa.n_met >= fc.n_met
     assert max(sa.overhead_ms) < 1000.0
+    py = O._run_online_py(s, "sa", n_instances=2, window_ms=5000.0, budget_ms=3.0, chains=1024)
+    assert py.n == 1500 and py.n_met >= fc.n_met
