@@ -23,6 +23,7 @@
 #include <climits>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <mutex>
@@ -176,6 +177,9 @@ __global__ void k_eval_exact(int count, int n, int mb, int words, const uint16_t
 
 // ================================================================ K3: chains
 #include "chains.cuh"
+
+// ================================================================ K5: chains, short queues
+#include "chains_small.cuh"
 
 // ================================================================ K2: exact replay
 #include "replay.cuh"
@@ -342,6 +346,7 @@ struct slo_ctx {
     int UPL = 1, grid = 0, block = 0, levels = 0, chain_count = 0;
     size_t smem = 0;
     bool smem_tab = false;
+    bool small = false;  // K5 (n <= 32) instead of K3
     double replay_scale = 0.0;
     int start_nb = 0;
     ChainParams kp{};
@@ -649,8 +654,63 @@ void launch_t(slo_ctx* c) {
     else k_chains<UPL, false, false><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
 }
 
+// K5: one chain per warp spread over as many SMs as the launch may use (a short queue's chain is
+// latency-bound: fewer warps per scheduler is faster), the block's tables in shared memory
+template <bool NEG, int MB>
+int configure_small_t(slo_ctx* c) {
+    constexpr auto K = k_chains_small<NEG, MB>;
+    const size_t tab = ((size_t)c->n * c->mb * 12 + 15) & ~(size_t)15;
+    int avail = c->sm_count;
+    if (c->prm.max_blocks > 0) avail = std::min(avail, c->prm.max_blocks);
+    const int W = std::max(1, std::min(kSmallThreads / 32, (c->chain_count + avail - 1) / avail));
+    c->smem = tab + (size_t)W * small_warp_bytes();
+    CK(ensure_smem_attr<K>(c->device, dyn_smem_max<K>(c)));
+    int occ = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, K, W * 32, c->smem));
+    if (occ < 1) return fail(SLO_ERR_CAPACITY, "slo_anneal_chains: short-queue kernel does not fit on an SM");
+    c->block = W * 32;
+    c->grid = std::min((c->chain_count + W - 1) / W, c->sm_count * occ);
+    if (c->prm.max_blocks > 0) c->grid = std::min(c->grid, c->prm.max_blocks);
+    return SLO_OK;
+}
+
+template <bool NEG, int MB>
+void launch_small_t(slo_ctx* c) {
+    const size_t ss = 32 * 12 + 1024 * 2 + 16 + 32 * 4 + 16;
+    k_start<1, NEG><<<1, 32, ss, c->stream>>>(c->kp);
+    k_chains_small<NEG, MB><<<c->grid, c->block, c->smem, c->stream>>>(c->kp);
+}
+
+// the segmented-max depth: the power of two >= mb
+template <bool NEG, template <bool, int> class F, typename R = int>
+R small_dispatch(slo_ctx* c) {
+    const int mb = c->mb;
+    if (mb <= 1) return F<NEG, 1>::run(c);
+    if (mb <= 2) return F<NEG, 2>::run(c);
+    if (mb <= 4) return F<NEG, 4>::run(c);
+    if (mb <= 8) return F<NEG, 8>::run(c);
+    return F<NEG, 16>::run(c);
+}
+template <bool NEG, int MB>
+struct SmallConfigure {
+    static int run(slo_ctx* c) { return configure_small_t<NEG, MB>(c); }
+};
+template <bool NEG, int MB>
+struct SmallLaunch {
+    static int run(slo_ctx* c) {
+        launch_small_t<NEG, MB>(c);
+        return 0;
+    }
+};
+
 // prologue (start-state summaries, one warp) then the chain kernel
 int launch_chains_U(slo_ctx* c) {
+    if (c->small) {
+        if (c->cofs > 0) small_dispatch<true, SmallLaunch>(c);
+        else small_dispatch<false, SmallLaunch>(c);
+        CK(cudaGetLastError());
+        return SLO_OK;
+    }
     switch (c->UPL) {
         case 1: launch_t<1>(c); break;
         case 2: launch_t<2>(c); break;
@@ -666,6 +726,8 @@ size_t chain_state_bytes(int upl) {
 }
 
 int configure_U(slo_ctx* c) {
+    if (c->small)
+        return c->cofs > 0 ? small_dispatch<true, SmallConfigure>(c) : small_dispatch<false, SmallConfigure>(c);
     switch (c->UPL) {
         case 1: return configure_chains<1>(c);
         case 2: return configure_chains<2>(c);
@@ -768,6 +830,10 @@ int slo_chains_prepare(slo_ctx* c, const slo_chain_params* prm, const int32_t* s
 
     const int UPL = pick_upl(n);
     c->UPL = UPL;
+    {  // K5 for short queues (SLOSCHED_SMALL_KERNEL=0 keeps K3: the equivalence tests run both)
+        const char* ev = std::getenv("SLOSCHED_SMALL_KERNEL");
+        c->small = n <= kSmallMaxN && c->mb <= 16 && !(ev && ev[0] == '0');
+    }
     const size_t ent_words = 1024 * (size_t)UPL, bit_words = 32 * (size_t)UPL;
     if (empty) {  // only the exchange buffers: the slot says "no chain"
         CK(c->result.reserve(sizeof(ChainResult)));

@@ -10,6 +10,8 @@ for planning all instances of a window concurrently). Policies:
   sa-dlstart  the same, with the deadline-first candidate among the chains' starts
   sa-full     every plan gets all --chains chains (the default sa arm scales them with the queue:
               64 per request, at least 256, so a short queue's plan ends well inside the budget)
+  sa-py the sa arm through the Python dispatch loop (online._run_online_py) instead of the library's
+        slosched_run_online: same plans, host overhead of the Python loop
   fcfs  arrival order, greedy batches (the reference's FCFS baseline)
   ref   the UNMODIFIED reference's CPU anneal() (oracle/_ref, default AnnealConfig) per window and
         instance, with the same remaining-slack SLOs the GPU arm plans with -- the reference
@@ -86,7 +88,10 @@ def main():
             kw = dict(policy="sa", chains_per_request=1 << 30)
         else:
             kw = dict(policy=pol)
-        r = O.run_online(stream, n_instances=args.instances, window_ms=args.window_ms, budget_ms=args.budget_ms,
+        fn = O.run_online
+        if pol == "sa-py":
+            kw, fn = dict(policy="sa"), O._run_online_py
+        r = fn(stream, n_instances=args.instances, window_ms=args.window_ms, budget_ms=args.budget_ms,
                          chains=args.chains, seed=args.seed, devices=devices, **kw)
         s = r.summary()
         s["policy"] = pol
