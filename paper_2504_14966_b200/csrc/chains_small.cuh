@@ -20,7 +20,7 @@
 // does (stride 20 words).
 
 constexpr int kSmallMaxN = 32;
-constexpr int kSmallThreads = 512;  // 16 warps: 128 registers (1024 threads cap them at 64)
+constexpr int kSmallThreads = 768;  // 24 warps (85 registers; 1024 threads cap them at 64, 512 park chains under an SM share)
 
 struct SmallScore {
     long long tot;  // total latency (ticks)

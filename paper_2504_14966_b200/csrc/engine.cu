@@ -374,6 +374,12 @@ void slo_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
     for (int i = 0; i < 4; ++i) out[i] = c[i];
 }
 
+}  // extern "C"
+namespace {
+void prewarm_kernels(slo_ctx* c);
+}
+extern "C" {
+
 int slo_ctx_create(int device, slo_ctx** out) {
     if (!out) return fail(SLO_ERR_ARG, "slo_ctx_create: null out");
     int ndev = 0;
@@ -396,6 +402,7 @@ int slo_ctx_create(int device, slo_ctx** out) {
         delete c;
         return fail(SLO_ERR_CUDA, std::string("slo_ctx_create: ") + cudaGetErrorString(e));
     }
+    prewarm_kernels(c);
     *out = c;
     return SLO_OK;
 }
@@ -734,6 +741,40 @@ int configure_U(slo_ctx* c) {
         case 4: return configure_chains<4>(c);
     }
     return fail(SLO_ERR_CAPACITY, "bad units-per-lane");
+}
+
+// Load every kernel of the annealing path (and raise its shared-memory limit) once per device when
+// the first context is created: with lazy module loading the first launch of each kernel otherwise
+// pays for its load inside a timed decision (online windows: one-off 10-35 ms planning outliers
+// the first time a queue size needs another kernel variant).
+template <void (*K)(ChainParams)>
+void warm_chain_kernel(slo_ctx* c) {
+    ensure_smem_attr<K>(c->device, dyn_smem_max<K>(c));
+}
+template <typename F>
+void warm_fn(F* f) {
+    cudaFuncAttributes a{};
+    cudaFuncGetAttributes(&a, f);
+}
+void prewarm_kernels(slo_ctx* c) {
+    static std::mutex mu;
+    static bool done[64] = {};
+    std::lock_guard<std::mutex> g(mu);
+    if (c->device < 0 || c->device >= 64 || done[c->device]) return;
+    done[c->device] = true;
+    warm_chain_kernel<k_chains<1, true, false>>(c), warm_chain_kernel<k_chains<1, false, false>>(c);
+    warm_chain_kernel<k_chains<1, false, true>>(c), warm_chain_kernel<k_chains<2, true, false>>(c);
+    warm_chain_kernel<k_chains<2, false, false>>(c), warm_chain_kernel<k_chains<2, false, true>>(c);
+    warm_chain_kernel<k_chains<4, true, false>>(c), warm_chain_kernel<k_chains<4, false, false>>(c);
+    warm_chain_kernel<k_chains<4, false, true>>(c);
+    warm_chain_kernel<k_chains_small<false, 1>>(c), warm_chain_kernel<k_chains_small<false, 2>>(c);
+    warm_chain_kernel<k_chains_small<false, 4>>(c), warm_chain_kernel<k_chains_small<false, 8>>(c);
+    warm_chain_kernel<k_chains_small<false, 16>>(c), warm_chain_kernel<k_chains_small<true, 1>>(c);
+    warm_chain_kernel<k_chains_small<true, 2>>(c), warm_chain_kernel<k_chains_small<true, 4>>(c);
+    warm_chain_kernel<k_chains_small<true, 8>>(c), warm_chain_kernel<k_chains_small<true, 16>>(c);
+    warm_fn(k_start<1, false>), warm_fn(k_start<1, true>), warm_fn(k_start<2, false>), warm_fn(k_start<2, true>);
+    warm_fn(k_start<4, false>), warm_fn(k_start<4, true>), warm_fn(k_argmax), warm_fn(k_tables);
+    cudaGetLastError();  // (a failure here surfaces again, with its message, at the launch)
 }
 
 }  // namespace

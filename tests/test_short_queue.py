@@ -88,7 +88,7 @@ def test_short_queue_kernel_matches_k3(eng, n, mb, chains, max_blocks):
     assert k5 == k3
 
 
-@pytest.mark.parametrize("n,mb,delta_p", [(24, 4, -400.0), (11, 8, -2500.0)])
+@pytest.mark.parametrize("n,mb,delta_p", [(24, 4, -400.0), (11, 8, -2500.0), (7, 4, -2500.0)])
 def test_short_queue_kernel_negative_exec(eng, n, mb, delta_p):
     base = S.table_coefficients()
     c = S.LatencyCoefficients(base.alpha_p, base.beta_p, base.gamma_p, delta_p, base.alpha_d, base.beta_d,
@@ -145,3 +145,14 @@ def test_short_queues_through_the_public_api():
         finally:
             os.environ.pop("SLOSCHED_SMALL_KERNEL", None)
         assert r.best.schedule.batches == r3.best.schedule.batches and r.best.g == r3.best.g
+
+
+def test_short_queue_budget_stops_early():
+    c = S.table_coefficients()
+    w = _three_class(7, 6)  # (the sorted start misses SLOs: no shortcut)
+    cfg = S.AnnealConfig(t0=500.0, tau=0.99, iter=2000, chains=256, budget_ms=0.2, seed=1)
+    r = S.anneal(w, w.ids(), c, cfg, 4)
+    assert 0 < r.stats.proposals < 256 * 2000 * r.stats.levels_run + 1
+    assert r.stats.kernel_ms < 0.2 + 0.1
+    assert r.best.schedule.is_partition_of(w.ids(), 4)
+    assert r.best.g >= max(r.stats.g_sorted_start, r.stats.g_input_start)
