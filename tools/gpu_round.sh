@@ -35,6 +35,12 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ch
 python tools/ncu_summary.py gpurun_out/k_chains_mb8.ncu-rep --proposals 39321600 --tag ${TAG:-r2} --n 1024 --mb 8 \
     --out k_chains_summary_n1024_mb8.json --desc "k_chains<1> (N=1024, mb=8, 16384 chains, prof_chains.py --bench --mb 8)" \
     > /dev/null 2>&1 && cp profiles/${TAG:-r2}/k_chains_summary_n1024_mb8.json gpurun_out/
+# the short-queue kernel (K5) at an online window's shape (n=6: 384 chains x 10 levels x 30 = 115200)
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:k_chains_small -c 1 \
+    -o gpurun_out/k5_n6 python tools/prof_small.py 6 > gpurun_out/ncu_k5.log 2>&1
+python tools/ncu_summary.py gpurun_out/k5_n6.ncu-rep --proposals 115200 --tag ${TAG:-r2} --n 6 --mb 4 \
+    --out k5_summary_n6.json --desc "k_chains_small (N=6, mb=4, 384 chains, tools/prof_small.py 6)" \
+    > /dev/null 2>&1 && cp profiles/${TAG:-r2}/k5_summary_n6.json gpurun_out/
 [ -n "$ONLINE" ] && timeout 1500 python tools/online_bench.py --n 100000 --policies sa,fcfs,ref \
     --out gpurun_out/online_config5.json > gpurun_out/online.log 2>&1
 for t in memcheck racecheck synccheck initcheck; do

@@ -31,4 +31,23 @@ S.exhaustive(w, w.ids(), c, 2)
 # more chains than resident warps: exercises parking
 w = S.generate_mixed(64, 9)
 S.anneal(w, w.ids(), c, S.AnnealConfig(seed=3, chains=148 * 24 + 50, t0=30.0, iter=8), 4)
+# short queues (K5): every segmented-max depth, negative execs, parked chains, the fp64 path
+for n, mb in [(6, 1), (12, 2), (9, 4), (20, 8), (31, 16)]:
+    w = S.generate_mixed(n, 40 + n)
+    S.anneal(w, w.ids(), c, S.AnnealConfig(seed=4, chains=96, t0=500.0, iter=30, scale_ladder=(1.0, 1e4)), mb)
+base = S.table_coefficients()
+cneg = S.LatencyCoefficients(base.alpha_p, base.beta_p, base.gamma_p, -2500.0, base.alpha_d, base.beta_d,
+                             base.gamma_d, base.delta_d)
+w = S.generate_mixed(11, 101)
+S.anneal(w, w.ids(), cneg, S.AnnealConfig(seed=5, chains=64, t0=100.0, iter=30, max_blocks=1), 8)
+eng = E.Engine(0)
+n = 16
+w = S.generate_mixed(n, 5)
+ex, dl = E.build_tables(w, w.ids(), c, 1)
+dl = dl.copy()
+dl[0] = np.cumsum(ex[0])[np.arange(n) % (n - 1)]
+eng.set_problem(ex, dl)
+eng.anneal_chains(list(range(n)), [1] * n, chains=100, t0=200.0, t_thres=20.0, tau=0.7, iter=30, seed=5,
+                  objective_scale=1e4, max_blocks=1)
+eng.close()
 print("sanitize run complete")
