@@ -493,6 +493,10 @@ int slosched_run_online(int32_t n, const double* arrival_ms, const int32_t* cls,
                         int32_t overhead_cap) {
     return guarded([&] {
         if (!cfg || !out) throw std::invalid_argument("run_online: null argument");
+        if (n < 0) throw DataError("run_online: negative request count");
+        if (n > 0 && (!arrival_ms || !cls || !input_len || !true_out || !pred_out))
+            throw std::invalid_argument("run_online: null stream array");
+        if (overhead_cap > 0 && !overhead_ms) throw std::invalid_argument("run_online: null overhead_ms");
         OnlineStream st;
         st.arrival_ms.assign(arrival_ms, arrival_ms + n);
         st.cls.assign(cls, cls + n), st.input_len.assign(input_len, input_len + n);

@@ -108,11 +108,16 @@ OnlineResult run_online(const OnlineStream& st, const LatencyCoefficients& c, co
     const int k = cfg.n_instances;
     if (k < 1) throw DataError("run_online: need at least one instance");
     if (!(cfg.window_ms > 0.0)) throw DataError("run_online: window_ms must be > 0");
+    if (cfg.max_batch < 1) throw DataError("run_online: max_batch must be >= 1");
+    if (!(cfg.dispatch_gap_ms >= 0.0)) throw DataError("run_online: dispatch_gap_ms must be >= 0");
     if (cfg.policy != Policy::SA && cfg.policy != Policy::FCFS)
         throw std::invalid_argument("run_online: policy must be SA or FCFS");
     if (st.cls.size() != (size_t)n || st.input_len.size() != (size_t)n || st.true_out.size() != (size_t)n ||
         st.pred_out.size() != (size_t)n)
         throw DataError("run_online: stream arrays differ in length");
+    for (int i = 0; i < n; ++i)
+        if (!std::isfinite(st.arrival_ms[i]) || st.arrival_ms[i] < 0.0 || (i > 0 && st.arrival_ms[i] < st.arrival_ms[i - 1]))
+            throw DataError("run_online: arrival times must be finite, >= 0 and nondecreasing");
     const std::vector<int> devs = cfg.devices.empty() ? std::vector<int>{detail::resolve_device(-1)} : cfg.devices;
     std::vector<int> dev_of(k), share(k, 0);
     for (int i = 0; i < k; ++i) dev_of[i] = devs[i % devs.size()];

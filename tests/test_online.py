@@ -77,3 +77,17 @@ def test_online_sa_beats_fcfs():
     assert max(sa.overhead_ms) < 1000.0
     py = O._run_online_py(s, "sa", n_instances=2, window_ms=5000.0, budget_ms=3.0, chains=1024)
     assert py.n == 1500 and py.n_met >= fc.n_met
+
+
+def test_native_driver_rejects_bad_input():
+    import numpy as np
+
+    from paper_2504_14966_b200.slosched import DataError
+    s = O.make_stream(50, rate_per_s=0.5, seed=2)
+    with pytest.raises(DataError):
+        O.run_online(s, "fcfs", n_instances=2, max_batch=0)
+    with pytest.raises(DataError):
+        O.run_online(s, "fcfs", n_instances=0)
+    bad = O.Stream(**{**s.__dict__, "arrival_ms": np.asarray(s.arrival_ms)[::-1].copy()})
+    with pytest.raises(DataError):
+        O.run_online(bad, "fcfs", n_instances=2)
