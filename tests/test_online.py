@@ -91,3 +91,17 @@ def test_native_driver_rejects_bad_input():
     bad = O.Stream(**{**s.__dict__, "arrival_ms": np.asarray(s.arrival_ms)[::-1].copy()})
     with pytest.raises(DataError):
         O.run_online(bad, "fcfs", n_instances=2)
+
+
+@pytest.mark.gpu
+def test_cpp_online_example():
+    """examples/online_example.cpp: the online driver through the C++ API (GPU chains vs FCFS)."""
+    import os
+    import subprocess
+
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "examples", "_build", "online_example")
+    assert os.path.exists(exe), "examples are built by python -m paper_2504_14966_b200.build"
+    out = subprocess.run([exe, "1200", "2"], capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert out.stdout.count("PASS") == 3 and "FAIL" not in out.stdout
