@@ -156,3 +156,20 @@ def test_short_queue_budget_stops_early():
     assert r.stats.kernel_ms < 0.2 + 0.1
     assert r.best.schedule.is_partition_of(w.ids(), 4)
     assert r.best.g >= max(r.stats.g_sorted_start, r.stats.g_input_start)
+
+
+def test_short_queue_over_device_groups():
+    """K5 behind the multi-device paths: a device list (two contexts on GPU 0, peer exchange) and a
+    rank context with an NCCL communicator return the one-context schedule."""
+    c = S.table_coefficients()
+    w = _three_class(14, 8)
+    base = dict(seed=4, chains=777, t0=300.0, iter=30, scale_ladder=(1.0, 1e2, 1e4))
+    one = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, device=0), 4)
+    two = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, devices=(0, 0)), 4)
+    assert two.best.schedule.batches == one.best.schedule.batches and two.best.g == one.best.g
+    assert two.stats.best_chain == one.stats.best_chain and two.stats.proposals == one.stats.proposals
+    e = E.Engine(0)
+    e.comm_init(1, 0, E.comm_unique_id())
+    got = S.anneal(w, w.ids(), c, S.AnnealConfig(**base, comm_ctx=e.handle, device=0, chain_begin=0, chain_end=-1), 4)
+    assert got.best.schedule.batches == one.best.schedule.batches and got.stats.exchange_ms > 0.0
+    e.close()
