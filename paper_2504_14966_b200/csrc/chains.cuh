@@ -799,12 +799,17 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                 if ((it & (kRows - 1)) == 0) {  // lane j draws the row of proposal prop + j
                     const uint32_t prop0 = (uint32_t)(lev * p.iter + it);
                     __syncwarp();                // every lane is done reading the previous rows
-                    if (lane < kRows) {
-                        // Philox block b of a row = counter (proposal, chain, b, tag)
-                        uint32_t* dst = rnd + rnd_stride<UPL>() * lane;
+                    {
+                        // Philox block b of a row = counter (proposal, chain, b, tag); with 16 rows
+                        // per refill the lane pair splits a row's blocks (3 + 2): every lane works
+                        constexpr int kSplit = kRows == 32 ? kRndBlocks : (kRndBlocks + 1) / 2;
+                        const int row = lane & (kRows - 1);
+                        const int b0 = kRows == 32 || lane < kRows ? 0 : kSplit;
+                        const int b1 = kRows == 32 || lane >= kRows ? kRndBlocks : kSplit;
+                        uint32_t* dst = rnd + rnd_stride<UPL>() * row;
 #pragma unroll kPhiloxUnroll
-                        for (int b = 0; b < kRndBlocks; ++b) {
-                            uint32_t r[4] = {prop0 + (uint32_t)lane, cid, (uint32_t)b, kTagMove};
+                        for (int b = b0; b < b1; ++b) {
+                            uint32_t r[4] = {prop0 + (uint32_t)row, cid, (uint32_t)b, kTagMove};
                             philox_rounds<SLO_PHILOX_ROUNDS>(r, p.key0, p.key1);
                             if constexpr (rnd_stride<UPL>() % 4 == 0) {
                                 reinterpret_cast<uint4*>(dst)[b] = make_uint4(r[0], r[1], r[2], r[3]);
