@@ -34,11 +34,11 @@
 #define SLO_CHAIN_THREADS2 768  // 20-word rows let 25 warps fit; 24 balance 16384 chains better (8.8e9 vs 6.1e9)
 #endif
 #ifndef SLO_CHAIN_THREADS4
-#define SLO_CHAIN_THREADS4 512
+#define SLO_CHAIN_THREADS4 448  // 14 warps: the 64 KiB tick table keeps more L1 beside their slots (512: -3 %)
 #endif
 // block-size bound per units-per-lane (N <= 1024 / 2048 / 4096): more resident warps hide the
 // dependent-latency stalls until registers spill (measured with tools/prof_chains.py --bench:
-// UPL 2 896 > 768 > 640 > 512, UPL 4 512 > 608 > 576). 16384 chains over 148 x 28 warps is 3.95
+// UPL 2 896 > 768 > 640 > 512, UPL 4 448 > 512 ~ 384 > 416). 16384 chains over 148 x 28 warps is 3.95
 // chains per warp, so 896 also balances; 832 and 960 leave a fifth/fourth round partly empty.
 template <int UPL>
 __host__ __device__ constexpr int chain_threads() {
