@@ -10,7 +10,10 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
+#include <condition_variable>
 #include <cstring>
+#include <deque>
+#include <functional>
 #include <exception>
 #include <future>
 #include <limits>
@@ -733,6 +736,119 @@ private:
 
 }  // namespace
 
+namespace {
+// Host worker threads shared by every anneal() call (its table build, the deadline-first variants,
+// the table upload): spawning threads per call cost ~20-40 us each on the decision's critical path.
+// A TaskGroup waits for its tasks in wait() and in its destructor (an early return or an exception
+// never leaves a task running on the caller's stack); a waiting thread runs queued tasks itself, so
+// nested groups cannot starve the pool.
+class HostPool {
+public:
+    static HostPool& get() {
+        static HostPool p(std::max(2u, std::min(8u, std::thread::hardware_concurrency())));
+        return p;
+    }
+    void submit(std::function<void()> f) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            q_.push_back(std::move(f));
+        }
+        cv_.notify_one();
+    }
+    bool try_run_one() {
+        std::function<void()> f;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            if (q_.empty()) return false;
+            f = std::move(q_.front());
+            q_.pop_front();
+        }
+        f();
+        return true;
+    }
+    ~HostPool() {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            stop_ = true;
+        }
+        cv_.notify_all();
+        for (auto& t : th_) t.join();
+    }
+
+private:
+    explicit HostPool(unsigned n) {
+        for (unsigned i = 0; i < n; ++i)
+            th_.emplace_back([this] {
+                while (true) {
+                    std::function<void()> f;
+                    {
+                        std::unique_lock<std::mutex> l(mu_);
+                        cv_.wait(l, [&] { return stop_ || !q_.empty(); });
+                        if (q_.empty()) return;
+                        f = std::move(q_.front());
+                        q_.pop_front();
+                    }
+                    f();
+                }
+            });
+    }
+    std::vector<std::thread> th_;
+    std::deque<std::function<void()>> q_;
+    std::mutex mu_;
+    std::condition_variable cv_;
+    bool stop_ = false;
+};
+
+class TaskGroup {
+public:
+    template <typename F>
+    void run(F&& f) {
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            ++pending_;
+        }
+        HostPool::get().submit([this, fn = std::forward<F>(f)]() mutable {
+            std::exception_ptr e;
+            try {
+                fn();
+            } catch (...) {
+                e = std::current_exception();
+            }
+            std::lock_guard<std::mutex> g(mu_);
+            if (e && !err_) err_ = e;
+            if (--pending_ == 0) cv_.notify_all();
+        });
+    }
+    void wait() {
+        drain();
+        std::exception_ptr e;
+        {
+            std::lock_guard<std::mutex> g(mu_);
+            std::swap(e, err_);
+        }
+        if (e) std::rethrow_exception(e);
+    }
+    ~TaskGroup() { drain(); }
+
+private:
+    void drain() {
+        while (true) {
+            {
+                std::lock_guard<std::mutex> g(mu_);
+                if (pending_ == 0) return;
+            }
+            if (HostPool::get().try_run_one()) continue;
+            std::unique_lock<std::mutex> l(mu_);
+            cv_.wait_for(l, std::chrono::microseconds(50), [&] { return pending_ == 0; });
+        }
+    }
+    std::mutex mu_;
+    std::condition_variable cv_;
+    int pending_ = 0;
+    std::exception_ptr err_;
+};
+}  // namespace
+
 void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCoefficients& c, int max_batch,
                  std::vector<double>& exec, std::vector<double>& deadline) {
     std::vector<int> sorted_ids = ids;
@@ -764,10 +880,10 @@ void cost_tables(const Workload& w, const std::vector<int>& ids, const LatencyCo
     };
     // large queues: the rows are independent, fill them on up to 4 threads
     const int parts = static_cast<int>(std::min<std::size_t>(4, (std::size_t)n * max_batch / 2048 + 1));
-    std::vector<std::future<void>> rest;
-    for (int k = 1; k < parts; ++k) rest.push_back(std::async(std::launch::async, fill, n * k / parts, n * (k + 1) / parts));
+    TaskGroup rest;
+    for (int k = 1; k < parts; ++k) rest.run([&fill, k, n, parts] { fill(n * k / parts, n * (k + 1) / parts); });
     fill(0, n / parts);
-    for (auto& f : rest) f.get();
+    rest.wait();
     // No batch can start later than the sum of every request's largest exec (a makespan is at
     // most the sum of its members'). A deadline at or beyond that bound is met in every schedule:
     // store +inf, which leaves every exact compare unchanged and lets the chain kernel count such
@@ -906,10 +1022,10 @@ double best_deadline_first(int n, int mb, const std::vector<double>& exec, const
         deadline_first_dense(n, mb, exec, deadline, v, exec_order, cand[v].perm, cand[v].sizes);
         cand[v].g = dense_score(n, exec, deadline, cand[v].perm, cand[v].sizes);
     };
-    std::vector<std::future<void>> others;
-    for (int v = 1; v < kDeadlineVariants; ++v) others.push_back(std::async(std::launch::async, build, v));
+    TaskGroup others;
+    for (int v = 1; v < kDeadlineVariants; ++v) others.run([&build, v] { build(v); });
     build(0);
-    for (auto& f : others) f.get();
+    others.wait();
     int best = 0;
     for (int v = 1; v < kDeadlineVariants; ++v)
         if (cand[v].g > cand[best].g) best = v;
@@ -964,15 +1080,17 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
             if (std::uncaught_exceptions() > pending) e.abandon(n);
         }
     } abandon_on_throw{eng, n};
-    auto tables = std::async(std::launch::async, [&] {
+    TaskGroup tables;
+    tables.run([&] {
         cost_tables(w, ids, c, max_batch, exec, deadline);
         // the upload (context, tables, device-side tick tables) overlaps the deadline-first start
-        auto upload = std::async(std::launch::async, [&] {
+        TaskGroup upload;
+        upload.run([&] {
             if (n >= 1 && n <= SLO_MAX_N && max_batch <= SLO_MAX_MB)
                 eng.problem_set(n, max_batch, exec.data(), deadline.data());
         });
         if (want_dl) g_dl = best_deadline_first(n, max_batch, exec, deadline, dl_perm, dl_sizes);
-        upload.get();
+        upload.wait();
     });
     auto [sorted_s, input_s] = initial_candidates(w, ids, c, max_batch);
     EvaluatedSchedule ev_sorted = evaluate(sorted_s, c, w);
@@ -989,7 +1107,7 @@ AnnealResult anneal(const Workload& w, const std::vector<int>& ids, const Latenc
     // test folded into a per-(batch size, request) deadline
     if (n > SLO_MAX_N) throw CapacityError("anneal: " + std::to_string(n) + " requests exceed the engine limit of 4096");
     if (max_batch > SLO_MAX_MB) throw CapacityError("anneal: max_batch above the engine limit of 16");
-    tables.get();
+    tables.wait();
     const bool use_sorted = ev_sorted.g >= ev_input.g;
     const Schedule& start = use_sorted ? sorted_s : input_s;
     std::vector<int> start_perm, start_sizes;

@@ -17,7 +17,7 @@ static double ms(clk::time_point a, clk::time_point b) { return std::chrono::dur
 
 int main() {
     const LatencyCoefficients c = table_coefficients();
-    for (int n : {6, 32, 1024}) {
+    for (int n : {6, 32, 1024, 4096}) {
         auto [code, chat] = default_synth_classes();
         std::vector<Request> reqs = generate_mixed(n, 1, code, chat);
         for (auto& r : reqs) r.predicted_output_len = r.true_output_len;  // (predictions do not matter here)
