@@ -5,12 +5,12 @@
 // (the reference's 8 + 1 attempt discipline, P:src/priority_mapper.cpp:184-198), the same tick
 // objective with the SLO count certified against the reference's fp64 arithmetic and the same
 // Metropolis test -- so a K5 chain follows K3's trajectory proposal for proposal and the winner
-// is bit-identical (tests/test_gpu_parity.py::test_short_queue_kernel_matches_k3).
+// is bit-identical (tests/test_short_queue.py: against the sequential model and against K3).
 //
 // What changes is the shape. At n <= 32 a schedule is one warp row: lane q holds the request at
 // position q (a register), the batch ends are one warp-uniform mask. K3's machinery for long
 // schedules -- shared-memory entries, unit anchors, the speculative rejection stage, cached
-// slacks -- costs ~720 warp instructions per proposal at n = 6 (ncu, profiles/r2), because an
+// slacks -- costs ~720 warp instructions per proposal at n = 6 (ncu; K5: 291), because an
 // online window's short queue at high temperature accepts a quarter of its proposals and most
 // moves are squeezes/delays that skip the speculative stage. K5 instead decodes the nine
 // attempts on nine lanes at once, applies the move as one shuffle (rotation or exchange) plus a
@@ -20,7 +20,7 @@
 // does (stride 20 words).
 
 constexpr int kSmallMaxN = 32;
-constexpr int kSmallThreads = 768;  // 24 warps (85 registers; 1024 threads cap them at 64, 512 park chains under an SM share)
+constexpr int kSmallThreads = 768;  // 24 warps (70 registers; 1024 threads cap them at 64, 512 park chains under an SM share)
 
 struct SmallScore {
     long long tot;  // total latency (ticks)
