@@ -6,8 +6,9 @@
 // score is the reference's sequential arithmetic (:259-279). The score is incremental yet exact:
 // the sequential running state (total, n_met, elapsed) is cached every 16 positions, so a
 // proposal restarts the exact left-to-right pass just before the first position it changed.
-// The (exec, deadline) pairs and batch makespans of the suffix are computed by all lanes into
-// shared memory first; lane 0 then runs the two dependence chains from shared memory.
+// The (exec, deadline) pairs and batch makespans of every position stay staged in shared memory;
+// a move restages only the (at most 32) positions of the batches it rebuilds, lane-parallel, and
+// undoes them on rejection; lane 0 then runs the two dependence chains from shared memory.
 
 struct ReplayParams {
     int n, mb, chains;
@@ -146,7 +147,6 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
     double* trail = reinterpret_cast<double*>(base + replay_trail_off(npad));
     double2* c_te = reinterpret_cast<double2*>(base + replay_cache_off(npad));  // {total, elapsed}
     int* c_nmet = reinterpret_cast<int*>(c_te + npad / 16 + 1);
-    const double2* dl2 = reinterpret_cast<const double2*>(dl);
     for (int i = lane; i < npad; i += 32) ent[i] = p.start_ent[i];
     for (int i = lane; i < words; i += 32) bits[i] = p.start_bits[i];
     if (lane == 0) c_te[0] = make_double2(0.0, 0.0), c_nmet[0] = 0;
@@ -158,8 +158,9 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
     // from s0, the start of r's batch; the dependence chains run on lane 0 with the
     // reference's arithmetic per position: met += elapsed <= deadline, total += elapsed + exec,
     // and elapsed += makespan at a batch end (elsewhere += 0.0, an exact no-op).
-    auto score_from = [&](int r, double& total_out, int& nmet_out) -> double {
-        const int s0 = prev_end(bits, r) + 1;
+    // {exec, makespan increment} and deadline of every position from s0 (the start of a batch):
+    // the whole schedule once; afterwards a move restages only the batches it rebuilds
+    auto stage_from = [&](int s0) {
         const int nw = (n - s0 + 31) >> 5;
         // windows of 32 are independent: a segmented max-scan over the lanes; a batch crossing
         // into window w takes window w-1's trailing partial max in the fix-up (batches <= 16)
@@ -194,6 +195,8 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
             }
         }
         __syncwarp();
+    };
+    auto score_from = [&](int r, double& total_out, int& nmet_out) -> double {
         double total = 0.0;
         int nm = 0;
         if (lane == 0) {
@@ -201,38 +204,19 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
             total = st.x;
             double el = st.y;
             nm = c_nmet[r >> 4];
-            // 16-position blocks, double-buffered: the next block's operands load while this
-            // block's chains run (8-cycle DADD latency is the floor); one cache entry per block
-            auto load16 = [&](double2 (&u)[16], double2 (&d)[8], int q0) {
-#pragma unroll
-                for (int j = 0; j < 16; ++j) u[j] = xa[q0 + j];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) d[j] = dl2[(q0 >> 1) + j];
-            };
-            auto run16 = [&](const double2 (&u)[16], const double2 (&d)[8], int q0) {
-                c_te[q0 >> 4] = make_double2(total, el), c_nmet[q0 >> 4] = nm;
+            // 16-position blocks, one cache entry each; the operands are read from shared memory
+            // inside the unrolled block (tools/probes/chain_loop.cu: 13.4 cycles per position,
+            // where double-buffering 16 positions in registers measured 15.3 and cost the kernel
+            // its registers)
+            int q = r;
+            for (; q + 16 <= n; q += 16) {
+                c_te[q >> 4] = make_double2(total, el), c_nmet[q >> 4] = nm;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    nm += el <= ((j & 1) ? d[j >> 1].y : d[j >> 1].x);
-                    total += el + u[j].x;
-                    el += u[j].y;
-                }
-            };
-            int q = r;
-            if (q + 16 <= n) {
-                double2 A[16], B[16], DA[8], DB[8];
-                load16(A, DA, q);
-                while (true) {
-                    const bool more = q + 32 <= n;
-                    if (more) load16(B, DB, q + 16);
-                    run16(A, DA, q);
-                    q += 16;
-                    if (!more) break;
-                    const bool more2 = q + 32 <= n;
-                    if (more2) load16(A, DA, q + 16);
-                    run16(B, DB, q);
-                    q += 16;
-                    if (!more2) break;
+                    const double2 v = xa[q + j];
+                    nm += el <= dl[q + j];
+                    total += el + v.x;
+                    el += v.y;
                 }
             }
             if (q < n) {
@@ -254,6 +238,7 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
 
     double tot0;
     int nm0;
+    stage_from(0);
     double f = score_from(0, tot0, nm0);
     int valid_end = n;  // block caches are valid at every boundary <= valid_end
     double best_f = f, best_t = tot0;
@@ -306,8 +291,43 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
                 __syncwarp();
                 lo_pos = min(mv.a, mv.b);
             }
-            // restart at the start of the batch holding the first changed position (or earlier
-            // if the caches were invalidated by a rejected proposal)
+            // restage the rebuilt batches (<= 32 positions, one per lane): exec, deadline and the
+            // makespan increment at each batch end (the reference's max from 0.0, :267-273)
+            int qs = -1, grp = 0;
+            if (mv.kind == 1) {
+                if (mv.lo + lane <= mv.hi) qs = mv.lo + lane, grp = qs <= mv.split ? 0 : 1;
+            } else if (mv.kind == 2) {
+                const int pa = min(mv.a, mv.b), pb = max(mv.a, mv.b);
+                const int sa = prev_end(bits, pa) + 1, sb = prev_end(bits, pb) + 1;
+                const int ea = next_end(bits, pa), eb = next_end(bits, pb);
+                if (lane < 16) {
+                    if (sa + lane <= ea) qs = sa + lane;
+                } else if (sb != sa && sb + lane - 16 <= eb) {
+                    qs = sb + lane - 16, grp = 1;
+                }
+            }
+            double2 old_xa = make_double2(0.0, 0.0);
+            double old_dl = 0.0;
+            if (mv.kind) {
+                double x = 0.0, d = 0.0;
+                if (qs >= 0) {
+                    const double2 v = __ldg(&p.tab[ent[qs]]);
+                    x = v.x, d = v.y;
+                    old_xa = xa[qs], old_dl = dl[qs];
+                }
+                double m0 = qs >= 0 && grp == 0 ? x : -INFINITY, m1 = qs >= 0 && grp == 1 ? x : -INFINITY;
+#pragma unroll
+                for (int o = 16; o; o >>= 1) {
+                    m0 = dmax(m0, __shfl_xor_sync(FULL, m0, o));
+                    m1 = dmax(m1, __shfl_xor_sync(FULL, m1, o));
+                }
+                if (qs >= 0) {
+                    const bool end = (bits[qs >> 5] >> (qs & 31)) & 1u;
+                    xa[qs] = make_double2(x, end ? dmax(0.0, grp ? m1 : m0) : 0.0);
+                    dl[qs] = d;
+                }
+                __syncwarp();
+            }
             // restart at the last cached block boundary before the first changed position (or
             // earlier if a rejected proposal left the later caches stale)
             const int r0 = min(lo_pos, valid_end) & ~15;
@@ -331,6 +351,7 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
                     for (int i = lane; i < words; i += 32) p.best_bits[(size_t)c * words + i] = bits[i];
                 }
             } else if (mv.kind) {
+                if (qs >= 0) xa[qs] = old_xa, dl[qs] = old_dl;
                 if (mv.kind == 1) {
                     if (q <= mv.hi) ent[q] = old_q;
                     if (lane == 0) bits[w1] = ow1, bits[w0] = ow0;
