@@ -152,6 +152,22 @@ def test_replay_matches_oracle_many_seeds(port, n, mb):
         assert (res.stats.proposals, res.stats.accepted) == (o["proposals"], o["accepted"])
 
 
+@pytest.mark.parametrize("n,mb", [(200, 8), (150, 16), (1024, 4), (61, 16)])
+def test_replay_long_batches_and_full_size(port, n, mb):
+    """K2's staged operands across long batches (a swap restages two 16-position batches, a squeeze
+    or delay up to 32 positions) and at the headline size: the reference walk, bit for bit."""
+    c = S.table_coefficients()
+    w = _three_class(n, 5 + n)
+    fw = _flat(w)
+    cfg = {"t0": 100.0, "iter": 40} if n >= 1024 else {}
+    for seed in (0, 1, 2):
+        res = S.anneal(w, w.ids(), c, _replay_cfg(seed, **cfg), mb)
+        o = port.anneal(fw, TABLE_COEFFS, w.ids(), mb, seed=seed, **cfg)
+        assert res.best.schedule.batches == o["batches"], (n, mb, seed)
+        assert (res.best.n, res.best.t_ms, res.best.g) == (o["n"], o["t"], o["g"])
+        assert (res.stats.proposals, res.stats.accepted) == (o["proposals"], o["accepted"])
+
+
 def test_replay_many_chains_in_one_launch(eng, port):
     """K2 with C chains: chain c reproduces the reference walk with seed + c."""
     n, mb = 48, 4
