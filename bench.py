@@ -445,7 +445,9 @@ def run_ours(args):
         "wall_s_timed": wall_s,
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "ms_per_call": 1e3 * e2e_s / args.e2e_steps, "api": "slosched_anneal (include/slosched_api.h)"},
-        "gpu_launches": 3 * args.steps,  # per step: k_start (prologue), k_chains, k_argmax
+        # per step: k_start (prologue), k_chains, k_argmax; with a communicator also k_pack and k_pick
+        # around the NCCL all-gather
+        "gpu_launches": (5 if comm else 3) * args.steps,
         "roofline": roof,
         "clocks": clocks.summary(),
         "cpu_baseline": cpu,
