@@ -248,8 +248,14 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
     XoshiroW rng(p.seed + (uint64_t)c);
     unsigned long long props = 0, accs = 0;
     int levels = 0;
+#ifdef SLO_K2_TIMING
+    long long t_score = 0, t_pre = 0;  // cycles: score_from / propose + apply + restage
+#endif
     for (double t = p.t0; t >= p.t_thres; t *= p.tau, ++levels) {
         for (int k = 0; k < p.iter; ++k) {
+#ifdef SLO_K2_TIMING
+            const long long tk0 = clock64();
+#endif
             const Move mv = replay_propose(ent, bits, n, mb, p.magic, rng);
             // apply in place (identical to the chain kernel), remember how to undo
             int q = 0, lo_pos = n;
@@ -333,7 +339,14 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
             const int r0 = min(lo_pos, valid_end) & ~15;
             double tot;
             int nm;
+#ifdef SLO_K2_TIMING
+            const long long tk1 = clock64();
+#endif
             const double f_new = mv.kind ? score_from(r0, tot, nm) : (tot = 0.0, nm = 0, f);
+#ifdef SLO_K2_TIMING
+            const long long tk2 = clock64();
+            t_score += tk2 - tk1, t_pre += tk1 - tk0;
+#endif
             ++props;
             bool accept = f_new > f;  // :385-391
             if (!accept) {
@@ -367,6 +380,9 @@ __global__ void __launch_bounds__(128) k_replay(const ReplayParams p) {
         ChainRec r;
         r.g = best_f, r.t = best_t, r.cur_f = f, r.n_met = best_n, r.levels = levels;
         r.proposals = props, r.accepted = accs, r.scan1 = 0, r.scan2 = 0;
+#ifdef SLO_K2_TIMING
+        r.scan1 = (unsigned long long)t_score, r.scan2 = (unsigned long long)t_pre;  // diagnostics
+#endif
         p.rec[c] = r;
     }
 }
