@@ -1,3 +1,5 @@
+"""Short-queue chain throughput vs chain count, iterations per level and SM share (n = 6, 16, 48):
+kernel time, proposals, proposals/s and acceptance per configuration."""
 import sys, time
 sys.path.insert(0, '.')
 import paper_2504_14966_b200 as S
