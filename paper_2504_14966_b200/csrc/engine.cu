@@ -76,19 +76,15 @@ constexpr int kPhiloxRoundsUnroll = SLO_PHILOX_ROUNDS_UNROLL;
 #ifndef SLO_PHILOX_ROUNDS
 #define SLO_PHILOX_ROUNDS 10
 #endif
+// One round = two 32x32->64 products: written as one wide multiply each (IMAD.WIDE.U32: both
+// halves from one instruction) instead of __umulhi + a low multiply (IMAD.HI + IMAD).
 template <int R = 10>
 __host__ __device__ __forceinline__ void philox_rounds(uint32_t c[4], uint32_t k0, uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-#if defined(__CUDA_ARCH__)
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), hi1 = __umulhi(0xCD9E8D57u, c[2]);
-#else
-        const uint32_t hi0 = (uint32_t)(((uint64_t)0xD2511F53u * c[0]) >> 32);
-        const uint32_t hi1 = (uint32_t)(((uint64_t)0xCD9E8D57u * c[2]) >> 32);
-#endif
-        const uint32_t lo0 = 0xD2511F53u * c[0], lo1 = 0xCD9E8D57u * c[2];
-        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-        c[0] = n0, c[1] = lo1, c[2] = n2, c[3] = lo0;
+        const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
+        const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
+        c[0] = n0, c[1] = (uint32_t)p1, c[2] = n2, c[3] = (uint32_t)p0;
         k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
     }
 }
