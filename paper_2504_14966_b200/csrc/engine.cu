@@ -69,10 +69,6 @@ __device__ __forceinline__ uint64_t gtimer() {
 }
 
 // Philox4x32-10, Random123 constants.
-#ifndef SLO_PHILOX_ROUNDS_UNROLL
-#define SLO_PHILOX_ROUNDS_UNROLL 10
-#endif
-constexpr int kPhiloxRoundsUnroll = SLO_PHILOX_ROUNDS_UNROLL;
 #ifndef SLO_PHILOX_ROUNDS
 #define SLO_PHILOX_ROUNDS 10
 #endif
@@ -85,21 +81,6 @@ __host__ __device__ __forceinline__ void philox_rounds(uint32_t c[4], uint32_t k
         const uint64_t p0 = (uint64_t)0xD2511F53u * c[0], p1 = (uint64_t)0xCD9E8D57u * c[2];
         const uint32_t n0 = (uint32_t)(p1 >> 32) ^ c[1] ^ k0, n2 = (uint32_t)(p0 >> 32) ^ c[3] ^ k1;
         c[0] = n0, c[1] = (uint32_t)p1, c[2] = n2, c[3] = (uint32_t)p0;
-        k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
-    }
-}
-__host__ __device__ __forceinline__ void philox10(uint32_t c[4], uint32_t k0, uint32_t k1) {
-#pragma unroll kPhiloxRoundsUnroll
-    for (int r = 0; r < 10; ++r) {
-#if defined(__CUDA_ARCH__)
-        const uint32_t hi0 = __umulhi(0xD2511F53u, c[0]), hi1 = __umulhi(0xCD9E8D57u, c[2]);
-#else
-        const uint32_t hi0 = (uint32_t)(((uint64_t)0xD2511F53u * c[0]) >> 32);
-        const uint32_t hi1 = (uint32_t)(((uint64_t)0xCD9E8D57u * c[2]) >> 32);
-#endif
-        const uint32_t lo0 = 0xD2511F53u * c[0], lo1 = 0xCD9E8D57u * c[2];
-        const uint32_t n0 = hi1 ^ c[1] ^ k0, n2 = hi0 ^ c[3] ^ k1;
-        c[0] = n0, c[1] = lo1, c[2] = n2, c[3] = lo0;
         k0 += 0x9E3779B9u, k1 += 0xBB67AE85u;
     }
 }
@@ -366,7 +347,7 @@ const char* slo_version(void) { return "slosched_b200 engine 0.1 (sm_100a)"; }
 
 void slo_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
     uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
-    philox10(c, key[0], key[1]);
+    philox_rounds<10>(c, key[0], key[1]);
     for (int i = 0; i < 4; ++i) out[i] = c[i];
 }
 
