@@ -924,37 +924,64 @@ void deadline_first_dense(int n, int mb, const std::vector<double>& exec, const 
     const std::vector<int> order = order_by_key(due);  // ascending due, ties by index
     auto by_exec = [&](int a, int b) { return ef[a] != ef[b] ? ef[a] < ef[b] : a < b; };
     std::vector<int> kept;
-    std::vector<double> start;  // start time of kept batch k (valid for batches before `dirty`)
-    start.push_back(0.0);
-    // re-time batches from batch k0 on; false if a kept request starts after its latest start
-    // (check: stop there, leaving later start times stale)
-    auto retime = [&](int k0, bool check) {
+    kept.reserve(n);
+    // start[k] = start time of kept batch k, valid for k <= `valid` (it depends on batches < k only);
+    // later entries are recomputed when a check first needs them (no eager re-time after a drop)
+    std::vector<double> start((std::size_t)n + 2, 0.0);
+    int valid = 0;
+    // the kept requests' full-batch (exec, latest start), in kept order: full batches read them
+    // contiguously (the trailing partial batch gathers its own size's tables)
+    std::vector<double> ke, kd;
+    ke.reserve(n), kd.reserve(n);
+    auto batch = [&](int k, double& mk) {  // latest-start test of batch k at start[k]; mk = its makespan
         const int m = static_cast<int>(kept.size());
-        const int nb = (m + mb - 1) / mb;
-        start.resize(nb + 1);
+        const int b0 = k * mb, sz = std::min(mb, m - b0);
+        const double s0 = start[k];
         bool ok = true;
-        for (int k = k0; k < nb; ++k) {
-            const int b0 = k * mb, sz = std::min(mb, m - b0);
-            const double* e = exec.data() + (std::size_t)(sz - 1) * n;
-            const double* d = deadline.data() + (std::size_t)(sz - 1) * n;
-            double mk = 0.0;
+        mk = 0.0;
+        if (sz == mb) {
             for (int j = b0; j < b0 + sz; ++j) {
-                ok = ok && start[k] <= d[kept[j]];
-                mk = std::max(mk, e[kept[j]]);
+                ok = ok && s0 <= kd[j];
+                mk = std::max(mk, ke[j]);
             }
-            if (check && !ok) return false;
-            start[k + 1] = start[k] + mk;
+            return ok;
+        }
+        const double* e = exec.data() + (std::size_t)(sz - 1) * n;
+        const double* d = deadline.data() + (std::size_t)(sz - 1) * n;
+        for (int j = b0; j < b0 + sz; ++j) {
+            ok = ok && s0 <= d[kept[j]];
+            mk = std::max(mk, e[kept[j]]);
         }
         return ok;
+    };
+    // every kept request of batches k0.. starts by its latest start (stops at the first that does not)
+    auto check_from = [&](int k0) {
+        double mk;
+        for (; valid < k0; ++valid) {  // batches before k0: times only
+            batch(valid, mk);
+            start[valid + 1] = start[valid] + mk;
+        }
+        const int nb = (static_cast<int>(kept.size()) + mb - 1) / mb;
+        for (int k = k0; k < nb; ++k) {
+            if (!batch(k, mk)) {
+                valid = k;
+                return false;
+            }
+            start[k + 1] = start[k] + mk;
+        }
+        valid = nb;
+        return true;
     };
     for (int i : order) {
         if (!(df[i] >= 0.0)) continue;  // cannot start in time even first (in a full batch)
         const auto it = std::lower_bound(kept.begin(), kept.end(), i, by_exec);
         const int p = static_cast<int>(it - kept.begin());
         kept.insert(it, i);
-        if (!retime(p / mb, true)) {  // Moore-Hodgson: drop the longest kept request
-            kept.pop_back();
-            retime(std::min(p, static_cast<int>(kept.size())) / mb, false);
+        ke.insert(ke.begin() + p, ef[i]), kd.insert(kd.begin() + p, df[i]);
+        valid = std::min(valid, p / mb);  // batches from p / mb on changed
+        if (!check_from(p / mb)) {  // Moore-Hodgson: drop the longest kept request
+            kept.pop_back(), ke.pop_back(), kd.pop_back();
+            valid = std::min(valid, std::min(p, static_cast<int>(kept.size())) / mb);
         }
     }
     std::vector<char> in(n, 0);

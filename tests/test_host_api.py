@@ -214,6 +214,20 @@ def test_deadline_first_candidate():
     assert ev_dl.n >= 74 and ev_dl.n > ev_sorted.n and ev_dl.g > ev_sorted.g
 
 
+def test_deadline_first_candidate_is_stable():
+    """The deadline-first start seeds every chain, so its output is part of the K3 trajectories:
+    pinned (sha256 of the batches) across host-side rewrites of the admission loop."""
+    import hashlib
+    c = S.table_coefficients()
+    h = hashlib.sha256()
+    for n in (5, 37, 256, 1024):
+        for seed in (0, 1):
+            w = S.generate_mixed(n, seed)
+            for mb in (1, 4, 8):
+                h.update(repr(S.deadline_first_candidate(w, w.ids(), c, mb).batches).encode())
+    assert h.hexdigest() == "5f97608dae55a47f831bd1a9fac3033712984cf2fec6b586558384cbc3949d57"
+
+
 def test_k3_model_philox_and_tick_objective():
     """The K3 model used by the GPU trajectory tests (tests/k3_model.py): its Philox matches the
     Random123 known answers; its SLO count is exactly CostModel::score's and its total latency
