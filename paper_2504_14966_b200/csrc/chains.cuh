@@ -739,10 +739,13 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     if (kk == cnt % UPL) ed = cur.E[kk];
                 e_dead = cnt < 32 * UPL ? __shfl_sync(FULL, ed, (cnt / UPL) & 31) : kPadE;
             };
+            // the live caches hold units [0, rf_nu); accepted moves since the last refresh rebuilt
+            // units [rf_lo, rf_hi] (contents or batch structure); units after them only shifted
+            int rf_lo = 0, rf_hi = 1 << 20, rf_nu = 0;
             auto refresh_sig = [&]() {
                 __syncwarp();
                 const int nu = min(u_live, kLiveCap);
-                for (int u = 0; u < nu; ++u) {  // unit u: register u % UPL of lane u / UPL
+                for (int u = min(rf_lo, rf_nu); u < nu; ++u) {  // unit u: register u % UPL of lane u / UPL
                     long long Es = cur.E[0];
                     uint32_t Fs_ = cur.F[0];
 #pragma unroll
@@ -751,6 +754,23 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     const long long Eu = __shfl_sync(FULL, Es, u / UPL);
                     const uint32_t Fu = __shfl_sync(FULL, Fs_, u / UPL);
                     const int q = (u << 5) + lane;
+                    if (u > rf_hi && u < rf_nu) {
+                        // same contents and batches, every batch start and the anchor moved by the
+                        // same shift: bst stands, each slack moves by it (re-read where it was clamped)
+                        const long long dE = Eu - cE[u];
+                        if (dE != 0) {
+                            const int sg = sig[q];
+                            if (sg != INT_MIN) {
+                                const long long sl = (sg == INT_MAX || sg == INT_MIN + 1)
+                                                         ? __ldg(p.dt + ent[q]) - (Eu + (long long)bst[q])
+                                                         : (long long)sg - dE;
+                                sig[q] = (int)max(min(sl, (long long)INT_MAX), (long long)INT_MIN + 1);
+                            }
+                            __syncwarp();
+                            if (lane == 0) cE[u] = Eu;
+                        }
+                        continue;
+                    }
                     const uint32_t w = bits[u];
                     uint32_t x = 0;
                     long long D = 0;
@@ -775,6 +795,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     bst[q] = sc - vv;
                     if (lane == 0) cE[u] = Eu;
                 }
+                rf_lo = 1 << 20, rf_hi = -1, rf_nu = nu;
                 __syncwarp();
             };
             // the live-prefix summary and caches are refreshed at the start of the next speculative
@@ -1148,6 +1169,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                         da = (int)mN0 - (int)mO0, db = (int)mN1 - (int)mO1;
                         dtot = sN - sO + (long long)da * (n - 1 - ea) + (long long)db * (n - 1 - eb);
                         if (sa == sb) dtot = 0, dA = 0;  // one batch: order inside a batch changes nothing
+                        r_lo = sa, r_hi = eb;
                     }
                     // the swap is written to shared memory only when an SLO walk or an accept needs
                     // it (the common rejected swap never touches the state)
@@ -1212,6 +1234,7 @@ __global__ void __launch_bounds__(chain_threads<UPL>(), 1) k_chains(const ChainP
                     cur = nx, tot = tot_new, A = A_new, nm_cur = nm;
                     f = f_new;
                     need_refresh = true;
+                    if (kind != 0) rf_lo = min(rf_lo, r_lo >> 5), rf_hi = max(rf_hi, r_hi >> 5);
                     pass_end = 0;  // the state changed: later speculative scores are stale
                     if (f > best_f) {
                         best_f = f;
