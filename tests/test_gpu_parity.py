@@ -891,3 +891,53 @@ def test_chain_trajectory_random_shapes(eng):
         assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
                                                        sum(x["accepted"] for x in runs)), case
         assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"], case
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,mb,seed", [(64, 4, 1), (300, 4, 2), (1100, 4, 3), (2100, 2, 4)])
+def test_chain_trajectory_loose_deadlines(eng, n, mb, seed):
+    """Deadlines far beyond the exec scale (> 2^31 ticks: the cached slacks clamp to int32) mixed
+    with tight, +inf and never-met ones, at temperatures that accept often: the incremental
+    live-cache refresh (shifted units, clamped slacks re-read from the deadline table) keeps the
+    chains on the model's trajectories (one, two and four units per lane)."""
+    import k3_model as K
+    rs = np.random.default_rng(seed)
+    base = rs.uniform(2.0, 60.0, n)
+    ex = np.stack([base * (1.0 + 0.15 * b) for b in range(mb)])  # [mb][n], growing with batch size
+    mx = float(ex.max())
+    kind = rs.choice(4, n, p=[0.35, 0.4, 0.15, 0.1])
+    dl = np.empty_like(ex)
+    for i in range(n):
+        if kind[i] == 0:    # tight: met only near the head of the schedule
+            dl[:, i] = rs.uniform(0.0, 4.0 * mx)
+        elif kind[i] == 1:  # loose but finite: slack beyond 2^31 ticks near the head
+            dl[:, i] = rs.uniform(40.0, 90.0) * mx
+        elif kind[i] == 2:
+            dl[:, i] = np.inf
+        else:
+            dl[:, i] = -np.inf
+    eng.set_problem(ex, dl)
+    prob = K.TickProblem(ex, dl, eng.tick_ms)
+    assert (dl[np.isfinite(dl)].max() / eng.tick_ms) > 2.0 ** 31  # the clamp is reachable
+    perm = list(rs.permutation(n))
+    sizes = [mb] * (n // mb) + ([n % mb] if n % mb else [])
+    start, q = [], 0
+    for s in sizes:
+        start.append([int(x) for x in perm[q:q + s]])
+        q += s
+    f0 = prob.score(start)[2]
+    t0, tau, it, chains = 2000.0, 0.6, 24, 2
+    scale = t0 / f0 if f0 > 0 else t0
+    sd = int(rs.integers(1 << 40))
+    bp, bs, r = eng.anneal_chains([int(x) for x in perm], sizes, chains=chains, t0=t0, t_thres=20.0, tau=tau,
+                                  iter=it, seed=sd, objective_scale=scale)
+    runs = [K.run_chain(prob, start, cid, sd, t0, 20.0, tau, it, scale) for cid in range(chains)]
+    win = min(range(chains), key=lambda k: (-runs[k]["best"][2], runs[k]["best"][1], k))
+    got, q = [], 0
+    for s in bs:
+        got.append([int(x) for x in bp[q:q + s]])
+        q += s
+    assert sum(x["accepted"] for x in runs) > 0.2 * sum(x["proposals"] for x in runs)  # accepts often
+    assert (r.chain, r.proposals, r.accepted) == (win, sum(x["proposals"] for x in runs),
+                                                   sum(x["accepted"] for x in runs))
+    assert (r.n_met, r.t, r.g) == runs[win]["best"] and got == runs[win]["best_batches"]
